@@ -1,0 +1,996 @@
+// Host orchestration of the sm_100a Newton-step path and its C ABI
+// (include/ncl_b200.h).
+//
+//   LdlSystem  -- symbolic-once / numeric-per-call static-pivot LDL^T on the
+//                 device: factorize (sparse.cpp:182-256), ldl_solve
+//                 (sparse.cpp:258-276), solve_refined (sparse.cpp:278-322).
+//   KktSystem  -- KktContext (kkt.cpp:41-314): bit-exact refill, delta loop
+//                 with inertia control, rhs, refined solve, recovery.
+// One CUDA stream per context; host synchronisation points are exactly the
+// scalars the reference branches on (inertia / perturbed / ok per attempt,
+// residual norms per refinement step).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/ncl_b200.h"
+#include "kkt_plan.hpp"
+#include "launch.hpp"
+
+namespace nclb {
+
+namespace {
+
+thread_local std::string g_err;
+
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+#define CK(x)                                                                   \
+  do {                                                                          \
+    cudaError_t e_ = (x);                                                       \
+    if (e_ != cudaSuccess)                                                      \
+      throw ::nclb::CudaError(std::string(#x) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+template <class T>
+struct DBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  DBuf() = default;
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  ~DBuf() {
+    if (p) cudaFree(p);
+  }
+  void alloc(size_t k) {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = k;
+    if (k) CK(cudaMalloc(&p, k * sizeof(T)));
+  }
+  void upload(const std::vector<T>& v) {
+    alloc(v.size());
+    if (!v.empty()) CK(cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+  }
+  void zero(cudaStream_t st) {
+    if (n) CK(cudaMemsetAsync(p, 0, n * sizeof(T), st));
+  }
+};
+
+struct Scalars {
+  int stats[4];   // n_pos, n_neg, perturbed, fail
+  int nonfinite;
+  int pad;
+  double hmax;
+  double norm[4];  // [0] max|b| [1] residual
+};
+
+}  // namespace
+
+struct FactorInfo {
+  bool ok = false;
+  int n_pos = 0, n_neg = 0, perturbed = 0;
+};
+
+// ---------------------------------------------------------------------------
+class LdlSystem {
+ public:
+  LdlSystem(const LowerCsc& K, const Symbolic& S, cudaStream_t st)
+      : K_(K), S_(S), st_(st) {
+    sn_ = build_supernodal(K_, S_);
+    N_ = K_.n;
+    upload();
+  }
+
+  int n() const { return N_; }
+  const Symbolic& sym() const { return S_; }
+  const Supernodal& sn() const { return sn_; }
+  const LowerCsc& pattern() const { return K_; }
+  Scalars* host_scalars() { return hs_; }
+  Scalars* dev_scalars() { return ds_.p; }
+  cudaStream_t stream() const { return st_; }
+
+  ~LdlSystem() {
+    if (hs_) cudaFreeHost(hs_);
+  }
+
+  // numeric factorization of the values kval (device, lower-CSC slot order);
+  // the stats land in dev_scalars()->stats (not synchronised)
+  void factorize_async(const double* kval, double eps) {
+    CK(cudaMemsetAsync(ds_.p, 0, sizeof(int) * 4, st_));
+    FactorDev fd = factor_dev();
+    if (sn_.path_ptr.size() > 1) {
+      CK(cudaMemsetAsync(counter_.p, 0, sizeof(int), st_));
+      ++epoch_;
+      launch_factor_warp(sd_, fd, kval, flags_.p, epoch_, counter_.p, npaths(), eps,
+                         grid_, st_);
+    }
+    for (size_t l = 0; l + 1 < sn_.lvl_ptr.size(); ++l)
+      launch_factor_wide(sd_, fd, kval, lvl_nodes_.p + sn_.lvl_ptr[l],
+                         sn_.lvl_ptr[l + 1] - sn_.lvl_ptr[l], eps, st_);
+    CK(cudaGetLastError());
+  }
+
+  FactorInfo read_factor_info() {
+    CK(cudaMemcpyAsync(hs_, ds_.p, sizeof(Scalars), cudaMemcpyDeviceToHost, st_));
+    CK(cudaStreamSynchronize(st_));
+    FactorInfo fi;
+    fi.n_pos = hs_->stats[0];
+    fi.n_neg = hs_->stats[1];
+    fi.perturbed = hs_->stats[2];
+    fi.ok = hs_->stats[3] == 0;
+    return fi;
+  }
+
+  // x = P^T L^-T D^-1 L^-1 P b (device vectors, async)
+  void solve_async(const double* b, double* x) {
+    launch_permute_in(N_, perm_.p, b, wp_.p, st_);
+    if (npaths()) {
+      CK(cudaMemsetAsync(counter_.p, 0, sizeof(int), st_));
+      ++epoch_;
+      launch_fwd_warp(sd_, lval_.p, wp_.p, uvec_.p, flags_.p, epoch_, counter_.p, npaths(),
+                      grid_, st_);
+    }
+    const int nl = static_cast<int>(sn_.lvl_ptr.size()) - 1;
+    for (int l = 0; l < nl; ++l)
+      launch_fwd_wide(sd_, lval_.p, wp_.p, uvec_.p, lvl_nodes_.p + sn_.lvl_ptr[l],
+                      sn_.lvl_ptr[l + 1] - sn_.lvl_ptr[l], sn_.max_wide_f, st_);
+    for (int l = nl - 1; l >= 0; --l)
+      launch_bwd_wide(sd_, lval_.p, d_.p, wp_.p, xp_.p, lvl_nodes_.p + sn_.lvl_ptr[l],
+                      sn_.lvl_ptr[l + 1] - sn_.lvl_ptr[l], sn_.max_wide_f, st_);
+    if (npaths()) {
+      CK(cudaMemsetAsync(counter_.p, 0, sizeof(int), st_));
+      ++epoch_;
+      launch_bwd_warp(sd_, lval_.p, d_.p, wp_.p, xp_.p, flags_.p, epoch_, wide_.p,
+                      counter_.p, npaths(), grid_, st_);
+    }
+    launch_permute_out(N_, perm_.p, xp_.p, x, st_);
+    CK(cudaGetLastError());
+  }
+
+  // r = b - A x; norm slot (device) receives max|r| (must be zeroed by caller)
+  void residual_async(const double* kval, const double* x, const double* b, double* r,
+                      double* norm) {
+    launch_residual(N_, fr_ptr_.p, fr_col_.p, fr_slot_.p, kval, x, b, r, norm, st_);
+  }
+
+  // solve_refined (sparse.cpp:278-322).  b on device; solution in x_out
+  // (device).  Returns steps; rel/conv through pointers.
+  int solve_refined(const double* kval, const double* b, int max_ref, double tol,
+                    double* x_out, double* rel_out, int* conv_out) {
+    double* x = rx_.p;
+    double* r = rr_.p;
+    double* dx = rdx_.p;
+    double* xn = rxn_.p;
+    double* rn = rrn_.p;
+    solve_async(b, x);
+    CK(cudaMemsetAsync(&ds_.p->norm[0], 0, sizeof(double) * 2, st_));
+    launch_absmax2(N_, b, 0, nullptr, &ds_.p->norm[0], st_);
+    residual_async(kval, x, b, r, &ds_.p->norm[1]);
+    CK(cudaMemcpyAsync(&hs_->norm[0], &ds_.p->norm[0], sizeof(double) * 2,
+                       cudaMemcpyDeviceToHost, st_));
+    CK(cudaStreamSynchronize(st_));
+    const double bnorm = hs_->norm[0];
+    const double denom = bnorm > 0.0 ? bnorm : 1.0;
+    double res = hs_->norm[1];
+    double prev = res;
+    int stagnant = 0, steps = 0;
+    while (steps < max_ref && res > tol * denom) {
+      solve_async(r, dx);
+      launch_axpy_to(N_, x, dx, xn, st_);
+      CK(cudaMemsetAsync(&ds_.p->norm[1], 0, sizeof(double), st_));
+      residual_async(kval, xn, b, rn, &ds_.p->norm[1]);
+      CK(cudaMemcpyAsync(&hs_->norm[1], &ds_.p->norm[1], sizeof(double),
+                         cudaMemcpyDeviceToHost, st_));
+      CK(cudaStreamSynchronize(st_));
+      const double res_new = hs_->norm[1];
+      if (!std::isfinite(res_new) || res_new >= res) break;
+      std::swap(x, xn);
+      std::swap(r, rn);
+      steps++;
+      stagnant = (res_new > 0.5 * prev) ? stagnant + 1 : 0;
+      prev = res_new;
+      res = res_new;
+      if (stagnant >= 2) break;
+    }
+    CK(cudaMemcpyAsync(x_out, x, sizeof(double) * N_, cudaMemcpyDeviceToDevice, st_));
+    if (rel_out) *rel_out = res / denom;
+    if (conv_out) *conv_out = res <= tol * denom;
+    return steps;
+  }
+
+  // host copy of the factors in the reference's LdlFactors layout
+  void factors_host(int* lcol_ptr, int* lrow_ind, double* lval, double* d) const {
+    const int nsn = sn_.nsn;
+    std::vector<double> lv(static_cast<size_t>(sn_.l_off[nsn]));
+    std::vector<double> dv(static_cast<size_t>(N_));
+    if (!lv.empty())
+      CK(cudaMemcpy(lv.data(), lval_.p, lv.size() * sizeof(double), cudaMemcpyDeviceToHost));
+    if (N_) CK(cudaMemcpy(dv.data(), d_.p, dv.size() * sizeof(double), cudaMemcpyDeviceToHost));
+    if (lcol_ptr) std::copy(S_.lcol_ptr.begin(), S_.lcol_ptr.end(), lcol_ptr);
+    if (d) std::copy(dv.begin(), dv.end(), d);
+    if (!lrow_ind && !lval) return;
+    // column j of L: rows below j in the front of its supernode, ascending
+    for (int s = 0; s < nsn; ++s) {
+      const int c0 = sn_.first[s], k = sn_.first[s + 1] - c0, f = sn_.f[s];
+      const int* rows = sn_.rows.data() + sn_.rows_ptr[s];
+      for (int p = 0; p < k; ++p) {
+        int q = S_.lcol_ptr[c0 + p];
+        for (int r = p + 1; r < f; ++r, ++q) {
+          if (lrow_ind) lrow_ind[q] = rows[r];
+          if (lval) lval[q] = lv[static_cast<size_t>(sn_.l_off[s] + r + static_cast<long long>(p) * f)];
+        }
+      }
+    }
+  }
+
+  // y += A x on the host pattern (diagnostic)
+  int npaths() const { return static_cast<int>(sn_.path_ptr.size()) - 1; }
+
+ private:
+  FactorDev factor_dev() {
+    FactorDev fd;
+    fd.lval = lval_.p;
+    fd.d = d_.p;
+    fd.upd = upd_.p;
+    fd.scratch = scratch_.p;
+    fd.stats = ds_.p->stats;
+    return fd;
+  }
+
+  void upload() {
+    const Supernodal& T = sn_;
+    first_.upload(T.first);
+    f_.upload(T.f);
+    sparent_.upload(T.sparent);
+    rows_ptr_.upload(T.rows_ptr);
+    rows_.upload(T.rows);
+    l_off_.upload(T.l_off);
+    u_off_.upload(T.u_off);
+    u_ld_.upload(T.u_ld);
+    asm_ptr_.upload(T.asm_ptr);
+    asm_pos_.upload(T.asm_pos);
+    asm_slot_.upload(T.asm_slot);
+    ch_ptr_.upload(T.ch_ptr);
+    ch_.upload(T.ch);
+    rel_ptr_.upload(T.rel_ptr);
+    rel_.upload(T.rel);
+    path_ptr_.upload(T.path_ptr);
+    path_nodes_.upload(T.path_nodes);
+    lvl_nodes_.upload(T.lvl_nodes);
+    std::vector<int8_t> wide(T.wide.begin(), T.wide.end());
+    wide_.upload(wide);
+    // wide-front scratch: fronts of one level side by side, levels reuse it
+    std::vector<long long> scr(static_cast<size_t>(T.nsn), 0);
+    long long scr_max = 0;
+    for (size_t l = 0; l + 1 < T.lvl_ptr.size(); ++l) {
+      long long off = 0;
+      for (int q = T.lvl_ptr[l]; q < T.lvl_ptr[l + 1]; ++q) {
+        const int s = T.lvl_nodes[q];
+        scr[s] = off;
+        off += static_cast<long long>(T.f[s]) * T.f[s];
+      }
+      scr_max = std::max(scr_max, off);
+    }
+    scr_off_.upload(scr);
+    scratch_.alloc(static_cast<size_t>(scr_max));
+    perm_.upload(S_.perm);
+    lval_.alloc(static_cast<size_t>(T.l_off[T.nsn]));
+    lval_.zero(st_);
+    d_.alloc(static_cast<size_t>(N_));
+    upd_.alloc(static_cast<size_t>(T.u_total));
+    uvec_.alloc(static_cast<size_t>(T.rel_ptr[T.nsn]));
+    flags_.alloc(static_cast<size_t>(std::max(T.nsn, 1)));
+    flags_.zero(st_);
+    counter_.alloc(1);
+    wp_.alloc(static_cast<size_t>(N_));
+    xp_.alloc(static_cast<size_t>(N_));
+    rx_.alloc(static_cast<size_t>(N_));
+    rr_.alloc(static_cast<size_t>(N_));
+    rdx_.alloc(static_cast<size_t>(N_));
+    rxn_.alloc(static_cast<size_t>(N_));
+    rrn_.alloc(static_cast<size_t>(N_));
+    ds_.alloc(1);
+    ds_.zero(st_);
+    CK(cudaMallocHost(&hs_, sizeof(Scalars)));
+    // full symmetric row pattern for the residual matvec
+    std::vector<int> cnt(static_cast<size_t>(N_) + 1, 0);
+    for (int j = 0; j < N_; ++j)
+      for (int p = K_.col_ptr[j]; p < K_.col_ptr[j + 1]; ++p) {
+        cnt[K_.row_ind[p] + 1]++;
+        if (K_.row_ind[p] != j) cnt[j + 1]++;
+      }
+    for (int i = 0; i < N_; ++i) cnt[i + 1] += cnt[i];
+    std::vector<int> fcol(static_cast<size_t>(cnt[N_])), fslot(static_cast<size_t>(cnt[N_]));
+    std::vector<int> nx(cnt.begin(), cnt.end() - 1);
+    // columns ascending within each row: upper part (cols > i) comes from
+    // column i itself, lower part (cols < i) from earlier columns
+    for (int j = 0; j < N_; ++j)
+      for (int p = K_.col_ptr[j]; p < K_.col_ptr[j + 1]; ++p) {
+        const int i = K_.row_ind[p];
+        if (i != j) {
+          fcol[nx[i]] = j;
+          fslot[nx[i]++] = p;
+        }
+      }
+    for (int j = 0; j < N_; ++j)
+      for (int p = K_.col_ptr[j]; p < K_.col_ptr[j + 1]; ++p) {
+        fcol[nx[j]] = K_.row_ind[p];
+        fslot[nx[j]++] = p;
+      }
+    fr_ptr_.upload(cnt);
+    fr_col_.upload(fcol);
+    fr_slot_.upload(fslot);
+    sd_.nsn = T.nsn;
+    sd_.first = first_.p;
+    sd_.f = f_.p;
+    sd_.sparent = sparent_.p;
+    sd_.rows_ptr = rows_ptr_.p;
+    sd_.rows = rows_.p;
+    sd_.l_off = l_off_.p;
+    sd_.u_off = u_off_.p;
+    sd_.u_ld = u_ld_.p;
+    sd_.asm_ptr = asm_ptr_.p;
+    sd_.asm_pos = asm_pos_.p;
+    sd_.asm_slot = asm_slot_.p;
+    sd_.ch_ptr = ch_ptr_.p;
+    sd_.ch = ch_.p;
+    sd_.rel_ptr = rel_ptr_.p;
+    sd_.rel = rel_.p;
+    sd_.path_ptr = path_ptr_.p;
+    sd_.path_nodes = path_nodes_.p;
+    sd_.scr_off = scr_off_.p;
+    grid_ = warp_tier_grid();
+    set_wide_smem_limit(T.max_wide_f);
+    CK(cudaStreamSynchronize(st_));
+  }
+
+  LowerCsc K_;
+  Symbolic S_;
+  Supernodal sn_;
+  cudaStream_t st_;
+  int N_ = 0;
+  int grid_ = 1;
+  int epoch_ = 0;
+  SnDev sd_{};
+  DBuf<int> first_, f_, sparent_, rows_ptr_, rows_, u_ld_, asm_ptr_, asm_pos_, asm_slot_,
+      ch_ptr_, ch_, rel_ptr_, rel_, path_ptr_, path_nodes_, lvl_nodes_, perm_, flags_,
+      counter_, fr_ptr_, fr_col_, fr_slot_;
+  DBuf<int8_t> wide_;
+  DBuf<long long> l_off_, u_off_, scr_off_;
+  DBuf<double> lval_, d_, upd_, uvec_, scratch_, wp_, xp_, rx_, rr_, rdx_, rxn_, rrn_;
+  DBuf<Scalars> ds_;
+  Scalars* hs_ = nullptr;
+};
+
+// ---------------------------------------------------------------------------
+class KktSystem {
+ public:
+  KktSystem(KktPlan plan, const ncl_kkt_opts& opt)
+      : P_(std::move(plan)), opt_(opt) {
+    CK(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
+    ldl_ = std::make_unique<LdlSystem>(P_.K, P_.sym, st_);
+    c_ptr_.upload(P_.c_ptr);
+    c_code_.upload(P_.c_code);
+    pair_row_.upload(P_.pair_row);
+    pair_pa_.upload(P_.pair_pa);
+    pair_pb_.upload(P_.pair_pb);
+    jp_ptr_.upload(P_.jp_ptr);
+    jp_idx_.upload(P_.jp_idx);
+    jt_ptr_.upload(P_.jt_ptr);
+    jt_row_.upload(P_.jt_row);
+    jt_slot_.upload(P_.jt_slot);
+    const size_t n = static_cast<size_t>(P_.n), m = static_cast<size_t>(P_.m);
+    hval_.alloc(P_.hp_idx.size());
+    jval_.alloc(P_.jp_idx.size());
+    sigma_.alloc(n);
+    r1_.alloc(n);
+    r2_.alloc(m);
+    r3_.alloc(m);
+    dx_.alloc(n);
+    dr_.alloc(m);
+    dy_.alloc(m);
+    kval_.alloc(static_cast<size_t>(P_.K.nnz()));
+    kval_.zero(st_);
+    wrow_.alloc(m);
+    v_.alloc(m);
+    wk_.alloc(static_cast<size_t>(P_.m_ineq));
+    rs_.alloc(static_cast<size_t>(P_.m_ineq));
+    pk_.alloc(static_cast<size_t>(P_.m_ineq));
+    rhs_.alloc(static_cast<size_t>(P_.N));
+    sol_.alloc(static_cast<size_t>(P_.N));
+    asm_.nnz = P_.K.nnz();
+    asm_.c_ptr = c_ptr_.p;
+    asm_.c_code = c_code_.p;
+    asm_.pair_row = pair_row_.p;
+    asm_.pair_pa = pair_pa_.p;
+    asm_.pair_pb = pair_pb_.p;
+    for (auto& e : ev_) CK(cudaEventCreate(&e));
+    CK(cudaStreamSynchronize(st_));
+  }
+
+  ~KktSystem() {
+    ldl_.reset();
+    for (auto& e : ev_) cudaEventDestroy(e);
+    if (st_) cudaStreamDestroy(st_);
+  }
+
+  const KktPlan& plan() const { return P_; }
+  LdlSystem& ldl() { return *ldl_; }
+  cudaStream_t stream() const { return st_; }
+
+  void refill_async(const double* hv, const double* jv, const double* sg, double rho,
+                    double delta) {
+    launch_assemble(asm_, P_.form, P_.m, P_.m_eq, P_.nt, hv, jv, sg, wrow_.p, rho, delta,
+                    kval_.p, st_);
+  }
+
+  void refill_host(const double* hv, const double* jv, const double* sg, double rho,
+                   double delta) {
+    upload_inputs(hv, jv, sg, nullptr, nullptr, nullptr);
+    refill_async(hval_.p, jval_.p, sigma_.p, rho, delta);
+    CK(cudaStreamSynchronize(st_));
+  }
+
+  void upload_inputs(const double* hv, const double* jv, const double* sg, const double* r1,
+                     const double* r2, const double* r3) {
+    auto h2d = [&](double* dst, const double* src, size_t k) {
+      if (k) CK(cudaMemcpyAsync(dst, src, k * sizeof(double), cudaMemcpyHostToDevice, st_));
+    };
+    h2d(hval_.p, hv, hval_.n);
+    h2d(jval_.p, jv, jval_.n);
+    h2d(sigma_.p, sg, sigma_.n);
+    if (r1) h2d(r1_.p, r1, r1_.n);
+    if (r2) h2d(r2_.p, r2, r2_.n);
+    if (r3) h2d(r3_.p, r3, r3_.n);
+  }
+
+  // KktContext::solve (kkt.cpp:266-314) on device-resident inputs
+  void solve_device(const double* hv, const double* jv, const double* sg, const double* r1,
+                    const double* r2, const double* r3, double rho, double warm, double* dx,
+                    double* dr, double* dy, ncl_kkt_stats* st) {
+    std::memset(st, 0, sizeof(*st));
+    std::fill(std::begin(ms_), std::end(ms_) - 1, 0.0);
+    Scalars* ds = ldl_->dev_scalars();
+    Scalars* hs = ldl_->host_scalars();
+    CK(cudaMemsetAsync(&ds->hmax, 0, sizeof(double), st_));
+    launch_absmax2(static_cast<int>(hval_.n), hv, P_.n, sg, &ds->hmax, st_);
+    double delta = 0.0;
+    bool first = true;
+    const int* tgt = P_.inertia_target;
+    for (;;) {
+      st->factor_attempts++;
+      mark(0);
+      refill_async(hv, jv, sg, rho, delta);
+      mark(1);
+      ldl_->factorize_async(kval_.p, opt_.pivot_eps);
+      mark(2);
+      const FactorInfo F = ldl_->read_factor_info();
+      accumulate(0, 0, 1);
+      accumulate(1, 1, 2);
+      if (F.ok && F.n_pos == tgt[0] && F.n_neg == tgt[1]) {
+        mark(0);
+        launch_rhs(P_, jt_ptr_.p, jt_row_.p, jt_slot_.p, jv, sg, r1, r2, r3, rho, delta, v_.p,
+                   wk_.p, rs_.p, pk_.p, rhs_.p, st_);
+        double rel = 0.0;
+        int conv = 0;
+        const int steps = ldl_->solve_refined(kval_.p, rhs_.p, opt_.max_refine,
+                                              opt_.refine_tol, sol_.p, &rel, &conv);
+        mark(1);
+        accumulate(2, 0, 1);
+        // bn = ||rhs||_inf was read inside solve_refined
+        const double bn = hs->norm[0];
+        const double abs_res = rel * (bn > 0.0 ? bn : 1.0);
+        const bool accept =
+            F.perturbed == 0 || abs_res <= opt_.accept_tol * std::max(1.0, bn);
+        if (accept) {
+          st->delta = delta;
+          st->refine_steps = steps;
+          st->perturbed_pivots = F.perturbed;
+          st->rel_residual = rel;
+          mark(0);
+          launch_recover(P_, jp_ptr_.p, jp_idx_.p, jv, sol_.p, v_.p, rs_.p, pk_.p, r2, rho,
+                         delta, dx, dr, dy, st_);
+          CK(cudaMemsetAsync(&ds->nonfinite, 0, sizeof(int), st_));
+          launch_nonfinite(P_.n, dx, &ds->nonfinite, st_);
+          launch_nonfinite(P_.m, dr, &ds->nonfinite, st_);
+          launch_nonfinite(P_.m, dy, &ds->nonfinite, st_);
+          CK(cudaMemcpyAsync(&hs->nonfinite, &ds->nonfinite, sizeof(int),
+                             cudaMemcpyDeviceToHost, st_));
+          mark(1);
+          CK(cudaStreamSynchronize(st_));
+          accumulate(3, 0, 1);
+          st->ok = hs->nonfinite == 0;
+          finish_timing();
+          return;
+        }
+      }
+      if (first) {
+        delta = warm > 0.0 ? std::max(1e-20, warm / 3.0) : 1e-8 * std::max(1.0, hs->hmax);
+        first = false;
+      } else {
+        delta *= 8.0;
+      }
+      if (delta > opt_.delta_max) {
+        st->ok = 0;
+        finish_timing();
+        return;
+      }
+    }
+  }
+
+  void solve_host(const double* hv, const double* jv, const double* sg, const double* r1,
+                  const double* r2, const double* r3, double rho, double warm, double* dx,
+                  double* dr, double* dy, ncl_kkt_stats* st) {
+    upload_inputs(hv, jv, sg, r1, r2, r3);
+    solve_device(hval_.p, jval_.p, sigma_.p, r1_.p, r2_.p, r3_.p, rho, warm, dx_.p, dr_.p,
+                 dy_.p, st);
+    auto d2h = [&](double* dst, const double* src, size_t k) {
+      if (k && dst) CK(cudaMemcpyAsync(dst, src, k * sizeof(double), cudaMemcpyDeviceToHost, st_));
+    };
+    if (st->factor_attempts && (st->ok || st->refine_steps >= 0)) {
+      d2h(dx, dx_.p, dx_.n);
+      d2h(dr, dr_.p, dr_.n);
+      d2h(dy, dy_.p, dy_.n);
+    }
+    CK(cudaStreamSynchronize(st_));
+  }
+
+  void matrix(int* cp, int* ri, double* val) const {
+    if (cp) std::copy(P_.K.col_ptr.begin(), P_.K.col_ptr.end(), cp);
+    if (ri) std::copy(P_.K.row_ind.begin(), P_.K.row_ind.end(), ri);
+    if (val && kval_.n)
+      CK(cudaMemcpy(val, kval_.p, kval_.n * sizeof(double), cudaMemcpyDeviceToHost));
+  }
+
+  void set_timing(bool on) { timing_ = on; }
+  void timing(double* out) const { std::copy(std::begin(ms_), std::end(ms_), out); }
+
+ private:
+  void mark(int i) {
+    if (timing_) CK(cudaEventRecord(ev_[i], st_));
+  }
+  void accumulate(int slot, int a, int b) {
+    if (!timing_) return;
+    CK(cudaEventSynchronize(ev_[b]));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, ev_[a], ev_[b]));
+    ms_[slot] += ms;
+  }
+  void finish_timing() {
+    ms_[4] = ms_[0] + ms_[1] + ms_[2] + ms_[3];
+    ms_[5] += 1.0;
+  }
+
+  KktPlan P_;
+  ncl_kkt_opts opt_;
+  cudaStream_t st_ = nullptr;
+  std::unique_ptr<LdlSystem> ldl_;
+  AsmDev asm_{};
+  DBuf<int> c_ptr_, pair_row_, pair_pa_, pair_pb_, jp_ptr_, jp_idx_, jt_ptr_, jt_row_,
+      jt_slot_;
+  DBuf<uint32_t> c_code_;
+  DBuf<double> hval_, jval_, sigma_, r1_, r2_, r3_, dx_, dr_, dy_, kval_, wrow_, v_, wk_, rs_,
+      pk_, rhs_, sol_;
+  cudaEvent_t ev_[2] = {nullptr, nullptr};
+  bool timing_ = false;
+  double ms_[6] = {0, 0, 0, 0, 0, 0};
+};
+
+// ---------------------------------------------------------------------------
+// plain sparse system (sparse.hpp API on the device LDL^T)
+class SparseSystem {
+ public:
+  SparseSystem(int n, const std::vector<int>& rows, const std::vector<int>& cols,
+               const std::vector<double>& vals, const int* perm) {
+    std::vector<int> slot;
+    K_ = sym_lower_from_pattern(n, rows, cols, &slot);
+    // values summed in sorted (stable) order like sym_from_triplets
+    std::vector<int> order(rows.size());
+    for (size_t k = 0; k < order.size(); ++k) order[k] = static_cast<int>(k);
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return slot[a] < slot[b]; });
+    val_.assign(static_cast<size_t>(K_.nnz()), 0.0);
+    std::vector<char> seen(static_cast<size_t>(K_.nnz()), 0);
+    for (int k : order) {
+      if (!seen[slot[k]]) {
+        val_[slot[k]] = vals[k];
+        seen[slot[k]] = 1;
+      } else {
+        val_[slot[k]] += vals[k];
+      }
+    }
+    std::vector<int> pm = perm ? std::vector<int>(perm, perm + n) : amd_order(K_);
+    S_ = analyze_with_permutation(K_, pm);
+    CK(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
+    ldl_ = std::make_unique<LdlSystem>(K_, S_, st_);
+    kval_.upload(val_);
+    b_.alloc(static_cast<size_t>(n));
+    x_.alloc(static_cast<size_t>(n));
+  }
+  ~SparseSystem() {
+    ldl_.reset();
+    if (st_) cudaStreamDestroy(st_);
+  }
+  LdlSystem& ldl() { return *ldl_; }
+  const LowerCsc& K() const { return K_; }
+  const std::vector<double>& val() const { return val_; }
+  FactorInfo factorize(double eps) {
+    ldl_->factorize_async(kval_.p, eps);
+    return ldl_->read_factor_info();
+  }
+  void solve(const double* b, double* x) {
+    const int n = K_.n;
+    if (!n) return;
+    CK(cudaMemcpyAsync(b_.p, b, sizeof(double) * n, cudaMemcpyHostToDevice, st_));
+    ldl_->solve_async(b_.p, x_.p);
+    CK(cudaMemcpyAsync(x, x_.p, sizeof(double) * n, cudaMemcpyDeviceToHost, st_));
+    CK(cudaStreamSynchronize(st_));
+  }
+  int solve_refined(const double* b, int max_ref, double tol, double* x, double* rel,
+                    int* conv) {
+    const int n = K_.n;
+    if (!n) {
+      if (rel) *rel = 0.0;
+      if (conv) *conv = 1;
+      return 0;
+    }
+    CK(cudaMemcpyAsync(b_.p, b, sizeof(double) * n, cudaMemcpyHostToDevice, st_));
+    const int steps = ldl_->solve_refined(kval_.p, b_.p, max_ref, tol, x_.p, rel, conv);
+    CK(cudaMemcpyAsync(x, x_.p, sizeof(double) * n, cudaMemcpyDeviceToHost, st_));
+    CK(cudaStreamSynchronize(st_));
+    return steps;
+  }
+  const Symbolic& sym() const { return S_; }
+
+ private:
+  LowerCsc K_;
+  Symbolic S_;
+  std::vector<double> val_;
+  cudaStream_t st_ = nullptr;
+  std::unique_ptr<LdlSystem> ldl_;
+  DBuf<double> kval_, b_, x_;
+};
+
+}  // namespace nclb
+
+// ===========================================================================
+// C ABI
+struct ncl_kkt {
+  std::unique_ptr<nclb::KktSystem> sys;
+};
+struct ncl_sparse {
+  std::unique_ptr<nclb::SparseSystem> sys;
+};
+struct ncl_plan {
+  nclb::KktPlan plan;
+};
+
+namespace {
+
+template <class F>
+int guard(F&& f) {
+  try {
+    f();
+    return NCL_OK;
+  } catch (const std::invalid_argument& e) {
+    nclb::g_err = e.what();
+    return NCL_EINVAL;
+  } catch (const std::logic_error& e) {
+    nclb::g_err = e.what();
+    return NCL_ELOGIC;
+  } catch (const nclb::CudaError& e) {
+    nclb::g_err = e.what();
+    return NCL_ECUDA;
+  } catch (const std::bad_alloc& e) {
+    nclb::g_err = "out of memory";
+    return NCL_ENOMEM;
+  } catch (const std::exception& e) {
+    nclb::g_err = e.what();
+    return NCL_ECUDA;
+  }
+}
+
+ncl_kkt_opts default_opts() {
+  ncl_kkt_opts o;
+  o.pivot_eps = 1e-10;
+  o.max_refine = 10;
+  o.refine_tol = 1e-12;
+  o.delta_max = 1e40;
+  o.accept_tol = 1e-8;
+  return o;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ncl_last_error(void) { return nclb::g_err.c_str(); }
+
+int ncl_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+  return n;
+}
+
+int ncl_kkt_create(int nt, const int* hp_ptr, const int* hp_idx, int m, const int* jp_ptr,
+                   const int* jp_idx, int ns, int m_eq, int form, const ncl_kkt_opts* opt,
+                   ncl_kkt** out) {
+  if (!out || !hp_ptr || !jp_ptr) {
+    nclb::g_err = "ncl_kkt_create: null argument";
+    return NCL_EINVAL;
+  }
+  *out = nullptr;
+  return guard([&] {
+    nclb::KktPlan plan =
+        nclb::make_kkt_plan(nt, hp_ptr, hp_idx, m, jp_ptr, jp_idx, ns, m_eq, form);
+    auto* c = new ncl_kkt;
+    try {
+      c->sys = std::make_unique<nclb::KktSystem>(std::move(plan), opt ? *opt : default_opts());
+    } catch (...) {
+      delete c;
+      throw;
+    }
+    *out = c;
+  });
+}
+
+void ncl_kkt_destroy(ncl_kkt* ctx) { delete ctx; }
+
+int ncl_kkt_solve(ncl_kkt* ctx, const double* hval, const double* jval, const double* sigma,
+                  const double* rbar1, const double* rbar2, const double* rbar3, double rho,
+                  double warm_delta, double* dx, double* dr, double* dy,
+                  ncl_kkt_stats* stats) {
+  if (!ctx || !stats) return NCL_EINVAL;
+  return guard([&] {
+    ctx->sys->solve_host(hval, jval, sigma, rbar1, rbar2, rbar3, rho, warm_delta, dx, dr, dy,
+                         stats);
+  });
+}
+
+int ncl_kkt_solve_device(ncl_kkt* ctx, const double* hval, const double* jval,
+                         const double* sigma, const double* rbar1, const double* rbar2,
+                         const double* rbar3, double rho, double warm_delta, double* dx,
+                         double* dr, double* dy, ncl_kkt_stats* stats) {
+  if (!ctx || !stats) return NCL_EINVAL;
+  return guard([&] {
+    ctx->sys->solve_device(hval, jval, sigma, rbar1, rbar2, rbar3, rho, warm_delta, dx, dr, dy,
+                           stats);
+  });
+}
+
+int ncl_kkt_info_get(const ncl_kkt* ctx, ncl_kkt_info* info) {
+  if (!ctx || !info) return NCL_EINVAL;
+  const auto& P = ctx->sys->plan();
+  const auto& T = ctx->sys->ldl().sn();
+  info->n = P.N;
+  info->nnz = P.K.nnz();
+  info->l_nnz = P.sym.l_nnz();
+  info->flops = T.flops;
+  info->n_supernodes = T.nsn;
+  info->sn_height = T.sn_height;
+  info->n_paths = static_cast<int>(T.path_ptr.size()) - 1;
+  info->n_wide = static_cast<int>(T.lvl_nodes.size());
+  info->n_levels = static_cast<int>(T.lvl_ptr.size()) - 1;
+  info->max_front = T.max_f;
+  info->npairs = static_cast<long long>(P.pair_slot.size());
+  return NCL_OK;
+}
+
+int ncl_kkt_inertia_target(const ncl_kkt* ctx, int* tgt3) {
+  if (!ctx || !tgt3) return NCL_EINVAL;
+  for (int i = 0; i < 3; ++i) tgt3[i] = ctx->sys->plan().inertia_target[i];
+  return NCL_OK;
+}
+
+int ncl_kkt_symbolic(const ncl_kkt* ctx, int* perm, int* parent, int* lcol_ptr) {
+  if (!ctx) return NCL_EINVAL;
+  const auto& S = ctx->sys->plan().sym;
+  if (perm) std::copy(S.perm.begin(), S.perm.end(), perm);
+  if (parent) std::copy(S.parent.begin(), S.parent.end(), parent);
+  if (lcol_ptr) std::copy(S.lcol_ptr.begin(), S.lcol_ptr.end(), lcol_ptr);
+  return NCL_OK;
+}
+
+int ncl_kkt_matrix(const ncl_kkt* ctx, int* col_ptr, int* row_ind, double* val) {
+  if (!ctx) return NCL_EINVAL;
+  return guard([&] { ctx->sys->matrix(col_ptr, row_ind, val); });
+}
+
+int ncl_kkt_refill(ncl_kkt* ctx, const double* hval, const double* jval, const double* sigma,
+                   double rho, double delta) {
+  if (!ctx) return NCL_EINVAL;
+  return guard([&] {
+    ctx->sys->refill_host(hval, jval, sigma, rho, delta);
+  });
+}
+
+int ncl_kkt_factors(const ncl_kkt* ctx, int* lcol_ptr, int* lrow_ind, double* lval, double* d,
+                    int* info4) {
+  if (!ctx) return NCL_EINVAL;
+  return guard([&] {
+    auto& L = ctx->sys->ldl();
+    L.factors_host(lcol_ptr, lrow_ind, lval, d);
+    if (info4) {
+      nclb::Scalars* hs = L.host_scalars();
+      CK(cudaMemcpy(hs, L.dev_scalars(), sizeof(nclb::Scalars), cudaMemcpyDeviceToHost));
+      info4[0] = hs->stats[3] == 0;
+      info4[1] = hs->stats[0];
+      info4[2] = hs->stats[1];
+      info4[3] = hs->stats[2];
+    }
+  });
+}
+
+int ncl_kkt_last_timing(const ncl_kkt* ctx, double* ms6) {
+  if (!ctx || !ms6) return NCL_EINVAL;
+  ctx->sys->timing(ms6);
+  return NCL_OK;
+}
+
+int ncl_kkt_set_timing(ncl_kkt* ctx, int enable) {
+  if (!ctx) return NCL_EINVAL;
+  ctx->sys->set_timing(enable != 0);
+  return NCL_OK;
+}
+
+// ---- host-only plan ---------------------------------------------------------
+int ncl_plan_create(int nt, const int* hp_ptr, const int* hp_idx, int m, const int* jp_ptr,
+                    const int* jp_idx, int ns, int m_eq, int form, ncl_plan** out) {
+  if (!out || !hp_ptr || !jp_ptr) return NCL_EINVAL;
+  *out = nullptr;
+  return guard([&] {
+    auto* p = new ncl_plan;
+    try {
+      p->plan = nclb::make_kkt_plan(nt, hp_ptr, hp_idx, m, jp_ptr, jp_idx, ns, m_eq, form);
+    } catch (...) {
+      delete p;
+      throw;
+    }
+    *out = p;
+  });
+}
+
+void ncl_plan_destroy(ncl_plan* plan) { delete plan; }
+
+int ncl_plan_info(const ncl_plan* plan, ncl_kkt_info* info) {
+  if (!plan || !info) return NCL_EINVAL;
+  const auto& P = plan->plan;
+  const auto& T = P.sn;
+  info->n = P.N;
+  info->nnz = P.K.nnz();
+  info->l_nnz = P.sym.l_nnz();
+  info->flops = T.flops;
+  info->n_supernodes = T.nsn;
+  info->sn_height = T.sn_height;
+  info->n_paths = static_cast<int>(T.path_ptr.size()) - 1;
+  info->n_wide = static_cast<int>(T.lvl_nodes.size());
+  info->n_levels = static_cast<int>(T.lvl_ptr.size()) - 1;
+  info->max_front = T.max_f;
+  info->npairs = static_cast<long long>(P.pair_slot.size());
+  return NCL_OK;
+}
+
+int ncl_plan_symbolic(const ncl_plan* plan, int* perm, int* parent, int* lcol_ptr) {
+  if (!plan) return NCL_EINVAL;
+  const auto& S = plan->plan.sym;
+  if (perm) std::copy(S.perm.begin(), S.perm.end(), perm);
+  if (parent) std::copy(S.parent.begin(), S.parent.end(), parent);
+  if (lcol_ptr) std::copy(S.lcol_ptr.begin(), S.lcol_ptr.end(), lcol_ptr);
+  return NCL_OK;
+}
+
+int ncl_plan_pattern(const ncl_plan* plan, int* col_ptr, int* row_ind) {
+  if (!plan) return NCL_EINVAL;
+  const auto& K = plan->plan.K;
+  if (col_ptr) std::copy(K.col_ptr.begin(), K.col_ptr.end(), col_ptr);
+  if (row_ind) std::copy(K.row_ind.begin(), K.row_ind.end(), row_ind);
+  return NCL_OK;
+}
+
+int ncl_analyze_host(int n, int ntrip, const int* rows, const int* cols, const int* perm_in,
+                     int* perm, int* parent, int* lcol_ptr) {
+  if (n < 0 || ntrip < 0) return NCL_EINVAL;
+  return guard([&] {
+    const nclb::LowerCsc K = nclb::sym_lower_from_pattern(
+        n, std::vector<int>(rows, rows + ntrip), std::vector<int>(cols, cols + ntrip));
+    const std::vector<int> pm =
+        perm_in ? std::vector<int>(perm_in, perm_in + n) : nclb::amd_order(K);
+    const nclb::Symbolic S = nclb::analyze_with_permutation(K, pm);
+    if (perm) std::copy(S.perm.begin(), S.perm.end(), perm);
+    if (parent) std::copy(S.parent.begin(), S.parent.end(), parent);
+    if (lcol_ptr) std::copy(S.lcol_ptr.begin(), S.lcol_ptr.end(), lcol_ptr);
+  });
+}
+
+// ---- sparse layer ---------------------------------------------------------
+int ncl_sparse_create(int n, int ntrip, const int* rows, const int* cols, const double* vals,
+                      const int* perm, ncl_sparse** out) {
+  if (!out || n < 0 || ntrip < 0) return NCL_EINVAL;
+  *out = nullptr;
+  return guard([&] {
+    std::vector<int> r(rows, rows + ntrip), c(cols, cols + ntrip);
+    std::vector<double> v(vals, vals + ntrip);
+    auto* s = new ncl_sparse;
+    try {
+      s->sys = std::make_unique<nclb::SparseSystem>(n, r, c, v, perm);
+    } catch (...) {
+      delete s;
+      throw;
+    }
+    *out = s;
+  });
+}
+
+void ncl_sparse_destroy(ncl_sparse* sp) { delete sp; }
+
+int ncl_sparse_nnz(const ncl_sparse* sp, int* nnz, long long* l_nnz) {
+  if (!sp) return NCL_EINVAL;
+  if (nnz) *nnz = sp->sys->K().nnz();
+  if (l_nnz) *l_nnz = sp->sys->sym().l_nnz();
+  return NCL_OK;
+}
+
+int ncl_sparse_symbolic(const ncl_sparse* sp, int* perm, int* parent, int* lcol_ptr) {
+  if (!sp) return NCL_EINVAL;
+  const auto& S = sp->sys->sym();
+  if (perm) std::copy(S.perm.begin(), S.perm.end(), perm);
+  if (parent) std::copy(S.parent.begin(), S.parent.end(), parent);
+  if (lcol_ptr) std::copy(S.lcol_ptr.begin(), S.lcol_ptr.end(), lcol_ptr);
+  return NCL_OK;
+}
+
+int ncl_sparse_factorize(ncl_sparse* sp, double pivot_eps, int* info4) {
+  if (!sp) return NCL_EINVAL;
+  return guard([&] {
+    const nclb::FactorInfo fi = sp->sys->factorize(pivot_eps);
+    if (info4) {
+      info4[0] = fi.ok;
+      info4[1] = fi.n_pos;
+      info4[2] = fi.n_neg;
+      info4[3] = fi.perturbed;
+    }
+  });
+}
+
+int ncl_sparse_factors(const ncl_sparse* sp, int* lcol_ptr, int* lrow_ind, double* lval,
+                       double* d) {
+  if (!sp) return NCL_EINVAL;
+  return guard([&] { sp->sys->ldl().factors_host(lcol_ptr, lrow_ind, lval, d); });
+}
+
+int ncl_sparse_ldl_solve(ncl_sparse* sp, const double* b, double* x) {
+  if (!sp) return NCL_EINVAL;
+  return guard([&] { sp->sys->solve(b, x); });
+}
+
+int ncl_sparse_solve_refined(ncl_sparse* sp, const double* b, int max_ref, double tol,
+                             double* x, int* steps, double* rel_residual, int* converged) {
+  if (!sp) return NCL_EINVAL;
+  return guard([&] {
+    const int s = sp->sys->solve_refined(b, max_ref, tol, x, rel_residual, converged);
+    if (steps) *steps = s;
+  });
+}
+
+int ncl_sparse_matvec(ncl_sparse* sp, const double* x, double* y) {
+  if (!sp) return NCL_EINVAL;
+  const auto& K = sp->sys->K();
+  const auto& v = sp->sys->val();
+  for (int j = 0; j < K.n; ++j)
+    for (int p = K.col_ptr[j]; p < K.col_ptr[j + 1]; ++p) {
+      const int i = K.row_ind[p];
+      y[i] += v[p] * x[j];
+      if (i != j) y[j] += v[p] * x[i];
+    }
+  return NCL_OK;
+}
+
+}  // extern "C"

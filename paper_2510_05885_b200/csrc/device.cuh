@@ -1,0 +1,58 @@
+// Device-side views shared by the sm_100a kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace nclb {
+
+// Supernodal structure on the device (see symbolic.hpp).
+struct SnDev {
+  int nsn;
+  const int* first;     // nsn+1
+  const int* f;         // nsn
+  const int* sparent;   // nsn
+  const int* rows_ptr;  // nsn+1
+  const int* rows;
+  const long long* l_off;  // nsn+1
+  const long long* u_off;  // nsn
+  const int* u_ld;         // nsn (f - k)
+  const int* asm_ptr;
+  const int* asm_pos;
+  const int* asm_slot;
+  const int* ch_ptr;
+  const int* ch;
+  const int* rel_ptr;  // also the offsets of the forward-solve update vectors
+  const int* rel;
+  const int* path_ptr;
+  const int* path_nodes;
+  const long long* scr_off;  // wide fronts: offset into the front scratch
+};
+
+// numeric factor storage
+struct FactorDev {
+  double* lval;   // l_off[nsn]
+  double* d;      // N (permuted order)
+  double* upd;    // u_total
+  double* scratch;  // wide fronts (f x f, column-major)
+  int* stats;     // [0] n_pos [1] n_neg [2] perturbed [3] fail
+};
+
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void st_release(int* p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// max of non-negative doubles (NaN skipped, like std::max(acc, nan) == acc)
+__device__ __forceinline__ void atomic_max_nonneg(double* addr, double v) {
+  if (!(v >= 0.0)) return;
+  atomicMax(reinterpret_cast<unsigned long long*>(addr),
+            static_cast<unsigned long long>(__double_as_longlong(v)));
+}
+
+}  // namespace nclb

@@ -1,0 +1,67 @@
+// Host-callable launchers of the sm_100a kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "device.cuh"
+#include "kkt_plan.hpp"
+
+namespace nclb {
+
+struct AsmDev {
+  int nnz;
+  const int* c_ptr;
+  const uint32_t* c_code;
+  const int* pair_row;
+  const int* pair_pa;
+  const int* pair_pb;
+};
+
+// ldl_kernels.cu
+void launch_factor_warp(const SnDev& sd, const FactorDev& fd, const double* kval,
+                        int* flags, int epoch, int* counter, int npaths,
+                        double eps, int grid, cudaStream_t st);
+void launch_factor_wide(const SnDev& sd, const FactorDev& fd, const double* kval,
+                        const int* nodes, int count, double eps, cudaStream_t st);
+void launch_fwd_warp(const SnDev& sd, const double* lval, double* w, double* uvec,
+                     int* flags, int epoch, int* counter, int npaths, int grid,
+                     cudaStream_t st);
+void launch_bwd_warp(const SnDev& sd, const double* lval, const double* d,
+                     const double* w, double* x, int* flags, int epoch,
+                     const int8_t* wide, int* counter, int npaths, int grid,
+                     cudaStream_t st);
+void launch_fwd_wide(const SnDev& sd, const double* lval, double* w, double* uvec,
+                     const int* nodes, int count, int max_f, cudaStream_t st);
+void launch_bwd_wide(const SnDev& sd, const double* lval, const double* d,
+                     const double* w, double* x, const int* nodes, int count,
+                     int max_f, cudaStream_t st);
+void launch_permute_in(int n, const int* perm, const double* b, double* w,
+                       cudaStream_t st);
+void launch_permute_out(int n, const int* perm, const double* xp, double* x,
+                        cudaStream_t st);
+int warp_tier_grid();
+void set_wide_smem_limit(int max_f);
+
+// kkt_kernels.cu
+void launch_assemble(const AsmDev& a, int form, int m, int m_eq, int nt,
+                     const double* hval, const double* jval, const double* sigma,
+                     double* wrow, double rho, double delta, double* kval,
+                     cudaStream_t st);
+void launch_absmax2(int n1, const double* a, int n2, const double* b, double* out,
+                    cudaStream_t st);
+void launch_rhs(const KktPlan& P, const int* jt_ptr, const int* jt_row, const int* jt_slot,
+                const double* jval, const double* sigma, const double* r1,
+                const double* r2, const double* r3, double rho, double delta, double* v,
+                double* wk, double* rs, double* pk, double* rhs, cudaStream_t st);
+void launch_recover(const KktPlan& P, const int* jp_ptr, const int* jp_idx,
+                    const double* jval, const double* sol, const double* v,
+                    const double* rs, const double* pk, const double* r2, double rho,
+                    double delta, double* dx, double* dr, double* dy, cudaStream_t st);
+void launch_nonfinite(int n, const double* a, int* flag, cudaStream_t st);
+void launch_residual(int N, const int* fr_ptr, const int* fr_col, const int* fr_slot,
+                     const double* kval, const double* x, const double* b, double* r,
+                     double* norm, cudaStream_t st);
+void launch_axpy_to(int n, const double* x, const double* dx, double* out, cudaStream_t st);
+
+}  // namespace nclb

@@ -1,0 +1,507 @@
+// Static-pivot supernodal multifrontal LDL^T and its triangular solves for
+// sm_100a.  Numeric semantics follow proj/src/sparse.cpp:182-276: pivots in
+// the fixed (AMD) order, |d| < eps replaced by sign(d)*eps (exact zero -> +eps)
+// and counted, inertia from the signs of D, ok = false on a non-finite or
+// zero pivot or a non-finite L entry.
+//
+// Two tiers (see symbolic.hpp):
+//  * warp tier  -- fronts of <= 32 rows.  One persistent kernel; each warp
+//    pulls a heavy path of the supernodal elimination tree from a global
+//    counter and walks it bottom-up (factor, forward solve) or top-down
+//    (backward solve) with the front in shared memory, one front row per
+//    lane.  Light children are other warps' paths that precede it in the
+//    path order, so a warp only ever spins on work that an already-running
+//    warp owns: no deadlock, no per-level launches, and long chains
+//    (ring-shaped power grids) run at on-chip latency.
+//  * wide tier  -- fronts above 32 rows and all their ancestors.  One launch
+//    per tree level, one CTA per front; the trailing Schur update is a tiled
+//    rank-32 FP64 update through shared memory.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "device.cuh"
+#include "launch.hpp"
+
+namespace nclb {
+
+constexpr int kWF = 32;       // warp-tier front limit (rows)
+constexpr int kFLD = 33;      // padded leading dimension of a warp front
+constexpr int kWarpsPerCta = 4;
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ int next_path(int* counter, int lane) {
+  int pi = 0;
+  if (lane == 0) pi = atomicAdd(counter, 1);
+  return __shfl_sync(0xffffffffu, pi, 0);
+}
+
+__device__ __forceinline__ void publish(int* flag, int epoch, int lane) {
+  __threadfence();
+  __syncwarp();
+  if (lane == 0) st_release(flag, epoch);
+}
+
+// ---------------------------------------------------------------------------
+// warp-tier numeric factorization
+__global__ void __launch_bounds__(kWarpsPerCta * 32)
+k_factor_warp(SnDev sd, FactorDev fd, const double* __restrict__ kval,
+              int* flags, int epoch, int* counter, int npaths, double eps) {
+  __shared__ double smem[kWarpsPerCta][kWF * kFLD];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  double* F = smem[wid];
+  int npos = 0, nneg = 0, pert = 0, fail = 0;
+  for (;;) {
+    const int pi = next_path(counter, lane);
+    if (pi >= npaths) break;
+    const int pb = sd.path_ptr[pi], pe = sd.path_ptr[pi + 1];
+    for (int q = pb; q < pe; ++q) {
+      const int s = sd.path_nodes[q];
+      const int c0 = sd.first[s], k = sd.first[s + 1] - c0, f = sd.f[s];
+      const int chb = sd.ch_ptr[s], che = sd.ch_ptr[s + 1];
+      for (int c = chb + lane; c < che; c += 32)
+        while (ld_acquire(flags + sd.ch[c]) != epoch) {
+        }
+      __syncwarp();
+      for (int c = 0; c < f; ++c) F[c * kFLD + lane] = 0.0;
+      __syncwarp();
+      for (int a = sd.asm_ptr[s] + lane; a < sd.asm_ptr[s + 1]; a += 32) {
+        const int pos = sd.asm_pos[a];
+        F[(pos >> 16) * kFLD + (pos & 0xffff)] += __ldg(kval + sd.asm_slot[a]);
+      }
+      __syncwarp();
+      for (int cc = chb; cc < che; ++cc) {
+        const int c = sd.ch[cc];
+        const int fu = sd.u_ld[c];
+        const int* rel = sd.rel + sd.rel_ptr[c];
+        const double* U = fd.upd + sd.u_off[c];
+        if (lane < fu) {
+          const int ri = rel[lane];
+          for (int j = 0; j <= lane; ++j)
+            F[rel[j] * kFLD + ri] += __ldcg(U + lane + static_cast<size_t>(j) * fu);
+        }
+        __syncwarp();
+      }
+      double* Lb = fd.lval + sd.l_off[s];
+      for (int p = 0; p < k; ++p) {
+        const double u = (lane < f) ? F[p * kFLD + lane] : 0.0;
+        double dp = __shfl_sync(0xffffffffu, u, p);
+        int pflag = 0;
+        if (fabs(dp) < eps) {
+          dp = (dp >= 0.0) ? eps : -eps;
+          pflag = 1;
+        }
+        const bool bad = !isfinite(dp) || dp == 0.0;
+        const bool mine = lane > p && lane < f;
+        const double l = mine ? u / dp : 0.0;
+#pragma unroll 4
+        for (int j = p + 1; j < f; ++j) {
+          const double uj = F[p * kFLD + j];
+          if (lane >= j && lane < f) F[j * kFLD + lane] -= l * uj;
+        }
+        if (mine) {
+          Lb[lane + static_cast<size_t>(p) * f] = l;
+          if (!isfinite(l)) fail = 1;
+        }
+        if (lane == 0) {
+          fd.d[c0 + p] = dp;
+          pert += pflag;
+          if (bad) fail = 1;
+          if (dp > 0.0)
+            npos++;
+          else
+            nneg++;
+        }
+        __syncwarp();
+      }
+      const int fu = f - k;
+      double* Us = fd.upd + sd.u_off[s];
+      if (lane >= k && lane < f) {
+        const int i = lane - k;
+        for (int j = 0; j <= i; ++j)
+          Us[i + static_cast<size_t>(j) * fu] = F[(k + j) * kFLD + lane];
+      }
+      publish(flags + s, epoch, lane);
+    }
+  }
+  fail = __any_sync(0xffffffffu, fail);
+  if (lane == 0) {
+    if (npos) atomicAdd(fd.stats + 0, npos);
+    if (nneg) atomicAdd(fd.stats + 1, nneg);
+    if (pert) atomicAdd(fd.stats + 2, pert);
+    if (fail) atomicOr(fd.stats + 3, 1);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// wide-tier numeric factorization: one CTA per front of one tree level
+constexpr int kWideThreads = 256;
+constexpr int kPanel = 32;
+constexpr int kTile = 64;
+
+__global__ void __launch_bounds__(kWideThreads)
+k_factor_wide(SnDev sd, FactorDev fd, const double* __restrict__ kval,
+              const int* __restrict__ nodes, double eps) {
+  __shared__ double As[kPanel][kTile + 1];
+  __shared__ double Bs[kPanel][kTile + 1];
+  __shared__ double colp[kPanel];
+  const int s = nodes[blockIdx.x];
+  const int c0 = sd.first[s], k = sd.first[s + 1] - c0, f = sd.f[s];
+  const int tid = threadIdx.x, nth = blockDim.x;
+  double* F = fd.scratch + sd.scr_off[s];
+  const size_t ff = static_cast<size_t>(f) * f;
+  for (size_t i = tid; i < ff; i += nth) F[i] = 0.0;
+  __syncthreads();
+  for (int a = sd.asm_ptr[s] + tid; a < sd.asm_ptr[s + 1]; a += nth) {
+    const int pos = sd.asm_pos[a];
+    F[(pos & 0xffff) + static_cast<size_t>(pos >> 16) * f] += kval[sd.asm_slot[a]];
+  }
+  __syncthreads();
+  for (int cc = sd.ch_ptr[s]; cc < sd.ch_ptr[s + 1]; ++cc) {
+    const int c = sd.ch[cc];
+    const int fu = sd.u_ld[c];
+    const int* rel = sd.rel + sd.rel_ptr[c];
+    const double* U = fd.upd + sd.u_off[c];
+    const size_t tot = static_cast<size_t>(fu) * fu;
+    for (size_t idx = tid; idx < tot; idx += nth) {
+      const int i = static_cast<int>(idx % fu), j = static_cast<int>(idx / fu);
+      if (i >= j) F[rel[i] + static_cast<size_t>(rel[j]) * f] += __ldcg(U + idx);
+    }
+    __syncthreads();
+  }
+  double* Lb = fd.lval + sd.l_off[s];
+  int npos = 0, nneg = 0, pert = 0, fail = 0;
+  for (int p0 = 0; p0 < k; p0 += kPanel) {
+    const int p1 = min(p0 + kPanel, k);
+    for (int p = p0; p < p1; ++p) {
+      __syncthreads();
+      double dp = F[p + static_cast<size_t>(p) * f];
+      int pflag = 0;
+      if (fabs(dp) < eps) {
+        dp = (dp >= 0.0) ? eps : -eps;
+        pflag = 1;
+      }
+      if (tid < p1 - p - 1) colp[tid] = F[(p + 1 + tid) + static_cast<size_t>(p) * f];
+      __syncthreads();
+      for (int r = p + 1 + tid; r < f; r += nth) {
+        const double l = F[r + static_cast<size_t>(p) * f] / dp;
+        Lb[r + static_cast<size_t>(p) * f] = l;
+        if (!isfinite(l)) fail = 1;
+        const int jmax = min(p1 - 1, r);
+        for (int j = p + 1; j <= jmax; ++j)
+          F[r + static_cast<size_t>(j) * f] -= l * colp[j - p - 1];
+      }
+      if (tid == 0) {
+        fd.d[c0 + p] = dp;
+        pert += pflag;
+        if (!isfinite(dp) || dp == 0.0) fail = 1;
+        if (dp > 0.0)
+          npos++;
+        else
+          nneg++;
+      }
+    }
+    __syncthreads();
+    // trailing update F[r][c] -= sum_q L[r][q] * F[c][q], p1 <= c <= r < f
+    const int nb = p1 - p0;
+    const int mt = f - p1;
+    if (mt <= 0) continue;
+    const int T = (mt + kTile - 1) / kTile;
+    const int tr = tid / 16, tc = tid % 16;
+    for (int ti = 0; ti < T; ++ti)
+      for (int tj = 0; tj <= ti; ++tj) {
+        const int r0 = p1 + ti * kTile, q0 = p1 + tj * kTile;
+        for (int idx = tid; idx < kTile * nb; idx += nth) {
+          const int rr = idx % kTile, qq = idx / kTile;
+          const int ra = r0 + rr, rb = q0 + rr;
+          As[qq][rr] = ra < f ? Lb[ra + static_cast<size_t>(p0 + qq) * f] : 0.0;
+          Bs[qq][rr] = rb < f ? F[rb + static_cast<size_t>(p0 + qq) * f] : 0.0;
+        }
+        __syncthreads();
+        double acc[4][4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+        for (int qq = 0; qq < nb; ++qq) {
+          double a[4], b[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) a[i] = As[qq][tr + 16 * i];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) b[j] = Bs[qq][tc + 16 * j];
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) acc[i][j] += a[i] * b[j];
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int r = r0 + tr + 16 * i, c = q0 + tc + 16 * j;
+            if (r < f && c < f && r >= c) F[r + static_cast<size_t>(c) * f] -= acc[i][j];
+          }
+        __syncthreads();
+      }
+  }
+  __syncthreads();
+  const int fu = f - k;
+  double* Us = fd.upd + sd.u_off[s];
+  const size_t tot = static_cast<size_t>(fu) * fu;
+  for (size_t idx = tid; idx < tot; idx += nth) {
+    const int i = static_cast<int>(idx % fu), j = static_cast<int>(idx / fu);
+    if (i >= j) Us[idx] = F[(k + i) + static_cast<size_t>(k + j) * f];
+  }
+  if (tid == 0) {
+    if (npos) atomicAdd(fd.stats + 0, npos);
+    if (nneg) atomicAdd(fd.stats + 1, nneg);
+    if (pert) atomicAdd(fd.stats + 2, pert);
+  }
+  if (fail) atomicOr(fd.stats + 3, 1);
+}
+
+// ---------------------------------------------------------------------------
+// forward solve L w = b (in place on the permuted vector w); update vectors of
+// the multifrontal solve live at uvec + rel_ptr[s] (f - k entries)
+__global__ void __launch_bounds__(kWarpsPerCta * 32)
+k_fwd_warp(SnDev sd, const double* __restrict__ lval, double* w, double* uvec,
+           int* flags, int epoch, int* counter, int npaths) {
+  __shared__ double Ts[kWarpsPerCta][kWF];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  double* T = Ts[wid];
+  for (;;) {
+    const int pi = next_path(counter, lane);
+    if (pi >= npaths) break;
+    for (int q = sd.path_ptr[pi]; q < sd.path_ptr[pi + 1]; ++q) {
+      const int s = sd.path_nodes[q];
+      const int c0 = sd.first[s], k = sd.first[s + 1] - c0, f = sd.f[s];
+      const int chb = sd.ch_ptr[s], che = sd.ch_ptr[s + 1];
+      for (int c = chb + lane; c < che; c += 32)
+        while (ld_acquire(flags + sd.ch[c]) != epoch) {
+        }
+      __syncwarp();
+      T[lane] = (lane < k) ? __ldcg(w + c0 + lane) : 0.0;
+      __syncwarp();
+      for (int cc = chb; cc < che; ++cc) {
+        const int c = sd.ch[cc];
+        const int fu = sd.u_ld[c];
+        if (lane < fu) T[sd.rel[sd.rel_ptr[c] + lane]] += __ldcg(uvec + sd.rel_ptr[c] + lane);
+        __syncwarp();
+      }
+      double t = (lane < f) ? T[lane] : 0.0;
+      const double* Lb = lval + sd.l_off[s];
+      for (int p = 0; p < k; ++p) {
+        const double lv = (lane > p && lane < f) ? Lb[lane + static_cast<size_t>(p) * f] : 0.0;
+        const double wp = __shfl_sync(0xffffffffu, t, p);
+        t -= lv * wp;
+      }
+      if (lane < k)
+        w[c0 + lane] = t;
+      else if (lane < f)
+        uvec[sd.rel_ptr[s] + lane - k] = t;
+      publish(flags + s, epoch, lane);
+    }
+  }
+}
+
+// backward solve L^T x = D^-1 w, paths taken in reverse order, top-down
+__global__ void __launch_bounds__(kWarpsPerCta * 32)
+k_bwd_warp(SnDev sd, const double* __restrict__ lval, const double* __restrict__ d,
+           const double* __restrict__ w, double* x, int* flags, int epoch,
+           const int8_t* __restrict__ wide, int* counter, int npaths) {
+  const int lane = threadIdx.x & 31;
+  for (;;) {
+    const int pj = next_path(counter, lane);
+    if (pj >= npaths) break;
+    const int pi = npaths - 1 - pj;
+    const int pb = sd.path_ptr[pi], pe = sd.path_ptr[pi + 1];
+    {
+      const int top = sd.path_nodes[pe - 1];
+      const int par = sd.sparent[top];
+      if (par >= 0 && !wide[par] && lane == 0)
+        while (ld_acquire(flags + par) != epoch) {
+        }
+      __syncwarp();
+    }
+    for (int q = pe - 1; q >= pb; --q) {
+      const int s = sd.path_nodes[q];
+      const int c0 = sd.first[s], k = sd.first[s + 1] - c0, f = sd.f[s];
+      double xr = 0.0;
+      if (lane >= k && lane < f) xr = __ldcg(x + sd.rows[sd.rows_ptr[s] + lane]);
+      const double zr = (lane < k) ? w[c0 + lane] / d[c0 + lane] : 0.0;
+      const double* Lb = lval + sd.l_off[s];
+      for (int p = k - 1; p >= 0; --p) {
+        const double part = (lane > p && lane < f) ? Lb[lane + static_cast<size_t>(p) * f] * xr : 0.0;
+        const double sum = warp_sum(part);
+        const double xp = __shfl_sync(0xffffffffu, zr, p) - sum;
+        if (lane == p) xr = xp;
+      }
+      if (lane < k) x[c0 + lane] = xr;
+      publish(flags + s, epoch, lane);
+    }
+  }
+}
+
+// wide-tier forward solve (one CTA per front of a level)
+__global__ void __launch_bounds__(kWideThreads)
+k_fwd_wide(SnDev sd, const double* __restrict__ lval, double* w, double* uvec,
+           const int* __restrict__ nodes) {
+  extern __shared__ double T[];
+  const int s = nodes[blockIdx.x];
+  const int c0 = sd.first[s], k = sd.first[s + 1] - c0, f = sd.f[s];
+  const int tid = threadIdx.x, nth = blockDim.x;
+  for (int r = tid; r < f; r += nth) T[r] = r < k ? w[c0 + r] : 0.0;
+  __syncthreads();
+  for (int cc = sd.ch_ptr[s]; cc < sd.ch_ptr[s + 1]; ++cc) {
+    const int c = sd.ch[cc];
+    const int fu = sd.u_ld[c];
+    for (int i = tid; i < fu; i += nth)
+      T[sd.rel[sd.rel_ptr[c] + i]] += uvec[sd.rel_ptr[c] + i];
+    __syncthreads();
+  }
+  const double* Lb = lval + sd.l_off[s];
+  for (int p = 0; p < k; ++p) {
+    const double wp = T[p];
+    for (int r = p + 1 + tid; r < f; r += nth) T[r] -= Lb[r + static_cast<size_t>(p) * f] * wp;
+    __syncthreads();
+  }
+  for (int r = tid; r < f; r += nth) {
+    if (r < k)
+      w[c0 + r] = T[r];
+    else
+      uvec[sd.rel_ptr[s] + r - k] = T[r];
+  }
+}
+
+// wide-tier backward solve (one CTA per front of a level, levels top-down)
+__global__ void __launch_bounds__(kWideThreads)
+k_bwd_wide(SnDev sd, const double* __restrict__ lval, const double* __restrict__ d,
+           const double* __restrict__ w, double* x, const int* __restrict__ nodes) {
+  extern __shared__ double X[];
+  const int s = nodes[blockIdx.x];
+  const int c0 = sd.first[s], k = sd.first[s + 1] - c0, f = sd.f[s];
+  const int tid = threadIdx.x, nth = blockDim.x;
+  const int lane = tid & 31, warp = tid >> 5, nwarps = nth >> 5;
+  const int* rows = sd.rows + sd.rows_ptr[s];
+  for (int r = tid; r < f; r += nth)
+    X[r] = r < k ? w[c0 + r] / d[c0 + r] : x[rows[r]];
+  __syncthreads();
+  const double* Lb = lval + sd.l_off[s];
+  for (int p = warp; p < k; p += nwarps) {
+    double part = 0.0;
+    for (int r = k + lane; r < f; r += 32) part += Lb[r + static_cast<size_t>(p) * f] * X[r];
+    part = warp_sum(part);
+    if (lane == 0) X[p] -= part;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    for (int p = k - 1; p >= 0; --p) {
+      double part = 0.0;
+      for (int r = p + 1 + lane; r < k; r += 32) part += Lb[r + static_cast<size_t>(p) * f] * X[r];
+      part = warp_sum(part);
+      if (lane == 0) X[p] -= part;
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+  for (int r = tid; r < k; r += nth) x[c0 + r] = X[r];
+}
+
+__global__ void k_permute_in(int n, const int* __restrict__ perm,
+                             const double* __restrict__ b, double* w) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) w[i] = b[perm[i]];
+}
+
+__global__ void k_permute_out(int n, const int* __restrict__ perm,
+                              const double* __restrict__ xp, double* x) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) x[perm[i]] = xp[i];
+}
+
+// ---------------------------------------------------------------------------
+// launch helpers (host)
+void launch_factor_warp(const SnDev& sd, const FactorDev& fd, const double* kval,
+                        int* flags, int epoch, int* counter, int npaths,
+                        double eps, int grid, cudaStream_t st) {
+  if (npaths == 0) return;
+  k_factor_warp<<<grid, kWarpsPerCta * 32, 0, st>>>(sd, fd, kval, flags, epoch,
+                                                   counter, npaths, eps);
+}
+
+void launch_factor_wide(const SnDev& sd, const FactorDev& fd, const double* kval,
+                        const int* nodes, int count, double eps, cudaStream_t st) {
+  if (count == 0) return;
+  k_factor_wide<<<count, kWideThreads, 0, st>>>(sd, fd, kval, nodes, eps);
+}
+
+void launch_fwd_warp(const SnDev& sd, const double* lval, double* w, double* uvec,
+                     int* flags, int epoch, int* counter, int npaths, int grid,
+                     cudaStream_t st) {
+  if (npaths == 0) return;
+  k_fwd_warp<<<grid, kWarpsPerCta * 32, 0, st>>>(sd, lval, w, uvec, flags, epoch,
+                                                counter, npaths);
+}
+
+void launch_bwd_warp(const SnDev& sd, const double* lval, const double* d,
+                     const double* w, double* x, int* flags, int epoch,
+                     const int8_t* wide, int* counter, int npaths, int grid,
+                     cudaStream_t st) {
+  if (npaths == 0) return;
+  k_bwd_warp<<<grid, kWarpsPerCta * 32, 0, st>>>(sd, lval, d, w, x, flags, epoch,
+                                                wide, counter, npaths);
+}
+
+void launch_fwd_wide(const SnDev& sd, const double* lval, double* w, double* uvec,
+                     const int* nodes, int count, int max_f, cudaStream_t st) {
+  if (count == 0) return;
+  k_fwd_wide<<<count, kWideThreads, sizeof(double) * max_f, st>>>(sd, lval, w, uvec, nodes);
+}
+
+void launch_bwd_wide(const SnDev& sd, const double* lval, const double* d,
+                     const double* w, double* x, const int* nodes, int count,
+                     int max_f, cudaStream_t st) {
+  if (count == 0) return;
+  k_bwd_wide<<<count, kWideThreads, sizeof(double) * max_f, st>>>(sd, lval, d, w, x, nodes);
+}
+
+void launch_permute_in(int n, const int* perm, const double* b, double* w,
+                       cudaStream_t st) {
+  if (n == 0) return;
+  k_permute_in<<<(n + 255) / 256, 256, 0, st>>>(n, perm, b, w);
+}
+
+void launch_permute_out(int n, const int* perm, const double* xp, double* x,
+                        cudaStream_t st) {
+  if (n == 0) return;
+  k_permute_out<<<(n + 255) / 256, 256, 0, st>>>(n, perm, xp, x);
+}
+
+void set_wide_smem_limit(int max_f) {
+  const int bytes = static_cast<int>(sizeof(double)) * (max_f > 0 ? max_f : 1);
+  if (bytes > 48 * 1024) {
+    cudaFuncSetAttribute(k_fwd_wide, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    cudaFuncSetAttribute(k_bwd_wide, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  }
+}
+
+int warp_tier_grid() {
+  int dev = 0, sms = 0, per_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_factor_warp,
+                                                kWarpsPerCta * 32, 0);
+  int a = 0, b = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, k_fwd_warp, kWarpsPerCta * 32, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_bwd_warp, kWarpsPerCta * 32, 0);
+  per_sm = per_sm < a ? per_sm : a;
+  per_sm = per_sm < b ? per_sm : b;
+  if (per_sm < 1) per_sm = 1;
+  return sms * per_sm;
+}
+
+}  // namespace nclb

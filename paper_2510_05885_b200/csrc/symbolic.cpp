@@ -1,0 +1,693 @@
+// Host symbolic analysis (see symbolic.hpp).
+#include "symbolic.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+#include <stdexcept>
+
+namespace nclb {
+
+// ---------------------------------------------------------------------------
+// sym_from_triplets (proj/src/sparse.cpp:33-68): mirror upper entries, sort by
+// (col,row), merge duplicates.  Only the pattern is needed here: KktContext
+// builds its matrix from zero-valued triplets (kkt.cpp:93).
+LowerCsc sym_lower_from_pattern(int n, const std::vector<int>& rows,
+                                const std::vector<int>& cols,
+                                std::vector<int>* slot_of_triplet) {
+  if (rows.size() != cols.size())
+    throw std::invalid_argument("sym_from_triplets: length mismatch");
+  const size_t nt = rows.size();
+  std::vector<long long> key(nt);
+  for (size_t k = 0; k < nt; ++k) {
+    int i = rows[k], j = cols[k];
+    if (i < 0 || i >= n || j < 0 || j >= n)
+      throw std::invalid_argument("sym_from_triplets: index out of range");
+    if (i < j) std::swap(i, j);
+    key[k] = (static_cast<long long>(j) << 32) | static_cast<unsigned>(i);
+  }
+  std::vector<int> order(nt);
+  std::iota(order.begin(), order.end(), 0);
+  std::stable_sort(order.begin(), order.end(),
+                   [&](int a, int b) { return key[a] < key[b]; });
+  LowerCsc A;
+  A.n = n;
+  A.col_ptr.assign(static_cast<size_t>(n) + 1, 0);
+  if (slot_of_triplet) slot_of_triplet->assign(nt, -1);
+  long long prev = -1;
+  for (size_t q = 0; q < nt; ++q) {
+    const long long kq = key[order[q]];
+    if (q == 0 || kq != prev) {
+      A.col_ptr[static_cast<size_t>(kq >> 32) + 1]++;
+      A.row_ind.push_back(static_cast<int>(kq & 0xffffffffLL));
+      prev = kq;
+    }
+    if (slot_of_triplet)
+      (*slot_of_triplet)[order[q]] = static_cast<int>(A.row_ind.size()) - 1;
+  }
+  for (int j = 0; j < n; ++j) A.col_ptr[j + 1] += A.col_ptr[j];
+  return A;
+}
+
+// ---------------------------------------------------------------------------
+// Approximate minimum degree, restating Eigen's AMDOrdering<int>
+// (Eigen/src/OrderingMethods/Amd.h: internal::minimum_degree_ordering, a port
+// of CSparse cs_amd) on the pattern of A^T + A with the diagonal kept, as
+// proj/src/sparse.cpp:81-100 calls it.  Quotient-graph elimination with
+// approximate external degrees, aggressive absorption, hash-based
+// indistinguishable-node detection and mass elimination; Eigen's structural
+// diagonal rule (a node without a diagonal entry, or denser than
+// max(16, 10 sqrt n) capped at n-2, is absorbed into the dummy root n); the
+// permutation is the postorder of the assembly tree.
+namespace {
+
+struct AmdState {
+  int n;
+  std::vector<int> Cp, Ci, len, nv, next, head, elen, degree, w, hhead, last;
+};
+
+inline int flip(int i) { return -i - 2; }
+
+int wclear(int mark, int lemax, std::vector<int>& w, int n) {
+  if (mark < 2 || (mark + lemax < 0)) {
+    for (int k = 0; k < n; k++)
+      if (w[k] != 0) w[k] = 1;
+    mark = 2;
+  }
+  return mark;
+}
+
+int tdfs(int j, int k, std::vector<int>& head, const std::vector<int>& next,
+         std::vector<int>& post, std::vector<int>& stack) {
+  int top = 0;
+  stack[0] = j;
+  while (top >= 0) {
+    const int p = stack[top];
+    const int i = head[p];
+    if (i == -1) {
+      top--;
+      post[k++] = p;
+    } else {
+      head[p] = next[i];
+      stack[++top] = i;
+    }
+  }
+  return k;
+}
+
+std::vector<int> min_degree(int n, const std::vector<int>& Ap,
+                            const std::vector<int>& Ai) {
+  std::vector<int> P(static_cast<size_t>(n) + 1, 0);
+  if (n == 0) return {};
+  int dense = std::max(16, static_cast<int>(10 * std::sqrt(static_cast<double>(n))));
+  dense = std::min(n - 2, dense);
+  int cnz = Ap[n];
+  const int nzmax = cnz + cnz / 5 + 2 * n;
+  std::vector<int> Cp(Ap.begin(), Ap.end());
+  std::vector<int> Ci(static_cast<size_t>(nzmax), 0);
+  std::copy(Ai.begin(), Ai.begin() + cnz, Ci.begin());
+  const size_t n1 = static_cast<size_t>(n) + 1;
+  std::vector<int> len(n1), nv(n1), next(n1), head(n1), elen(n1), degree(n1),
+      w(n1), hhead(n1);
+  std::vector<int>& last = P;
+  for (int k = 0; k < n; k++) len[k] = Cp[k + 1] - Cp[k];
+  len[n] = 0;
+  for (int i = 0; i <= n; i++) {
+    head[i] = -1;
+    last[i] = -1;
+    next[i] = -1;
+    hhead[i] = -1;
+    nv[i] = 1;
+    w[i] = 1;
+    elen[i] = 0;
+    degree[i] = len[i];
+  }
+  int mark = wclear(0, 0, w, n);
+  int nel = 0, mindeg = 0, lemax = 0;
+  for (int i = 0; i < n; i++) {
+    bool has_diag = false;
+    for (int p = Cp[i]; p < Cp[i + 1]; ++p)
+      if (Ci[p] == i) {
+        has_diag = true;
+        break;
+      }
+    const int d = degree[i];
+    if (d == 1 && has_diag) {
+      elen[i] = -2;
+      nel++;
+      Cp[i] = -1;
+      w[i] = 0;
+    } else if (d > dense || !has_diag) {
+      nv[i] = 0;
+      elen[i] = -1;
+      nel++;
+      Cp[i] = flip(n);
+      nv[n]++;
+    } else {
+      if (head[d] != -1) last[head[d]] = i;
+      next[i] = head[d];
+      head[d] = i;
+    }
+  }
+  elen[n] = -2;
+  Cp[n] = -1;
+  w[n] = 0;
+
+  while (nel < n) {
+    int k = -1;
+    for (; mindeg < n && (k = head[mindeg]) == -1; mindeg++) {
+    }
+    if (next[k] != -1) last[next[k]] = -1;
+    head[mindeg] = next[k];
+    const int elenk = elen[k];
+    int nvk = nv[k];
+    nel += nvk;
+
+    if (elenk > 0 && cnz + mindeg >= nzmax) {  // garbage collection
+      for (int j = 0; j < n; j++) {
+        int p;
+        if ((p = Cp[j]) >= 0) {
+          Cp[j] = Ci[p];
+          Ci[p] = flip(j);
+        }
+      }
+      int q = 0;
+      for (int p = 0; p < cnz;) {
+        int j;
+        if ((j = flip(Ci[p++])) >= 0) {
+          Ci[q] = Cp[j];
+          Cp[j] = q++;
+          for (int k3 = 0; k3 < len[j] - 1; k3++) Ci[q++] = Ci[p++];
+        }
+      }
+      cnz = q;
+    }
+
+    int dk = 0;  // construct the new element
+    nv[k] = -nvk;
+    int p = Cp[k];
+    const int pk1 = (elenk == 0) ? p : cnz;
+    int pk2 = pk1;
+    for (int k1 = 1; k1 <= elenk + 1; k1++) {
+      int e, pj, ln;
+      if (k1 > elenk) {
+        e = k;
+        pj = p;
+        ln = len[k] - elenk;
+      } else {
+        e = Ci[p++];
+        pj = Cp[e];
+        ln = len[e];
+      }
+      for (int k2 = 1; k2 <= ln; k2++) {
+        const int i = Ci[pj++];
+        int nvi;
+        if ((nvi = nv[i]) <= 0) continue;
+        dk += nvi;
+        nv[i] = -nvi;
+        Ci[pk2++] = i;
+        if (next[i] != -1) last[next[i]] = last[i];
+        if (last[i] != -1)
+          next[last[i]] = next[i];
+        else
+          head[degree[i]] = next[i];
+      }
+      if (e != k) {
+        Cp[e] = flip(k);
+        w[e] = 0;
+      }
+    }
+    if (elenk != 0) cnz = pk2;
+    degree[k] = dk;
+    Cp[k] = pk1;
+    len[k] = pk2 - pk1;
+    elen[k] = -2;
+
+    mark = wclear(mark, lemax, w, n);  // set differences |Le \ Lk|
+    for (int pk = pk1; pk < pk2; pk++) {
+      const int i = Ci[pk];
+      const int eln = elen[i];
+      if (eln <= 0) continue;
+      const int nvi = -nv[i];
+      const int wnvi = mark - nvi;
+      for (p = Cp[i]; p <= Cp[i] + eln - 1; p++) {
+        const int e = Ci[p];
+        if (w[e] >= mark)
+          w[e] -= nvi;
+        else if (w[e] != 0)
+          w[e] = degree[e] + wnvi;
+      }
+    }
+
+    for (int pk = pk1; pk < pk2; pk++) {  // degree update
+      const int i = Ci[pk];
+      const int p1 = Cp[i];
+      const int p2 = p1 + elen[i] - 1;
+      int pn = p1;
+      int h = 0, d = 0;
+      for (p = p1; p <= p2; p++) {
+        const int e = Ci[p];
+        if (w[e] != 0) {
+          const int dext = w[e] - mark;
+          if (dext > 0) {
+            d += dext;
+            Ci[pn++] = e;
+            h += e;
+          } else {
+            Cp[e] = flip(k);
+            w[e] = 0;
+          }
+        }
+      }
+      elen[i] = pn - p1 + 1;
+      const int p3 = pn;
+      const int p4 = p1 + len[i];
+      for (p = p2 + 1; p < p4; p++) {
+        const int j = Ci[p];
+        int nvj;
+        if ((nvj = nv[j]) <= 0) continue;
+        d += nvj;
+        Ci[pn++] = j;
+        h += j;
+      }
+      if (d == 0) {  // mass elimination
+        Cp[i] = flip(k);
+        const int nvi = -nv[i];
+        dk -= nvi;
+        nvk += nvi;
+        nel += nvi;
+        nv[i] = 0;
+        elen[i] = -1;
+      } else {
+        degree[i] = std::min(degree[i], d);
+        Ci[pn] = Ci[p3];
+        Ci[p3] = Ci[p1];
+        Ci[p1] = k;
+        len[i] = pn - p1 + 1;
+        h = ((h < 0) ? (-h) : h) % n;
+        next[i] = hhead[h];
+        hhead[h] = i;
+        last[i] = h;
+      }
+    }
+    degree[k] = dk;
+    lemax = std::max(lemax, dk);
+    mark = wclear(mark + lemax, lemax, w, n);
+
+    for (int pk = pk1; pk < pk2; pk++) {  // supernode detection
+      int i = Ci[pk];
+      if (nv[i] >= 0) continue;
+      const int h = last[i];
+      i = hhead[h];
+      hhead[h] = -1;
+      for (; i != -1 && next[i] != -1; i = next[i], mark++) {
+        const int ln = len[i];
+        const int eln = elen[i];
+        for (p = Cp[i] + 1; p <= Cp[i] + ln - 1; p++) w[Ci[p]] = mark;
+        int jlast = i;
+        for (int j = next[i]; j != -1;) {
+          bool ok = (len[j] == ln) && (elen[j] == eln);
+          for (p = Cp[j] + 1; ok && p <= Cp[j] + ln - 1; p++)
+            if (w[Ci[p]] != mark) ok = false;
+          if (ok) {
+            Cp[j] = flip(i);
+            nv[i] += nv[j];
+            nv[j] = 0;
+            elen[j] = -1;
+            j = next[j];
+            next[jlast] = j;
+          } else {
+            jlast = j;
+            j = next[j];
+          }
+        }
+      }
+    }
+
+    int pq = pk1;  // finalize the new element
+    for (int pk = pk1; pk < pk2; pk++) {
+      const int i = Ci[pk];
+      int nvi;
+      if ((nvi = -nv[i]) <= 0) continue;
+      nv[i] = nvi;
+      int d = degree[i] + dk - nvi;
+      d = std::min(d, n - nel - nvi);
+      if (head[d] != -1) last[head[d]] = i;
+      next[i] = head[d];
+      last[i] = -1;
+      head[d] = i;
+      mindeg = std::min(mindeg, d);
+      degree[i] = d;
+      Ci[pq++] = i;
+    }
+    nv[k] = nvk;
+    if ((len[k] = pq - pk1) == 0) {
+      Cp[k] = -1;
+      w[k] = 0;
+    }
+    if (elenk != 0) cnz = pq;
+  }
+
+  for (int i = 0; i < n; i++) Cp[i] = flip(Cp[i]);  // postorder
+  for (int j = 0; j <= n; j++) head[j] = -1;
+  for (int j = n; j >= 0; j--) {
+    if (nv[j] > 0) continue;
+    next[j] = head[Cp[j]];
+    head[Cp[j]] = j;
+  }
+  for (int e = n; e >= 0; e--) {
+    if (nv[e] <= 0) continue;
+    if (Cp[e] != -1) {
+      next[e] = head[Cp[e]];
+      head[Cp[e]] = e;
+    }
+  }
+  std::vector<int> post(n1), stack(n1);
+  for (int k = 0, i = 0; i <= n; i++)
+    if (Cp[i] == -1) k = tdfs(i, k, head, next, post, stack);
+  post.resize(static_cast<size_t>(n));
+  return post;
+}
+
+}  // namespace
+
+std::vector<int> amd_order(const LowerCsc& A) {
+  const int n = A.n;
+  // full symmetric pattern, rows sorted (mirrored rows < j, then lower part)
+  std::vector<int> cnt(static_cast<size_t>(n), 0);
+  for (int j = 0; j < n; ++j)
+    for (int p = A.col_ptr[j]; p < A.col_ptr[j + 1]; ++p) {
+      cnt[j]++;
+      if (A.row_ind[p] != j) cnt[A.row_ind[p]]++;
+    }
+  std::vector<int> Mp(static_cast<size_t>(n) + 1, 0);
+  for (int j = 0; j < n; ++j) Mp[j + 1] = Mp[j] + cnt[j];
+  std::vector<int> Mi(static_cast<size_t>(Mp[n]));
+  std::vector<int> nx(Mp.begin(), Mp.end() - 1);
+  for (int r = 0; r < n; ++r)
+    for (int p = A.col_ptr[r]; p < A.col_ptr[r + 1]; ++p)
+      if (A.row_ind[p] != r) Mi[nx[A.row_ind[p]]++] = r;
+  for (int j = 0; j < n; ++j)
+    for (int p = A.col_ptr[j]; p < A.col_ptr[j + 1]; ++p)
+      Mi[nx[j]++] = A.row_ind[p];
+  return min_degree(n, Mp, Mi);
+}
+
+// ---------------------------------------------------------------------------
+// analyze_with_permutation (proj/src/sparse.cpp:102-176)
+Symbolic analyze_with_permutation(const LowerCsc& A,
+                                  const std::vector<int>& perm) {
+  const int n = A.n;
+  for (int j = 0; j < n; ++j) {
+    if (A.col_ptr[j] > A.col_ptr[j + 1])
+      throw std::invalid_argument("sparse: col_ptr not nondecreasing");
+    for (int p = A.col_ptr[j]; p < A.col_ptr[j + 1]; ++p) {
+      if (A.row_ind[p] < j || A.row_ind[p] >= n)
+        throw std::invalid_argument("sparse: row index outside lower triangle");
+      if (p > A.col_ptr[j] && A.row_ind[p] <= A.row_ind[p - 1])
+        throw std::invalid_argument("sparse: rows not strictly increasing");
+    }
+  }
+  if (static_cast<int>(perm.size()) != n)
+    throw std::invalid_argument("analyze: permutation length mismatch");
+  Symbolic S;
+  S.n = n;
+  S.perm = perm;
+  S.iperm.assign(static_cast<size_t>(n), -1);
+  for (int k = 0; k < n; ++k) {
+    if (perm[k] < 0 || perm[k] >= n || S.iperm[perm[k]] != -1)
+      throw std::invalid_argument("analyze: not a permutation");
+    S.iperm[perm[k]] = k;
+  }
+  const int nnz = A.nnz();
+  // permuted upper pattern by column; a_map = orig slot -> sorted slot
+  std::vector<int> acp(static_cast<size_t>(n) + 1, 0);
+  for (int j = 0; j < n; ++j)
+    for (int p = A.col_ptr[j]; p < A.col_ptr[j + 1]; ++p)
+      acp[std::max(S.iperm[A.row_ind[p]], S.iperm[j]) + 1]++;
+  for (int c = 0; c < n; ++c) acp[c + 1] += acp[c];
+  std::vector<long long> key(static_cast<size_t>(nnz));
+  std::vector<int> nx(acp.begin(), acp.end() - 1), orig(static_cast<size_t>(nnz));
+  std::vector<int> ari(static_cast<size_t>(nnz));
+  for (int j = 0; j < n; ++j)
+    for (int p = A.col_ptr[j]; p < A.col_ptr[j + 1]; ++p) {
+      const int pi = S.iperm[A.row_ind[p]], pj = S.iperm[j];
+      const int s = nx[std::max(pi, pj)]++;
+      ari[s] = std::min(pi, pj);
+      orig[s] = p;
+    }
+  S.a_map.assign(static_cast<size_t>(nnz), 0);
+  std::vector<std::pair<int, int>> buf;
+  for (int c = 0; c < n; ++c) {
+    buf.clear();
+    for (int s = acp[c]; s < acp[c + 1]; ++s) buf.emplace_back(ari[s], orig[s]);
+    std::sort(buf.begin(), buf.end());
+    for (int k = 0; k < static_cast<int>(buf.size()); ++k) {
+      ari[acp[c] + k] = buf[k].first;
+      S.a_map[buf[k].second] = acp[c] + k;
+    }
+  }
+  // elimination tree + column counts by up-looking reach
+  S.parent.assign(static_cast<size_t>(n), -1);
+  std::vector<int> lnz(static_cast<size_t>(n), 0), flag(static_cast<size_t>(n), -1);
+  for (int k = 0; k < n; ++k) {
+    flag[k] = k;
+    for (int p = acp[k]; p < acp[k + 1]; ++p) {
+      int i = ari[p];
+      if (i >= k) continue;
+      while (flag[i] != k) {
+        if (S.parent[i] == -1) S.parent[i] = k;
+        lnz[i]++;
+        flag[i] = k;
+        i = S.parent[i];
+      }
+    }
+  }
+  S.lcol_ptr.assign(static_cast<size_t>(n) + 1, 0);
+  for (int c = 0; c < n; ++c) S.lcol_ptr[c + 1] = S.lcol_ptr[c] + lnz[c];
+  return S;
+}
+
+// ---------------------------------------------------------------------------
+// Fundamental supernodes, front structures, maps and schedules.
+Supernodal build_supernodal(const LowerCsc& A, const Symbolic& S) {
+  const int n = S.n;
+  Supernodal T;
+  T.n = n;
+  std::vector<int> cnt(static_cast<size_t>(n)), nchild(static_cast<size_t>(n), 0);
+  for (int j = 0; j < n; ++j) {
+    cnt[j] = S.lcol_ptr[j + 1] - S.lcol_ptr[j];
+    if (S.parent[j] >= 0) nchild[S.parent[j]]++;
+    T.flops += static_cast<long long>(cnt[j]) * (cnt[j] + 2);
+  }
+  // fundamental supernodes: j+1 continues j iff parent[j] == j+1, j+1 has
+  // j as its only child and count(j) == count(j+1) + 1
+  T.first.push_back(0);
+  for (int j = 1; j < n; ++j) {
+    const bool cont = S.parent[j - 1] == j && nchild[j] == 1 &&
+                      cnt[j - 1] == cnt[j] + 1 &&
+                      (j - T.first.back()) < 1024;
+    if (!cont) T.first.push_back(j);
+  }
+  if (n > 0) T.first.push_back(n);
+  T.nsn = n > 0 ? static_cast<int>(T.first.size()) - 1 : 0;
+  if (n == 0) T.first.assign(1, 0);
+  const int nsn = T.nsn;
+  std::vector<int> col2sn(static_cast<size_t>(n));
+  for (int s = 0; s < nsn; ++s)
+    for (int c = T.first[s]; c < T.first[s + 1]; ++c) col2sn[c] = s;
+  T.sparent.assign(static_cast<size_t>(nsn), -1);
+  T.f.assign(static_cast<size_t>(nsn), 0);
+  for (int s = 0; s < nsn; ++s) {
+    const int last = T.first[s + 1] - 1;
+    const int p = S.parent[last];
+    T.sparent[s] = p >= 0 ? col2sn[p] : -1;
+    T.f[s] = (T.first[s + 1] - T.first[s]) + cnt[last];
+  }
+  // children lists (increasing)
+  T.ch_ptr.assign(static_cast<size_t>(nsn) + 1, 0);
+  for (int s = 0; s < nsn; ++s)
+    if (T.sparent[s] >= 0) T.ch_ptr[T.sparent[s] + 1]++;
+  for (int s = 0; s < nsn; ++s) T.ch_ptr[s + 1] += T.ch_ptr[s];
+  T.ch.assign(static_cast<size_t>(T.ch_ptr[nsn]), 0);
+  {
+    std::vector<int> nx(T.ch_ptr.begin(), T.ch_ptr.end() - 1);
+    for (int s = 0; s < nsn; ++s)
+      if (T.sparent[s] >= 0) T.ch[nx[T.sparent[s]]++] = s;
+  }
+  // permuted lower pattern by column: (row, slot of A)
+  std::vector<int> lcp(static_cast<size_t>(n) + 1, 0);
+  for (int j = 0; j < n; ++j)
+    for (int p = A.col_ptr[j]; p < A.col_ptr[j + 1]; ++p)
+      lcp[std::min(S.iperm[A.row_ind[p]], S.iperm[j]) + 1]++;
+  for (int c = 0; c < n; ++c) lcp[c + 1] += lcp[c];
+  std::vector<int> lri(static_cast<size_t>(A.nnz())), lsl(static_cast<size_t>(A.nnz()));
+  {
+    std::vector<int> nx(lcp.begin(), lcp.end() - 1);
+    for (int j = 0; j < n; ++j)
+      for (int p = A.col_ptr[j]; p < A.col_ptr[j + 1]; ++p) {
+        const int pi = S.iperm[A.row_ind[p]], pj = S.iperm[j];
+        const int q = nx[std::min(pi, pj)]++;
+        lri[q] = std::max(pi, pj);
+        lsl[q] = p;
+      }
+  }
+  // front rows: pivots, then union of A rows and children's update rows
+  T.rows_ptr.assign(static_cast<size_t>(nsn) + 1, 0);
+  std::vector<int> mark(static_cast<size_t>(n), -1), pos(static_cast<size_t>(n), -1);
+  std::vector<int> below;
+  T.asm_ptr.assign(static_cast<size_t>(nsn) + 1, 0);
+  T.rel_ptr.assign(static_cast<size_t>(nsn) + 1, 0);
+  for (int s = 0; s < nsn; ++s) {
+    const int c0 = T.first[s], c1 = T.first[s + 1], k = c1 - c0;
+    below.clear();
+    for (int c = c0; c < c1; ++c)
+      for (int q = lcp[c]; q < lcp[c + 1]; ++q) {
+        const int r = lri[q];
+        if (r >= c1 && mark[r] != s) {
+          mark[r] = s;
+          below.push_back(r);
+        }
+      }
+    for (int q = T.ch_ptr[s]; q < T.ch_ptr[s + 1]; ++q) {
+      const int c = T.ch[q];
+      const int* cr = T.rows.data() + T.rows_ptr[c];
+      const int kc = T.first[c + 1] - T.first[c];
+      for (int i = kc; i < T.f[c]; ++i) {
+        const int r = cr[i];
+        if (r >= c1 && mark[r] != s) {
+          mark[r] = s;
+          below.push_back(r);
+        }
+      }
+    }
+    std::sort(below.begin(), below.end());
+    if (k + static_cast<int>(below.size()) != T.f[s])
+      throw std::logic_error("supernodal: front size disagrees with column counts");
+    for (int c = c0; c < c1; ++c) T.rows.push_back(c);
+    T.rows.insert(T.rows.end(), below.begin(), below.end());
+    T.rows_ptr[s + 1] = static_cast<int>(T.rows.size());
+    const int* rs = T.rows.data() + T.rows_ptr[s];
+    for (int i = 0; i < T.f[s]; ++i) pos[rs[i]] = i;
+    for (int c = c0; c < c1; ++c)
+      for (int q = lcp[c]; q < lcp[c + 1]; ++q) {
+        T.asm_pos.push_back(pos[lri[q]] | ((c - c0) << 16));
+        T.asm_slot.push_back(lsl[q]);
+      }
+    T.asm_ptr[s + 1] = static_cast<int>(T.asm_pos.size());
+    for (int q = T.ch_ptr[s]; q < T.ch_ptr[s + 1]; ++q) {
+      const int c = T.ch[q];
+      const int* cr = T.rows.data() + T.rows_ptr[c];
+      const int kc = T.first[c + 1] - T.first[c];
+      // rel entries of child c are stored contiguously at rel_ptr[c]
+      (void)cr;
+      (void)kc;
+    }
+    T.max_f = std::max(T.max_f, T.f[s]);
+  }
+  // rel maps (need final row lists of parents)
+  for (int c = 0; c < nsn; ++c) {
+    const int kc = T.first[c + 1] - T.first[c];
+    T.rel_ptr[c + 1] = T.rel_ptr[c] + (T.f[c] - kc);
+  }
+  T.rel.assign(static_cast<size_t>(T.rel_ptr[nsn]), 0);
+  for (int s = 0; s < nsn; ++s) {
+    const int* rs = T.rows.data() + T.rows_ptr[s];
+    for (int i = 0; i < T.f[s]; ++i) pos[rs[i]] = i;
+    for (int q = T.ch_ptr[s]; q < T.ch_ptr[s + 1]; ++q) {
+      const int c = T.ch[q];
+      const int* cr = T.rows.data() + T.rows_ptr[c];
+      const int kc = T.first[c + 1] - T.first[c];
+      for (int i = kc; i < T.f[c]; ++i) T.rel[T.rel_ptr[c] + i - kc] = pos[cr[i]];
+    }
+  }
+  // tiers: wide = front above the warp limit, closed upward
+  T.wide.assign(static_cast<size_t>(nsn), 0);
+  for (int s = 0; s < nsn; ++s) {
+    if (T.f[s] > kWarpFront) T.wide[s] = 1;
+    if (T.wide[s] && T.sparent[s] >= 0) T.wide[T.sparent[s]] = 1;
+  }
+  // storage: L blocks (f x k col-major), update blocks
+  T.l_off.assign(static_cast<size_t>(nsn) + 1, 0);
+  T.u_off.assign(static_cast<size_t>(nsn), 0);
+  T.u_ld.assign(static_cast<size_t>(nsn), 0);
+  long long uoff = 0;
+  for (int s = 0; s < nsn; ++s) {
+    const int k = T.first[s + 1] - T.first[s];
+    T.l_off[s + 1] = T.l_off[s] + static_cast<long long>(T.f[s]) * k;
+    const int fu = T.f[s] - k;
+    T.u_off[s] = uoff;
+    T.u_ld[s] = fu;
+    uoff += static_cast<long long>(fu) * fu;
+    if (T.wide[s]) {
+      T.max_wide_f = std::max(T.max_wide_f, T.f[s]);
+      T.wide_front_elems += static_cast<long long>(T.f[s]) * T.f[s];
+    }
+  }
+  T.u_total = uoff;
+  // heights (supernodal), heavy child = child of maximal height
+  std::vector<int> height(static_cast<size_t>(nsn), 0);
+  for (int s = 0; s < nsn; ++s)
+    if (T.sparent[s] >= 0)
+      height[T.sparent[s]] = std::max(height[T.sparent[s]], height[s] + 1);
+  for (int s = 0; s < nsn; ++s) T.sn_height = std::max(T.sn_height, height[s] + 1);
+  std::vector<int> heavy(static_cast<size_t>(nsn), -1);
+  for (int s = 0; s < nsn; ++s) {
+    int best = -1;
+    for (int q = T.ch_ptr[s]; q < T.ch_ptr[s + 1]; ++q) {
+      const int c = T.ch[q];
+      if (T.wide[c]) continue;
+      if (best < 0 || height[c] > height[best]) best = c;
+    }
+    heavy[s] = T.wide[s] ? -1 : best;
+  }
+  // warp-tier paths: tops are narrow nodes that are not the heavy child of a
+  // narrow parent; a path runs from its top down the heavy children
+  std::vector<int> depth(static_cast<size_t>(nsn), 0);
+  for (int s = nsn - 1; s >= 0; --s)
+    depth[s] = T.sparent[s] >= 0 ? depth[T.sparent[s]] + 1 : 0;
+  std::vector<int> tops;
+  for (int s = 0; s < nsn; ++s) {
+    if (T.wide[s]) continue;
+    const int p = T.sparent[s];
+    if (p < 0 || T.wide[p] || heavy[p] != s) tops.push_back(s);
+  }
+  std::stable_sort(tops.begin(), tops.end(),
+                   [&](int a, int b) { return depth[a] > depth[b]; });
+  T.path_ptr.assign(1, 0);
+  std::vector<int> tmp;
+  for (int t : tops) {
+    tmp.clear();
+    for (int s = t; s >= 0; s = heavy[s]) tmp.push_back(s);
+    std::reverse(tmp.begin(), tmp.end());  // bottom -> top
+    T.path_nodes.insert(T.path_nodes.end(), tmp.begin(), tmp.end());
+    T.path_ptr.push_back(static_cast<int>(T.path_nodes.size()));
+  }
+  // wide-tier levels by wide-height (children first)
+  std::vector<int> wl(static_cast<size_t>(nsn), -1);
+  int nlev = 0;
+  for (int s = 0; s < nsn; ++s) {
+    if (!T.wide[s]) continue;
+    int l = 0;
+    for (int q = T.ch_ptr[s]; q < T.ch_ptr[s + 1]; ++q) {
+      const int c = T.ch[q];
+      if (T.wide[c]) l = std::max(l, wl[c] + 1);
+    }
+    wl[s] = l;
+    nlev = std::max(nlev, l + 1);
+  }
+  T.lvl_ptr.assign(static_cast<size_t>(nlev) + 1, 0);
+  for (int s = 0; s < nsn; ++s)
+    if (T.wide[s]) T.lvl_ptr[wl[s] + 1]++;
+  for (int l = 0; l < nlev; ++l) T.lvl_ptr[l + 1] += T.lvl_ptr[l];
+  T.lvl_nodes.assign(static_cast<size_t>(T.lvl_ptr[nlev]), 0);
+  {
+    std::vector<int> nx(T.lvl_ptr.begin(), T.lvl_ptr.end() - 1);
+    for (int s = 0; s < nsn; ++s)
+      if (T.wide[s]) T.lvl_nodes[nx[wl[s]]++] = s;
+  }
+  return T;
+}
+
+}  // namespace nclb

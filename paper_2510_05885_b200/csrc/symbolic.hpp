@@ -1,0 +1,85 @@
+// Host-side symbolic analysis for the sm_100a static-pivot LDL^T.
+//
+// Everything here runs once per KKT pattern (KktContext construction,
+// proj/src/kkt.cpp:41-138) and is bit-exact with the reference where the
+// reference defines a result:
+//   sym_lower_from_pattern  == sym_from_triplets   (proj/src/sparse.cpp:33-68)
+//   amd_order               == Eigen AMDOrdering    (proj/src/sparse.cpp:81-100)
+//   analyze_with_permutation: perm/iperm/parent/lcol_ptr/a_map
+//                                                  (proj/src/sparse.cpp:102-176)
+// and adds the B200-side structures the reference does not have: the
+// fundamental-supernode partition, front row lists, assembly / extend-add
+// maps, the warp tier (fronts <= 32 rows) with its heavy-path schedule, and
+// the level schedule of the wide-front tier.
+#pragma once
+
+#include <cstdint>
+#include <vector>
+
+namespace nclb {
+
+// lower CSC (row >= col, rows strictly increasing per column)
+struct LowerCsc {
+  int n = 0;
+  std::vector<int> col_ptr, row_ind;
+  int nnz() const { return col_ptr.empty() ? 0 : col_ptr[n]; }
+};
+
+// (rows, cols) triplets, upper mirrored, sorted by (col,row), duplicates
+// merged; dup_of[k] = slot of triplet k.
+LowerCsc sym_lower_from_pattern(int n, const std::vector<int>& rows,
+                                const std::vector<int>& cols,
+                                std::vector<int>* slot_of_triplet = nullptr);
+
+std::vector<int> amd_order(const LowerCsc& A);
+
+struct Symbolic {
+  int n = 0;
+  std::vector<int> perm, iperm, parent, lcol_ptr;
+  std::vector<int> a_map;  // orig lower slot -> permuted upper slot
+  long long l_nnz() const { return lcol_ptr.empty() ? 0 : lcol_ptr[n]; }
+};
+
+// throws std::invalid_argument like the reference
+Symbolic analyze_with_permutation(const LowerCsc& A,
+                                  const std::vector<int>& perm);
+
+// Supernodal structure consumed by the CUDA kernels (all indices in the
+// permuted numbering).
+struct Supernodal {
+  int n = 0;
+  int nsn = 0;
+  std::vector<int> first;      // nsn+1: first pivot column of each supernode
+  std::vector<int> f;          // front size (pivots + rows below)
+  std::vector<int> sparent;    // supernodal parent, -1 for roots
+  std::vector<int> rows_ptr;   // nsn+1
+  std::vector<int> rows;       // front rows (global permuted ids)
+  std::vector<long long> l_off;  // nsn+1: offset of the f x k column-major
+                                 // L block (diag: unit, not stored; d apart)
+  std::vector<long long> u_off;  // offset of the update block (ld u_ld)
+  std::vector<int> u_ld;
+  long long u_total = 0;
+  // assembly of A into the front: packed (front_row | front_col << 16), slot
+  std::vector<int> asm_ptr, asm_pos, asm_slot;
+  // children in increasing order and their update-row map into the parent
+  std::vector<int> ch_ptr, ch;
+  std::vector<int> rel_ptr, rel;  // indexed by child: f_c - k_c entries
+  // tiers
+  std::vector<int8_t> wide;  // 1: front > warp limit, or any descendant is
+                             // (upward closed)
+  // warp tier: heavy paths (bottom -> top), ordered so that every light
+  // child's path precedes the path it hangs from
+  std::vector<int> path_ptr, path_nodes;
+  // wide tier: level lists (level 0 = deepest wide fronts)
+  std::vector<int> lvl_ptr, lvl_nodes;
+  int max_f = 0, max_wide_f = 0;
+  long long flops = 0;      // sum_j c_j (c_j + 2), the SURVEY 8(d) figure
+  long long wide_front_elems = 0;
+  int sn_height = 0;
+};
+
+constexpr int kWarpFront = 32;
+
+Supernodal build_supernodal(const LowerCsc& A, const Symbolic& S);
+
+}  // namespace nclb
