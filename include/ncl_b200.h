@@ -121,6 +121,10 @@ int ncl_kkt_factors(const ncl_kkt* ctx, int* lcol_ptr, int* lrow_ind,
  * over attempts; [4] total; [5] number of accepted solves so far */
 int ncl_kkt_last_timing(const ncl_kkt* ctx, double* ms6);
 int ncl_kkt_set_timing(ncl_kkt* ctx, int enable);
+/* the context's CUDA stream (cudaStream_t) for event timing by callers */
+int ncl_kkt_get_stream(const ncl_kkt* ctx, void** stream);
+/* number of kernels this context has launched so far */
+int ncl_kkt_launch_count(const ncl_kkt* ctx, long long* count);
 
 /* ---- host-only symbolic plan (no GPU needed) ------------------------------
  * The symbolic-once half of KktContext construction (pattern, slot maps,

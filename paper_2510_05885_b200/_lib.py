@@ -66,6 +66,8 @@ SIGS = {
     "ncl_kkt_factors": ([_p, _ip, _ip, _dp, _dp, _ip], _i),
     "ncl_kkt_last_timing": ([_p, _dp], _i),
     "ncl_kkt_set_timing": ([_p, _i], _i),
+    "ncl_kkt_get_stream": ([_p, C.POINTER(_p)], _i),
+    "ncl_kkt_launch_count": ([_p, C.POINTER(_ll)], _i),
     "ncl_plan_create": ([_i, _ip, _ip, _i, _ip, _ip, _i, _i, _i, C.POINTER(_p)], _i),
     "ncl_plan_destroy": ([_p], None),
     "ncl_plan_info": ([_p, C.POINTER(KktInfo)], _i),

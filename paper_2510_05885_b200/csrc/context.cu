@@ -12,6 +12,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <array>
 #include <cmath>
 #include <cstring>
 #include <memory>
@@ -116,8 +117,12 @@ class LdlSystem {
     for (size_t l = 0; l + 1 < sn_.lvl_ptr.size(); ++l)
       launch_factor_wide(sd_, fd, kval, lvl_nodes_.p + sn_.lvl_ptr[l],
                          sn_.lvl_ptr[l + 1] - sn_.lvl_ptr[l], eps, st_);
+    launches_ += (npaths() > 0 ? 1 : 0) + nlevels();
     CK(cudaGetLastError());
   }
+
+  int nlevels() const { return static_cast<int>(sn_.lvl_ptr.size()) - 1; }
+  long long launches() const { return launches_; }
 
   FactorInfo read_factor_info() {
     CK(cudaMemcpyAsync(hs_, ds_.p, sizeof(Scalars), cudaMemcpyDeviceToHost, st_));
@@ -153,6 +158,7 @@ class LdlSystem {
                       counter_.p, npaths(), grid_, st_);
     }
     launch_permute_out(N_, perm_.p, xp_.p, x, st_);
+    launches_ += 2 + (npaths() > 0 ? 2 : 0) + 2 * nlevels();
     CK(cudaGetLastError());
   }
 
@@ -160,6 +166,7 @@ class LdlSystem {
   void residual_async(const double* kval, const double* x, const double* b, double* r,
                       double* norm) {
     launch_residual(N_, fr_ptr_.p, fr_col_.p, fr_slot_.p, kval, x, b, r, norm, st_);
+    launches_ += 1;
   }
 
   // solve_refined (sparse.cpp:278-322).  b on device; solution in x_out
@@ -174,6 +181,7 @@ class LdlSystem {
     solve_async(b, x);
     CK(cudaMemsetAsync(&ds_.p->norm[0], 0, sizeof(double) * 2, st_));
     launch_absmax2(N_, b, 0, nullptr, &ds_.p->norm[0], st_);
+    launches_ += 1;
     residual_async(kval, x, b, r, &ds_.p->norm[1]);
     CK(cudaMemcpyAsync(&hs_->norm[0], &ds_.p->norm[0], sizeof(double) * 2,
                        cudaMemcpyDeviceToHost, st_));
@@ -186,6 +194,7 @@ class LdlSystem {
     while (steps < max_ref && res > tol * denom) {
       solve_async(r, dx);
       launch_axpy_to(N_, x, dx, xn, st_);
+      launches_ += 1;
       CK(cudaMemsetAsync(&ds_.p->norm[1], 0, sizeof(double), st_));
       residual_async(kval, xn, b, rn, &ds_.p->norm[1]);
       CK(cudaMemcpyAsync(&hs_->norm[1], &ds_.p->norm[1], sizeof(double),
@@ -360,6 +369,7 @@ class LdlSystem {
   int N_ = 0;
   int grid_ = 1;
   int epoch_ = 0;
+  long long launches_ = 0;
   SnDev sd_{};
   DBuf<int> first_, f_, sparent_, rows_ptr_, rows_, u_ld_, asm_ptr_, asm_pos_, asm_slot_,
       ch_ptr_, ch_, rel_ptr_, rel_, path_ptr_, path_nodes_, lvl_nodes_, perm_, flags_,
@@ -413,13 +423,12 @@ class KktSystem {
     asm_.pair_row = pair_row_.p;
     asm_.pair_pa = pair_pa_.p;
     asm_.pair_pb = pair_pb_.p;
-    for (auto& e : ev_) CK(cudaEventCreate(&e));
     CK(cudaStreamSynchronize(st_));
   }
 
   ~KktSystem() {
     ldl_.reset();
-    for (auto& e : ev_) cudaEventDestroy(e);
+    for (auto& e : pool_) cudaEventDestroy(e);
     if (st_) cudaStreamDestroy(st_);
   }
 
@@ -466,26 +475,29 @@ class KktSystem {
     double delta = 0.0;
     bool first = true;
     const int* tgt = P_.inertia_target;
+    launches_ += 1;
     for (;;) {
       st->factor_attempts++;
-      mark(0);
+      const int e0 = tick();
       refill_async(hv, jv, sg, rho, delta);
-      mark(1);
+      launches_ += P_.form == kK1s ? 2 : 1;
+      const int e1 = tick();
       ldl_->factorize_async(kval_.p, opt_.pivot_eps);
-      mark(2);
+      const int e2 = tick();
+      span(0, e0, e1);
+      span(1, e1, e2);
       const FactorInfo F = ldl_->read_factor_info();
-      accumulate(0, 0, 1);
-      accumulate(1, 1, 2);
       if (F.ok && F.n_pos == tgt[0] && F.n_neg == tgt[1]) {
-        mark(0);
+        const int e3 = tick();
         launch_rhs(P_, jt_ptr_.p, jt_row_.p, jt_slot_.p, jv, sg, r1, r2, r3, rho, delta, v_.p,
                    wk_.p, rs_.p, pk_.p, rhs_.p, st_);
+        launches_ += P_.form == kK1s ? 2 : 1;
         double rel = 0.0;
         int conv = 0;
         const int steps = ldl_->solve_refined(kval_.p, rhs_.p, opt_.max_refine,
                                               opt_.refine_tol, sol_.p, &rel, &conv);
-        mark(1);
-        accumulate(2, 0, 1);
+        const int e4 = tick();
+        span(2, e3, e4);
         // bn = ||rhs||_inf was read inside solve_refined
         const double bn = hs->norm[0];
         const double abs_res = rel * (bn > 0.0 ? bn : 1.0);
@@ -496,18 +508,19 @@ class KktSystem {
           st->refine_steps = steps;
           st->perturbed_pivots = F.perturbed;
           st->rel_residual = rel;
-          mark(0);
+          const int e5 = tick();
           launch_recover(P_, jp_ptr_.p, jp_idx_.p, jv, sol_.p, v_.p, rs_.p, pk_.p, r2, rho,
                          delta, dx, dr, dy, st_);
           CK(cudaMemsetAsync(&ds->nonfinite, 0, sizeof(int), st_));
           launch_nonfinite(P_.n, dx, &ds->nonfinite, st_);
           launch_nonfinite(P_.m, dr, &ds->nonfinite, st_);
           launch_nonfinite(P_.m, dy, &ds->nonfinite, st_);
+          launches_ += 4;
           CK(cudaMemcpyAsync(&hs->nonfinite, &ds->nonfinite, sizeof(int),
                              cudaMemcpyDeviceToHost, st_));
-          mark(1);
+          const int e6 = tick();
+          span(3, e5, e6);
           CK(cudaStreamSynchronize(st_));
-          accumulate(3, 0, 1);
           st->ok = hs->nonfinite == 0;
           finish_timing();
           return;
@@ -553,19 +566,35 @@ class KktSystem {
 
   void set_timing(bool on) { timing_ = on; }
   void timing(double* out) const { std::copy(std::begin(ms_), std::end(ms_), out); }
+  long long launches() const { return launches_ + ldl_->launches(); }
 
  private:
-  void mark(int i) {
-    if (timing_) CK(cudaEventRecord(ev_[i], st_));
+  // sync-free phase timing: events are recorded on the context stream and
+  // only read after the solve's final synchronisation
+  int tick() {
+    if (!timing_) return -1;
+    if (nev_ == pool_.size()) {
+      cudaEvent_t e;
+      CK(cudaEventCreate(&e));
+      pool_.push_back(e);
+    }
+    CK(cudaEventRecord(pool_[nev_], st_));
+    return static_cast<int>(nev_++);
   }
-  void accumulate(int slot, int a, int b) {
-    if (!timing_) return;
-    CK(cudaEventSynchronize(ev_[b]));
-    float ms = 0.f;
-    CK(cudaEventElapsedTime(&ms, ev_[a], ev_[b]));
-    ms_[slot] += ms;
+  void span(int phase, int a, int b) {
+    if (timing_) spans_.push_back({phase, a, b});
   }
   void finish_timing() {
+    if (timing_) {
+      CK(cudaStreamSynchronize(st_));
+      for (const auto& s : spans_) {
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, pool_[s[1]], pool_[s[2]]));
+        ms_[s[0]] += ms;
+      }
+    }
+    spans_.clear();
+    nev_ = 0;
     ms_[4] = ms_[0] + ms_[1] + ms_[2] + ms_[3];
     ms_[5] += 1.0;
   }
@@ -580,9 +609,12 @@ class KktSystem {
   DBuf<uint32_t> c_code_;
   DBuf<double> hval_, jval_, sigma_, r1_, r2_, r3_, dx_, dr_, dy_, kval_, wrow_, v_, wk_, rs_,
       pk_, rhs_, sol_;
-  cudaEvent_t ev_[2] = {nullptr, nullptr};
+  std::vector<cudaEvent_t> pool_;
+  size_t nev_ = 0;
+  std::vector<std::array<int, 3>> spans_;
   bool timing_ = false;
   double ms_[6] = {0, 0, 0, 0, 0, 0};
+  long long launches_ = 0;
 };
 
 // ---------------------------------------------------------------------------
@@ -832,6 +864,18 @@ int ncl_kkt_factors(const ncl_kkt* ctx, int* lcol_ptr, int* lrow_ind, double* lv
 int ncl_kkt_last_timing(const ncl_kkt* ctx, double* ms6) {
   if (!ctx || !ms6) return NCL_EINVAL;
   ctx->sys->timing(ms6);
+  return NCL_OK;
+}
+
+int ncl_kkt_get_stream(const ncl_kkt* ctx, void** stream) {
+  if (!ctx || !stream) return NCL_EINVAL;
+  *stream = static_cast<void*>(ctx->sys->stream());
+  return NCL_OK;
+}
+
+int ncl_kkt_launch_count(const ncl_kkt* ctx, long long* count) {
+  if (!ctx || !count) return NCL_EINVAL;
+  *count = ctx->sys->launches();
   return NCL_OK;
 }
 

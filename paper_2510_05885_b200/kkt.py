@@ -256,6 +256,17 @@ class KktContext:
         return dict(ok=bool(info[0]), n_pos=int(info[1]), n_neg=int(info[2]),
                     perturbed=int(info[3]), lcol_ptr=lcp, lrow_ind=lri, lval=lv, d=d)
 
+    def stream(self) -> int:
+        """the context's cudaStream_t (for torch.cuda.ExternalStream timing)"""
+        s = C.c_void_p()
+        check(self._L.ncl_kkt_get_stream(self._h, C.byref(s)), "get_stream")
+        return s.value or 0
+
+    def launch_count(self) -> int:
+        n = C.c_longlong()
+        check(self._L.ncl_kkt_launch_count(self._h, C.byref(n)), "launch_count")
+        return n.value
+
     def set_timing(self, on: bool = True) -> None:
         check(self._L.ncl_kkt_set_timing(self._h, int(on)), "set_timing")
 
