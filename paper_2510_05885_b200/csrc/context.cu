@@ -14,6 +14,8 @@
 #include <algorithm>
 #include <array>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <stdexcept>
@@ -114,11 +116,49 @@ class LdlSystem {
       launch_factor_warp(sd_, fd, kval, flags_.p, epoch_, counter_.p, npaths(), eps,
                          grid_, st_);
     }
-    for (size_t l = 0; l + 1 < sn_.lvl_ptr.size(); ++l)
-      launch_factor_wide(sd_, fd, kval, lvl_nodes_.p + sn_.lvl_ptr[l],
-                         sn_.lvl_ptr[l + 1] - sn_.lvl_ptr[l], eps, st_);
-    launches_ += (npaths() > 0 ? 1 : 0) + nlevels();
+    launches_ += npaths() > 0 ? 1 : 0;
+    const auto& T = sn_;
+    for (int l = 0; l < nlevels(); ++l) {
+      if (lvl_cluster_[l] > 0) {  // one launch, one cluster per front
+        unsigned long long* tr = (l == trace_level_) ? trace_.p : nullptr;
+        const int used = launch_wide_front(sd_, fd, kval, lvl_nodes_.p + T.lvl_ptr[l],
+                                           T.lvl_ptr[l + 1] - T.lvl_ptr[l], lvl_cluster_[l],
+                                           eps, st_, tr);
+        if (tr) dump_trace(l);
+        if (used == 0) throw CudaError("k_wide_front: no cluster configuration fits");
+        lvl_cluster_[l] = used;
+        launches_ += 1;
+        continue;
+      }
+      const int na = T.asm_task_ptr[l + 1] - T.asm_task_ptr[l];
+      launch_wide_assemble(sd_, fd, kval, asm_task_.p + T.asm_task_ptr[l], na, st_);
+      launches_ += na > 0;
+      for (int g = T.lp_ptr[l]; g < T.lp_ptr[l + 1]; ++g) {
+        const int np = T.pn_ptr[g + 1] - T.pn_ptr[g];
+        const int nt = T.tl_ptr[g + 1] - T.tl_ptr[g];
+        launch_wide_panel(sd_, fd, pn_tasks_.p + T.pn_ptr[g], np, g - T.lp_ptr[l], eps, st_);
+        launch_wide_update(sd_, fd, tiles_.p + T.tl_ptr[g], nt, st_);
+        launches_ += (np > 0) + (nt > 0);
+      }
+    }
     CK(cudaGetLastError());
+  }
+
+  // diagnostic: NCL_WIDE_TRACE=<level> prints per-phase timestamps of the
+  // first front of that wide level (cluster rank 0, %globaltimer) to stderr
+  void dump_trace(int l) {
+    std::vector<unsigned long long> h(128);
+    CK(cudaMemcpyAsync(h.data(), trace_.p, 128 * sizeof(unsigned long long),
+                       cudaMemcpyDeviceToHost, st_));
+    CK(cudaStreamSynchronize(st_));
+    const int s = sn_.lvl_nodes[sn_.lvl_ptr[l]];
+    std::fprintf(stderr, "[ncl trace] level %d front %d f=%d k=%d cluster=%d:", l, s, sn_.f[s],
+                 sn_.first[s + 1] - sn_.first[s], lvl_cluster_[l]);
+    for (int i = 1; i < 120 && h[i] > h[0]; ++i)
+      std::fprintf(stderr, " %.1f", (h[i] - h[i - 1]) / 1e3);
+    std::fprintf(stderr, " (us per phase); first panel: diag %.2f bar %.2f rows %.2f us\n",
+                 (h[121] - h[120]) / 1e3, (h[122] - h[121]) / 1e3, (h[123] - h[122]) / 1e3);
+    CK(cudaMemsetAsync(trace_.p, 0, 128 * sizeof(unsigned long long), st_));
   }
 
   int nlevels() const { return static_cast<int>(sn_.lvl_ptr.size()) - 1; }
@@ -250,7 +290,6 @@ class LdlSystem {
     fd.lval = lval_.p;
     fd.d = d_.p;
     fd.upd = upd_.p;
-    fd.scratch = scratch_.p;
     fd.stats = ds_.p->stats;
     return fd;
   }
@@ -277,20 +316,39 @@ class LdlSystem {
     lvl_nodes_.upload(T.lvl_nodes);
     std::vector<int8_t> wide(T.wide.begin(), T.wide.end());
     wide_.upload(wide);
-    // wide-front scratch: fronts of one level side by side, levels reuse it
-    std::vector<long long> scr(static_cast<size_t>(T.nsn), 0);
-    long long scr_max = 0;
-    for (size_t l = 0; l + 1 < T.lvl_ptr.size(); ++l) {
-      long long off = 0;
-      for (int q = T.lvl_ptr[l]; q < T.lvl_ptr[l + 1]; ++q) {
-        const int s = T.lvl_nodes[q];
-        scr[s] = off;
-        off += static_cast<long long>(T.f[s]) * T.f[s];
-      }
-      scr_max = std::max(scr_max, off);
+    std::vector<int4> at(T.asm_task.size());
+    for (size_t i = 0; i < at.size(); ++i)
+      at[i] = make_int4(T.asm_task[i][0], T.asm_task[i][1], T.asm_task[i][2], T.asm_task[i][3]);
+    asm_task_.upload(at);
+    std::vector<int2> pt(T.pn_tasks.size());
+    for (size_t i = 0; i < pt.size(); ++i) pt[i] = make_int2(T.pn_tasks[i][0], T.pn_tasks[i][1]);
+    pn_tasks_.upload(pt);
+    std::vector<int4> tl(T.tiles.size());
+    for (size_t i = 0; i < tl.size(); ++i)
+      tl[i] = make_int4(T.tiles[i][0], T.tiles[i][1], T.tiles[i][2], T.tiles[i][3]);
+    tiles_.upload(tl);
+    // per level: cluster size of the fused launch, or 0 = huge-front path
+    int sms = 148;
+    {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     }
-    scr_off_.upload(scr);
-    scratch_.alloc(static_cast<size_t>(scr_max));
+    lvl_cluster_.assign(static_cast<size_t>(nlevels()), 0);
+    for (int l = 0; l < nlevels(); ++l) {
+      int fmax = 0;
+      const int nf = T.lvl_ptr[l + 1] - T.lvl_ptr[l];
+      for (int q = T.lvl_ptr[l]; q < T.lvl_ptr[l + 1]; ++q) fmax = std::max(fmax, T.f[T.lvl_nodes[q]]);
+      if (fmax > kHugeFront) continue;
+      int c = 16;
+      while (c > 1 && nf * c > 2 * sms) c >>= 1;
+      lvl_cluster_[l] = c;
+    }
+    if (const char* e = std::getenv("NCL_WIDE_TRACE")) {
+      trace_level_ = std::atoi(e);
+      trace_.alloc(128 * static_cast<size_t>(std::max(1, T.lvl_ptr.empty() ? 1 : T.nsn)));
+      trace_.zero(st_);
+    }
     perm_.upload(S_.perm);
     lval_.alloc(static_cast<size_t>(T.l_off[T.nsn]));
     lval_.zero(st_);
@@ -356,7 +414,7 @@ class LdlSystem {
     sd_.rel = rel_.p;
     sd_.path_ptr = path_ptr_.p;
     sd_.path_nodes = path_nodes_.p;
-    sd_.scr_off = scr_off_.p;
+    sd_.wide = wide_.p;
     grid_ = warp_tier_grid();
     set_wide_smem_limit(T.max_wide_f);
     CK(cudaStreamSynchronize(st_));
@@ -370,13 +428,19 @@ class LdlSystem {
   int grid_ = 1;
   int epoch_ = 0;
   long long launches_ = 0;
+  std::vector<int> lvl_cluster_;
+  int trace_level_ = -1;
+  DBuf<unsigned long long> trace_;
   SnDev sd_{};
   DBuf<int> first_, f_, sparent_, rows_ptr_, rows_, u_ld_, asm_ptr_, asm_pos_, asm_slot_,
       ch_ptr_, ch_, rel_ptr_, rel_, path_ptr_, path_nodes_, lvl_nodes_, perm_, flags_,
       counter_, fr_ptr_, fr_col_, fr_slot_;
   DBuf<int8_t> wide_;
-  DBuf<long long> l_off_, u_off_, scr_off_;
-  DBuf<double> lval_, d_, upd_, uvec_, scratch_, wp_, xp_, rx_, rr_, rdx_, rxn_, rrn_;
+  DBuf<int4> asm_task_;
+  DBuf<int2> pn_tasks_;
+  DBuf<int4> tiles_;
+  DBuf<long long> l_off_, u_off_;
+  DBuf<double> lval_, d_, upd_, uvec_, wp_, xp_, rx_, rr_, rdx_, rxn_, rrn_;
   DBuf<Scalars> ds_;
   Scalars* hs_ = nullptr;
 };

@@ -26,15 +26,18 @@ struct SnDev {
   const int* rel;
   const int* path_ptr;
   const int* path_nodes;
-  const long long* scr_off;  // wide fronts: offset into the front scratch
+  const int8_t* wide;        // 1: wide-tier front (stored f x f in lval)
 };
+
+__device__ __forceinline__ int f_minus_k(const SnDev& sd, int s) {
+  return sd.f[s] - (sd.first[s + 1] - sd.first[s]);
+}
 
 // numeric factor storage
 struct FactorDev {
-  double* lval;   // l_off[nsn]
+  double* lval;   // l_off[nsn]: warp-tier L blocks and whole wide fronts
   double* d;      // N (permuted order)
-  double* upd;    // u_total
-  double* scratch;  // wide fronts (f x f, column-major)
+  double* upd;    // u_total: warp-tier update blocks
   int* stats;     // [0] n_pos [1] n_neg [2] perturbed [3] fail
 };
 

@@ -22,8 +22,17 @@ struct AsmDev {
 void launch_factor_warp(const SnDev& sd, const FactorDev& fd, const double* kval,
                         int* flags, int epoch, int* counter, int npaths,
                         double eps, int grid, cudaStream_t st);
-void launch_factor_wide(const SnDev& sd, const FactorDev& fd, const double* kval,
-                        const int* nodes, int count, double eps, cudaStream_t st);
+// wide_kernels.cu
+// returns the cluster size used (0: launch impossible)
+int launch_wide_front(const SnDev& sd, const FactorDev& fd, const double* kval, const int* nodes,
+                      int count, int cluster, double eps, cudaStream_t st,
+                      unsigned long long* trace = nullptr);
+void launch_wide_assemble(const SnDev& sd, const FactorDev& fd, const double* kval,
+                          const int4* tasks, int count, cudaStream_t st);
+void launch_wide_panel(const SnDev& sd, const FactorDev& fd, const int2* tasks, int count,
+                       int panel, double eps, cudaStream_t st);
+void launch_wide_update(const SnDev& sd, const FactorDev& fd, const int4* tiles, int count,
+                        cudaStream_t st);
 void launch_fwd_warp(const SnDev& sd, const double* lval, double* w, double* uvec,
                      int* flags, int epoch, int* counter, int npaths, int grid,
                      cudaStream_t st);

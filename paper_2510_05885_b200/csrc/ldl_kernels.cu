@@ -27,6 +27,7 @@ namespace nclb {
 constexpr int kWF = 32;       // warp-tier front limit (rows)
 constexpr int kFLD = 33;      // padded leading dimension of a warp front
 constexpr int kWarpsPerCta = 4;
+constexpr int kWideThreads = 256;
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
@@ -138,133 +139,6 @@ k_factor_warp(SnDev sd, FactorDev fd, const double* __restrict__ kval,
 }
 
 // ---------------------------------------------------------------------------
-// wide-tier numeric factorization: one CTA per front of one tree level
-constexpr int kWideThreads = 256;
-constexpr int kPanel = 32;
-constexpr int kTile = 64;
-
-__global__ void __launch_bounds__(kWideThreads)
-k_factor_wide(SnDev sd, FactorDev fd, const double* __restrict__ kval,
-              const int* __restrict__ nodes, double eps) {
-  __shared__ double As[kPanel][kTile + 1];
-  __shared__ double Bs[kPanel][kTile + 1];
-  __shared__ double colp[kPanel];
-  const int s = nodes[blockIdx.x];
-  const int c0 = sd.first[s], k = sd.first[s + 1] - c0, f = sd.f[s];
-  const int tid = threadIdx.x, nth = blockDim.x;
-  double* F = fd.scratch + sd.scr_off[s];
-  const size_t ff = static_cast<size_t>(f) * f;
-  for (size_t i = tid; i < ff; i += nth) F[i] = 0.0;
-  __syncthreads();
-  for (int a = sd.asm_ptr[s] + tid; a < sd.asm_ptr[s + 1]; a += nth) {
-    const int pos = sd.asm_pos[a];
-    F[(pos & 0xffff) + static_cast<size_t>(pos >> 16) * f] += kval[sd.asm_slot[a]];
-  }
-  __syncthreads();
-  for (int cc = sd.ch_ptr[s]; cc < sd.ch_ptr[s + 1]; ++cc) {
-    const int c = sd.ch[cc];
-    const int fu = sd.u_ld[c];
-    const int* rel = sd.rel + sd.rel_ptr[c];
-    const double* U = fd.upd + sd.u_off[c];
-    const size_t tot = static_cast<size_t>(fu) * fu;
-    for (size_t idx = tid; idx < tot; idx += nth) {
-      const int i = static_cast<int>(idx % fu), j = static_cast<int>(idx / fu);
-      if (i >= j) F[rel[i] + static_cast<size_t>(rel[j]) * f] += __ldcg(U + idx);
-    }
-    __syncthreads();
-  }
-  double* Lb = fd.lval + sd.l_off[s];
-  int npos = 0, nneg = 0, pert = 0, fail = 0;
-  for (int p0 = 0; p0 < k; p0 += kPanel) {
-    const int p1 = min(p0 + kPanel, k);
-    for (int p = p0; p < p1; ++p) {
-      __syncthreads();
-      double dp = F[p + static_cast<size_t>(p) * f];
-      int pflag = 0;
-      if (fabs(dp) < eps) {
-        dp = (dp >= 0.0) ? eps : -eps;
-        pflag = 1;
-      }
-      if (tid < p1 - p - 1) colp[tid] = F[(p + 1 + tid) + static_cast<size_t>(p) * f];
-      __syncthreads();
-      for (int r = p + 1 + tid; r < f; r += nth) {
-        const double l = F[r + static_cast<size_t>(p) * f] / dp;
-        Lb[r + static_cast<size_t>(p) * f] = l;
-        if (!isfinite(l)) fail = 1;
-        const int jmax = min(p1 - 1, r);
-        for (int j = p + 1; j <= jmax; ++j)
-          F[r + static_cast<size_t>(j) * f] -= l * colp[j - p - 1];
-      }
-      if (tid == 0) {
-        fd.d[c0 + p] = dp;
-        pert += pflag;
-        if (!isfinite(dp) || dp == 0.0) fail = 1;
-        if (dp > 0.0)
-          npos++;
-        else
-          nneg++;
-      }
-    }
-    __syncthreads();
-    // trailing update F[r][c] -= sum_q L[r][q] * F[c][q], p1 <= c <= r < f
-    const int nb = p1 - p0;
-    const int mt = f - p1;
-    if (mt <= 0) continue;
-    const int T = (mt + kTile - 1) / kTile;
-    const int tr = tid / 16, tc = tid % 16;
-    for (int ti = 0; ti < T; ++ti)
-      for (int tj = 0; tj <= ti; ++tj) {
-        const int r0 = p1 + ti * kTile, q0 = p1 + tj * kTile;
-        for (int idx = tid; idx < kTile * nb; idx += nth) {
-          const int rr = idx % kTile, qq = idx / kTile;
-          const int ra = r0 + rr, rb = q0 + rr;
-          As[qq][rr] = ra < f ? Lb[ra + static_cast<size_t>(p0 + qq) * f] : 0.0;
-          Bs[qq][rr] = rb < f ? F[rb + static_cast<size_t>(p0 + qq) * f] : 0.0;
-        }
-        __syncthreads();
-        double acc[4][4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-#pragma unroll
-          for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
-        for (int qq = 0; qq < nb; ++qq) {
-          double a[4], b[4];
-#pragma unroll
-          for (int i = 0; i < 4; ++i) a[i] = As[qq][tr + 16 * i];
-#pragma unroll
-          for (int j = 0; j < 4; ++j) b[j] = Bs[qq][tc + 16 * j];
-#pragma unroll
-          for (int i = 0; i < 4; ++i)
-#pragma unroll
-            for (int j = 0; j < 4; ++j) acc[i][j] += a[i] * b[j];
-        }
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const int r = r0 + tr + 16 * i, c = q0 + tc + 16 * j;
-            if (r < f && c < f && r >= c) F[r + static_cast<size_t>(c) * f] -= acc[i][j];
-          }
-        __syncthreads();
-      }
-  }
-  __syncthreads();
-  const int fu = f - k;
-  double* Us = fd.upd + sd.u_off[s];
-  const size_t tot = static_cast<size_t>(fu) * fu;
-  for (size_t idx = tid; idx < tot; idx += nth) {
-    const int i = static_cast<int>(idx % fu), j = static_cast<int>(idx / fu);
-    if (i >= j) Us[idx] = F[(k + i) + static_cast<size_t>(k + j) * f];
-  }
-  if (tid == 0) {
-    if (npos) atomicAdd(fd.stats + 0, npos);
-    if (nneg) atomicAdd(fd.stats + 1, nneg);
-    if (pert) atomicAdd(fd.stats + 2, pert);
-  }
-  if (fail) atomicOr(fd.stats + 3, 1);
-}
-
-// ---------------------------------------------------------------------------
 // forward solve L w = b (in place on the permuted vector w); update vectors of
 // the multifrontal solve live at uvec + rel_ptr[s] (f - k entries)
 __global__ void __launch_bounds__(kWarpsPerCta * 32)
@@ -288,7 +162,7 @@ k_fwd_warp(SnDev sd, const double* __restrict__ lval, double* w, double* uvec,
       __syncwarp();
       for (int cc = chb; cc < che; ++cc) {
         const int c = sd.ch[cc];
-        const int fu = sd.u_ld[c];
+        const int fu = f_minus_k(sd, c);
         if (lane < fu) T[sd.rel[sd.rel_ptr[c] + lane]] += __ldcg(uvec + sd.rel_ptr[c] + lane);
         __syncwarp();
       }
@@ -358,15 +232,38 @@ k_fwd_wide(SnDev sd, const double* __restrict__ lval, double* w, double* uvec,
   __syncthreads();
   for (int cc = sd.ch_ptr[s]; cc < sd.ch_ptr[s + 1]; ++cc) {
     const int c = sd.ch[cc];
-    const int fu = sd.u_ld[c];
+    const int fu = f_minus_k(sd, c);
     for (int i = tid; i < fu; i += nth)
       T[sd.rel[sd.rel_ptr[c] + i]] += uvec[sd.rel_ptr[c] + i];
     __syncthreads();
   }
   const double* Lb = lval + sd.l_off[s];
-  for (int p = 0; p < k; ++p) {
-    const double wp = T[p];
-    for (int r = p + 1 + tid; r < f; r += nth) T[r] -= Lb[r + static_cast<size_t>(p) * f] * wp;
+  const int lane = tid & 31, warp = tid >> 5;
+  // blocked: warp 0 solves the 32x32 unit-triangular diagonal block with
+  // shuffles, then every thread updates its rows below with the 32 values
+  __shared__ double Ld[32][33];
+  for (int p0 = 0; p0 < k; p0 += 32) {
+    const int p1 = min(p0 + 32, k), nb = p1 - p0;
+    for (int idx = tid; idx < nb * nb; idx += nth) {
+      const int i = idx % nb, j = idx / nb;
+      Ld[i][j] = i > j ? Lb[(p0 + i) + static_cast<size_t>(p0 + j) * f] : 0.0;
+    }
+    __syncthreads();
+    if (warp == 0) {
+      double t = lane < nb ? T[p0 + lane] : 0.0;
+      for (int p = 0; p < nb; ++p) {
+        const double wp = __shfl_sync(0xffffffffu, t, p);
+        if (lane > p && lane < nb) t -= Ld[lane][p] * wp;
+      }
+      if (lane < nb) T[p0 + lane] = t;
+    }
+    __syncthreads();
+    for (int r = p1 + tid; r < f; r += nth) {
+      double acc = T[r];
+#pragma unroll 8
+      for (int q = 0; q < nb; ++q) acc -= Lb[r + static_cast<size_t>(p0 + q) * f] * T[p0 + q];
+      T[r] = acc;
+    }
     __syncthreads();
   }
   for (int r = tid; r < f; r += nth) {
@@ -382,6 +279,7 @@ __global__ void __launch_bounds__(kWideThreads)
 k_bwd_wide(SnDev sd, const double* __restrict__ lval, const double* __restrict__ d,
            const double* __restrict__ w, double* x, const int* __restrict__ nodes) {
   extern __shared__ double X[];
+  __shared__ double Ld[32][33];
   const int s = nodes[blockIdx.x];
   const int c0 = sd.first[s], k = sd.first[s + 1] - c0, f = sd.f[s];
   const int tid = threadIdx.x, nth = blockDim.x;
@@ -398,16 +296,33 @@ k_bwd_wide(SnDev sd, const double* __restrict__ lval, const double* __restrict__
     if (lane == 0) X[p] -= part;
   }
   __syncthreads();
-  if (warp == 0) {
-    for (int p = k - 1; p >= 0; --p) {
+  // blocked from the last pivot block up: GEMV with the solved pivots below
+  // the block (warp per pivot), then warp 0 finishes the diagonal block
+  for (int p1 = k; p1 > 0;) {
+    const int p0 = max(0, p1 - 32), nb = p1 - p0;
+    for (int p = p0 + warp; p < p1; p += nwarps) {
       double part = 0.0;
-      for (int r = p + 1 + lane; r < k; r += 32) part += Lb[r + static_cast<size_t>(p) * f] * X[r];
+      for (int r = p1 + lane; r < k; r += 32) part += Lb[r + static_cast<size_t>(p) * f] * X[r];
       part = warp_sum(part);
       if (lane == 0) X[p] -= part;
-      __syncwarp();
     }
+    for (int idx = tid; idx < nb * nb; idx += nth) {
+      const int i = idx % nb, j = idx / nb;
+      Ld[i][j] = i > j ? Lb[(p0 + i) + static_cast<size_t>(p0 + j) * f] : 0.0;
+    }
+    __syncthreads();
+    if (warp == 0) {
+      double xv = lane < nb ? X[p0 + lane] : 0.0;
+      for (int p = nb - 1; p >= 0; --p) {
+        const double part = (lane > p && lane < nb) ? Ld[lane][p] * xv : 0.0;
+        const double sum = warp_sum(part);
+        if (lane == p) xv -= sum;
+      }
+      if (lane < nb) X[p0 + lane] = xv;
+    }
+    __syncthreads();
+    p1 = p0;
   }
-  __syncthreads();
   for (int r = tid; r < k; r += nth) x[c0 + r] = X[r];
 }
 
@@ -431,12 +346,6 @@ void launch_factor_warp(const SnDev& sd, const FactorDev& fd, const double* kval
   if (npaths == 0) return;
   k_factor_warp<<<grid, kWarpsPerCta * 32, 0, st>>>(sd, fd, kval, flags, epoch,
                                                    counter, npaths, eps);
-}
-
-void launch_factor_wide(const SnDev& sd, const FactorDev& fd, const double* kval,
-                        const int* nodes, int count, double eps, cudaStream_t st) {
-  if (count == 0) return;
-  k_factor_wide<<<count, kWideThreads, 0, st>>>(sd, fd, kval, nodes, eps);
 }
 
 void launch_fwd_warp(const SnDev& sd, const double* lval, double* w, double* uvec,

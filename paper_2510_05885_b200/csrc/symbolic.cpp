@@ -608,21 +608,28 @@ Supernodal build_supernodal(const LowerCsc& A, const Symbolic& S) {
     if (T.f[s] > kWarpFront) T.wide[s] = 1;
     if (T.wide[s] && T.sparent[s] >= 0) T.wide[T.sparent[s]] = 1;
   }
-  // storage: L blocks (f x k col-major), update blocks
+  // storage.  Warp tier: an f x k column-major L block in lval and a compact
+  // (f-k)^2 update block in upd.  Wide tier: the whole f x f column-major
+  // front lives in lval (its first k columns ARE the L block, ld = f) and the
+  // update block is the trailing (f-k)^2 corner of it (u_ld = f).
   T.l_off.assign(static_cast<size_t>(nsn) + 1, 0);
   T.u_off.assign(static_cast<size_t>(nsn), 0);
   T.u_ld.assign(static_cast<size_t>(nsn), 0);
   long long uoff = 0;
   for (int s = 0; s < nsn; ++s) {
     const int k = T.first[s + 1] - T.first[s];
-    T.l_off[s + 1] = T.l_off[s] + static_cast<long long>(T.f[s]) * k;
     const int fu = T.f[s] - k;
-    T.u_off[s] = uoff;
-    T.u_ld[s] = fu;
-    uoff += static_cast<long long>(fu) * fu;
     if (T.wide[s]) {
+      T.l_off[s + 1] = T.l_off[s] + static_cast<long long>(T.f[s]) * T.f[s];
+      T.u_off[s] = T.l_off[s] + static_cast<long long>(k) * T.f[s] + k;
+      T.u_ld[s] = T.f[s];
       T.max_wide_f = std::max(T.max_wide_f, T.f[s]);
       T.wide_front_elems += static_cast<long long>(T.f[s]) * T.f[s];
+    } else {
+      T.l_off[s + 1] = T.l_off[s] + static_cast<long long>(T.f[s]) * k;
+      T.u_off[s] = uoff;
+      T.u_ld[s] = fu;
+      uoff += static_cast<long long>(fu) * fu;
     }
   }
   T.u_total = uoff;
@@ -686,6 +693,44 @@ Supernodal build_supernodal(const LowerCsc& A, const Symbolic& S) {
     std::vector<int> nx(T.lvl_ptr.begin(), T.lvl_ptr.end() - 1);
     for (int s = 0; s < nsn; ++s)
       if (T.wide[s]) T.lvl_nodes[nx[wl[s]]++] = s;
+  }
+  // wide-tier launch schedule: per level, assembly tasks (front, 64-column
+  // block); per (level, panel) the fronts that factor that panel and the
+  // 64x64 tiles of their trailing lower triangle
+  T.asm_task_ptr.assign(1, 0);
+  T.lp_ptr.assign(static_cast<size_t>(nlev) + 1, 0);
+  T.pn_ptr.assign(1, 0);
+  T.tl_ptr.assign(1, 0);
+  for (int l = 0; l < nlev; ++l) {
+    int maxp = 0;
+    for (int q = T.lvl_ptr[l]; q < T.lvl_ptr[l + 1]; ++q) {
+      const int s = T.lvl_nodes[q];
+      const int f = T.f[s], k = T.first[s + 1] - T.first[s];
+      for (int cb = 0; cb * kWideTile < f; ++cb)
+        for (int rb = cb; rb * kWideTile < f; ++rb)
+          T.asm_task.push_back({s, rb * kWideTile, cb * kWideTile, 0});
+      maxp = std::max(maxp, (k + kWidePanel - 1) / kWidePanel);
+    }
+    T.asm_task_ptr.push_back(static_cast<int>(T.asm_task.size()));
+    for (int p = 0; p < maxp; ++p) {
+      for (int q = T.lvl_ptr[l]; q < T.lvl_ptr[l + 1]; ++q) {
+        const int s = T.lvl_nodes[q];
+        const int f = T.f[s], k = T.first[s + 1] - T.first[s];
+        if (k <= p * kWidePanel) continue;
+        const int p1 = std::min((p + 1) * kWidePanel, k);
+        const int mt = f - p1;
+        const int nrb = std::max(1, (mt + kPanelRows - 1) / kPanelRows);
+        for (int rb = 0; rb < nrb; ++rb) T.pn_tasks.push_back({s, rb});
+        const int nt = (mt + kUpdTile - 1) / kUpdTile;
+        for (int ti = 0; ti < nt; ++ti)
+          for (int tj = 0; tj <= ti; ++tj)
+            T.tiles.push_back({s, p1 + ti * kUpdTile, p1 + tj * kUpdTile, p});
+        T.wide_update_flops += 2LL * (p1 - p * kWidePanel) * mt * (mt + 1) / 2;
+      }
+      T.pn_ptr.push_back(static_cast<int>(T.pn_tasks.size()));
+      T.tl_ptr.push_back(static_cast<int>(T.tiles.size()));
+    }
+    T.lp_ptr[l + 1] = T.lp_ptr[l] + maxp;
   }
   return T;
 }

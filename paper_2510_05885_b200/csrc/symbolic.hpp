@@ -13,6 +13,7 @@
 // the level schedule of the wide-front tier.
 #pragma once
 
+#include <array>
 #include <cstdint>
 #include <vector>
 
@@ -72,6 +73,15 @@ struct Supernodal {
   std::vector<int> path_ptr, path_nodes;
   // wide tier: level lists (level 0 = deepest wide fronts)
   std::vector<int> lvl_ptr, lvl_nodes;
+  // wide-tier schedule: assembly tasks {front, column block} per level;
+  // panels of level l are lp_ptr[l]..lp_ptr[l+1]-1 (global panel index g),
+  // panel tasks {front, row block} of panel g are pn_tasks[pn_ptr[g]..],
+  // trailing-update tiles {front, row0, col0, panel} are tiles[tl_ptr[g]..]
+  std::vector<std::array<int, 4>> asm_task;  // {front, row0, col0, 0}
+  std::vector<std::array<int, 2>> pn_tasks;
+  std::vector<int> asm_task_ptr, lp_ptr, pn_ptr, tl_ptr;
+  std::vector<std::array<int, 4>> tiles;
+  long long wide_update_flops = 0;
   int max_f = 0, max_wide_f = 0;
   long long flops = 0;      // sum_j c_j (c_j + 2), the SURVEY 8(d) figure
   long long wide_front_elems = 0;
@@ -79,6 +89,12 @@ struct Supernodal {
 };
 
 constexpr int kWarpFront = 32;
+constexpr int kWidePanel = 32;  // pivots per panel of a wide front
+constexpr int kWideTile = 64;   // assembly tile edge
+constexpr int kUpdTile = 32;    // trailing-update tile edge (one warp)
+constexpr int kPanelRows = 128; // rows below a panel staged per CTA pass
+constexpr int kHugeFront = 1536;  // levels with a larger front use the
+                                  // three-kernel (whole-GPU) path
 
 Supernodal build_supernodal(const LowerCsc& A, const Symbolic& S);
 
