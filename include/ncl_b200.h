@@ -139,6 +139,11 @@ int ncl_plan_info(const ncl_plan* plan, ncl_kkt_info* info);
 int ncl_plan_symbolic(const ncl_plan* plan, int* perm, int* parent,
                       int* lcol_ptr);
 int ncl_plan_pattern(const ncl_plan* plan, int* col_ptr, int* row_ind);
+/* Eigen AMDOrdering<int> restated (the ordering the reference calls at
+ * sparse.cpp:81-100) on a full symmetric CSC pattern with sorted rows:
+ * perm[k] = node eliminated k-th.  Lets a reference build without Eigen use
+ * the same ordering as this library. */
+int ncl_amd_full_pattern(int n, const int* Ap, const int* Ai, int* perm);
 /* analyze / analyze_with_permutation of a triplet pattern (perm_in may be
  * NULL = AMD); outputs perm, parent (n), lcol_ptr (n+1) */
 int ncl_analyze_host(int n, int ntrip, const int* rows, const int* cols,
@@ -166,6 +171,49 @@ int ncl_sparse_solve_refined(ncl_sparse* sp, const double* b, int max_ref,
                              double* rel_residual, int* converged);
 /* y += A x (sparse.cpp:70-79), host vectors */
 int ncl_sparse_matvec(ncl_sparse* sp, const double* x, double* y);
+
+/* ---- fused NCL vector kernels ------------------
+ * Device pointers throughout; per-element arithmetic bitwise the reference's.
+ * An ncl_nlp holds the Jacobian pattern (+ its transpose) and the NLP-form
+ * bounds (x = (t, s), n = nt + ns; +-inf for absent bounds). */
+typedef struct ncl_nlp ncl_nlp;
+int ncl_nlp_create(int nt, int ns, int m_eq, int m, const int* jp_ptr,
+                   const int* jp_idx, const double* lb, const double* ub,
+                   ncl_nlp** out);
+void ncl_nlp_destroy(ncl_nlp* h);
+int ncl_nlp_sync(ncl_nlp* h);
+/* InnerSolver::solve_prepared's KktInput (ipm.cpp:184-208) */
+int ncl_nlp_kkt_input(ncl_nlp* h, const double* jval, const double* grad,
+                      const double* c, const double* x, const double* zl,
+                      const double* zu, const double* r, const double* y,
+                      const double* yk, double mu, double rho, double* sigma,
+                      double* rbar1, double* rbar2, double* rbar3);
+/* barrier_kkt_residual (kkt.cpp:341-366); block vectors may be NULL;
+ * norm5 (host) = stat, mult, primal, compl_l, compl_u inf-norms */
+int ncl_nlp_residual(ncl_nlp* h, const double* jval, const double* grad,
+                     const double* c, const double* r, const double* y,
+                     const double* yk, double rho, const double* x,
+                     const double* zl, const double* zu, double mu,
+                     double* stat, double* mult, double* primal,
+                     double* compl_l, double* compl_u, double* norm5);
+/* recover_bound_duals (kkt.cpp:316-328) and the fraction-to-boundary
+ * minima (ipm.cpp:124-141): alpha3 (host) = primal, dual zl, dual zu */
+int ncl_nlp_step(ncl_nlp* h, const double* x, const double* zl,
+                 const double* zu, double mu, const double* dx, double tau,
+                 double* dzl, double* dzu, double* alpha3);
+/* out = v + a d (trial point / commit, ipm.cpp:267-271) */
+int ncl_nlp_axpy(ncl_nlp* h, int n, const double* v, double a, const double* d,
+                 double* out);
+/* clip_duals (ipm.cpp:232-249), in place */
+int ncl_nlp_clip_duals(ncl_nlp* h, const double* x, double mu, double* zl,
+                       double* zu);
+/* ||r||_inf (host out) and, if update, y_k += rho_used r (solver.cpp:213-217) */
+int ncl_nlp_outer(ncl_nlp* h, const double* r, double* yk, double rho_used,
+                  int update, double* rnorm);
+/* outer schedule (solver.cpp:21-41) on {mu, eta, omega, rho, rho_max} */
+void ncl_initial_outer_state(double mu0, double rho0, double rho_max,
+                             double* state5);
+int ncl_outer_update(double* state5, double rnorm);
 
 #ifdef __cplusplus
 }

@@ -73,6 +73,7 @@ SIGS = {
     "ncl_plan_info": ([_p, C.POINTER(KktInfo)], _i),
     "ncl_plan_symbolic": ([_p, _ip, _ip, _ip], _i),
     "ncl_plan_pattern": ([_p, _ip, _ip], _i),
+    "ncl_amd_full_pattern": ([_i, _ip, _ip, _ip], _i),
     "ncl_analyze_host": ([_i, _i, _ip, _ip, _ip, _ip, _ip, _ip], _i),
     "ncl_sparse_create": ([_i, _i, _ip, _ip, _dp, _ip, C.POINTER(_p)], _i),
     "ncl_sparse_destroy": ([_p], None),
@@ -83,6 +84,17 @@ SIGS = {
     "ncl_sparse_ldl_solve": ([_p, _dp, _dp], _i),
     "ncl_sparse_solve_refined": ([_p, _dp, _i, _d, _dp, _ip, _dp, _ip], _i),
     "ncl_sparse_matvec": ([_p, _dp, _dp], _i),
+    "ncl_nlp_create": ([_i, _i, _i, _i, _ip, _ip, _dp, _dp, C.POINTER(_p)], _i),
+    "ncl_nlp_destroy": ([_p], None),
+    "ncl_nlp_sync": ([_p], _i),
+    "ncl_nlp_kkt_input": ([_p] + [_p] * 9 + [_d, _d] + [_p] * 4, _i),
+    "ncl_nlp_residual": ([_p] + [_p] * 6 + [_d] + [_p] * 3 + [_d] + [_p] * 5 + [_dp], _i),
+    "ncl_nlp_step": ([_p, _p, _p, _p, _d, _p, _d, _p, _p, _dp], _i),
+    "ncl_nlp_axpy": ([_p, _i, _p, _d, _p, _p], _i),
+    "ncl_nlp_clip_duals": ([_p, _p, _d, _p, _p], _i),
+    "ncl_nlp_outer": ([_p, _p, _p, _d, _i, _dp], _i),
+    "ncl_initial_outer_state": ([_d, _d, _d, _dp], None),
+    "ncl_outer_update": ([_dp, _d], _i),
 }
 
 

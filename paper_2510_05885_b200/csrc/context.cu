@@ -23,50 +23,18 @@
 #include <vector>
 
 #include "../../include/ncl_b200.h"
+#include "cuda_util.hpp"
 #include "kkt_plan.hpp"
 #include "launch.hpp"
 
 namespace nclb {
 
+std::string& last_error() {
+  static thread_local std::string e;
+  return e;
+}
+
 namespace {
-
-thread_local std::string g_err;
-
-struct CudaError : std::runtime_error {
-  using std::runtime_error::runtime_error;
-};
-
-#define CK(x)                                                                   \
-  do {                                                                          \
-    cudaError_t e_ = (x);                                                       \
-    if (e_ != cudaSuccess)                                                      \
-      throw ::nclb::CudaError(std::string(#x) + ": " + cudaGetErrorString(e_)); \
-  } while (0)
-
-template <class T>
-struct DBuf {
-  T* p = nullptr;
-  size_t n = 0;
-  DBuf() = default;
-  DBuf(const DBuf&) = delete;
-  DBuf& operator=(const DBuf&) = delete;
-  ~DBuf() {
-    if (p) cudaFree(p);
-  }
-  void alloc(size_t k) {
-    if (p) cudaFree(p);
-    p = nullptr;
-    n = k;
-    if (k) CK(cudaMalloc(&p, k * sizeof(T)));
-  }
-  void upload(const std::vector<T>& v) {
-    alloc(v.size());
-    if (!v.empty()) CK(cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
-  }
-  void zero(cudaStream_t st) {
-    if (n) CK(cudaMemsetAsync(p, 0, n * sizeof(T), st));
-  }
-};
 
 struct Scalars {
   int stats[4];   // n_pos, n_neg, perturbed, fail
@@ -771,28 +739,7 @@ struct ncl_plan {
 
 namespace {
 
-template <class F>
-int guard(F&& f) {
-  try {
-    f();
-    return NCL_OK;
-  } catch (const std::invalid_argument& e) {
-    nclb::g_err = e.what();
-    return NCL_EINVAL;
-  } catch (const std::logic_error& e) {
-    nclb::g_err = e.what();
-    return NCL_ELOGIC;
-  } catch (const nclb::CudaError& e) {
-    nclb::g_err = e.what();
-    return NCL_ECUDA;
-  } catch (const std::bad_alloc& e) {
-    nclb::g_err = "out of memory";
-    return NCL_ENOMEM;
-  } catch (const std::exception& e) {
-    nclb::g_err = e.what();
-    return NCL_ECUDA;
-  }
-}
+using nclb::guard;
 
 ncl_kkt_opts default_opts() {
   ncl_kkt_opts o;
@@ -808,7 +755,7 @@ ncl_kkt_opts default_opts() {
 
 extern "C" {
 
-const char* ncl_last_error(void) { return nclb::g_err.c_str(); }
+const char* ncl_last_error(void) { return nclb::last_error().c_str(); }
 
 int ncl_device_count(void) {
   int n = 0;
@@ -820,7 +767,7 @@ int ncl_kkt_create(int nt, const int* hp_ptr, const int* hp_idx, int m, const in
                    const int* jp_idx, int ns, int m_eq, int form, const ncl_kkt_opts* opt,
                    ncl_kkt** out) {
   if (!out || !hp_ptr || !jp_ptr) {
-    nclb::g_err = "ncl_kkt_create: null argument";
+    nclb::last_error() = "ncl_kkt_create: null argument";
     return NCL_EINVAL;
   }
   *out = nullptr;
@@ -1001,6 +948,15 @@ int ncl_plan_pattern(const ncl_plan* plan, int* col_ptr, int* row_ind) {
   if (col_ptr) std::copy(K.col_ptr.begin(), K.col_ptr.end(), col_ptr);
   if (row_ind) std::copy(K.row_ind.begin(), K.row_ind.end(), row_ind);
   return NCL_OK;
+}
+
+int ncl_amd_full_pattern(int n, const int* Ap, const int* Ai, int* perm) {
+  if (n < 0 || !Ap || !perm) return NCL_EINVAL;
+  return guard([&] {
+    const std::vector<int> p = nclb::amd_full_pattern(
+        n, std::vector<int>(Ap, Ap + n + 1), std::vector<int>(Ai, Ai + Ap[n]));
+    std::copy(p.begin(), p.end(), perm);
+  });
 }
 
 int ncl_analyze_host(int n, int ntrip, const int* rows, const int* cols, const int* perm_in,

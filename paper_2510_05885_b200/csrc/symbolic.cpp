@@ -372,6 +372,11 @@ std::vector<int> min_degree(int n, const std::vector<int>& Ap,
 
 }  // namespace
 
+std::vector<int> amd_full_pattern(int n, const std::vector<int>& Ap,
+                                  const std::vector<int>& Ai) {
+  return min_degree(n, Ap, Ai);
+}
+
 std::vector<int> amd_order(const LowerCsc& A) {
   const int n = A.n;
   // full symmetric pattern, rows sorted (mirrored rows < j, then lower part)

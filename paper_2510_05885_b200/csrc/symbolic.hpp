@@ -33,6 +33,10 @@ LowerCsc sym_lower_from_pattern(int n, const std::vector<int>& rows,
                                 std::vector<int>* slot_of_triplet = nullptr);
 
 std::vector<int> amd_order(const LowerCsc& A);
+// minimum-degree core on a full symmetric pattern (CSC, rows sorted, the
+// structural diagonal present where it exists) -- Eigen's entry point
+std::vector<int> amd_full_pattern(int n, const std::vector<int>& Ap,
+                                  const std::vector<int>& Ai);
 
 struct Symbolic {
   int n = 0;
