@@ -91,7 +91,7 @@ class LdlSystem {
         unsigned long long* tr = (l == trace_level_) ? trace_.p : nullptr;
         const int used = launch_wide_front(sd_, fd, kval, lvl_nodes_.p + T.lvl_ptr[l],
                                            T.lvl_ptr[l + 1] - T.lvl_ptr[l], lvl_cluster_[l],
-                                           eps, st_, tr);
+                                           lvl_fmax_[l], eps, st_, tr);
         if (tr) dump_trace(l);
         if (used == 0) throw CudaError("k_wide_front: no cluster configuration fits");
         lvl_cluster_[l] = used;
@@ -102,11 +102,13 @@ class LdlSystem {
       launch_wide_assemble(sd_, fd, kval, asm_task_.p + T.asm_task_ptr[l], na, st_);
       launches_ += na > 0;
       for (int g = T.lp_ptr[l]; g < T.lp_ptr[l + 1]; ++g) {
+        const int nd = T.dg_ptr[g + 1] - T.dg_ptr[g];
         const int np = T.pn_ptr[g + 1] - T.pn_ptr[g];
         const int nt = T.tl_ptr[g + 1] - T.tl_ptr[g];
-        launch_wide_panel(sd_, fd, pn_tasks_.p + T.pn_ptr[g], np, g - T.lp_ptr[l], eps, st_);
+        launch_wide_diag(sd_, fd, dg_nodes_.p + T.dg_ptr[g], nd, g - T.lp_ptr[l], eps, st_);
+        launch_wide_panel(sd_, fd, pn_tasks_.p + T.pn_ptr[g], np, g - T.lp_ptr[l], st_);
         launch_wide_update(sd_, fd, tiles_.p + T.tl_ptr[g], nt, st_);
-        launches_ += (np > 0) + (nt > 0);
+        launches_ += (nd > 0) + (np > 0) + (nt > 0);
       }
     }
     CK(cudaGetLastError());
@@ -124,8 +126,10 @@ class LdlSystem {
                  sn_.first[s + 1] - sn_.first[s], lvl_cluster_[l]);
     for (int i = 1; i < 120 && h[i] > h[0]; ++i)
       std::fprintf(stderr, " %.1f", (h[i] - h[i - 1]) / 1e3);
-    std::fprintf(stderr, " (us per phase); first panel: diag %.2f bar %.2f rows %.2f us\n",
-                 (h[121] - h[120]) / 1e3, (h[122] - h[121]) / 1e3, (h[123] - h[122]) / 1e3);
+    std::fprintf(stderr, " (us per phase); panel detail:");
+    const char* nm[7] = {"diag", "bar", "trsm", "csync", "l11", "tiles", "csync"};
+    for (int i = 0; i < 7; ++i) std::fprintf(stderr, " %s %.2f", nm[i], (h[121 + i] - h[120 + i]) / 1e3);
+    std::fprintf(stderr, " us\n");
     CK(cudaMemsetAsync(trace_.p, 0, 128 * sizeof(unsigned long long), st_));
   }
 
@@ -152,13 +156,22 @@ class LdlSystem {
       launch_fwd_warp(sd_, lval_.p, wp_.p, uvec_.p, flags_.p, epoch_, counter_.p, npaths(),
                       grid_, st_);
     }
-    const int nl = static_cast<int>(sn_.lvl_ptr.size()) - 1;
-    for (int l = 0; l < nl; ++l)
-      launch_fwd_wide(sd_, lval_.p, wp_.p, uvec_.p, lvl_nodes_.p + sn_.lvl_ptr[l],
-                      sn_.lvl_ptr[l + 1] - sn_.lvl_ptr[l], sn_.max_wide_f, st_);
-    for (int l = nl - 1; l >= 0; --l)
-      launch_bwd_wide(sd_, lval_.p, d_.p, wp_.p, xp_.p, lvl_nodes_.p + sn_.lvl_ptr[l],
-                      sn_.lvl_ptr[l + 1] - sn_.lvl_ptr[l], sn_.max_wide_f, st_);
+    const int nl = nlevels();
+    for (int l = 0; l < nl; ++l) {
+      const int used = launch_fwd_front(sd_, lval_.p, wp_.p, uvec_.p, lvl_nodes_.p + sn_.lvl_ptr[l],
+                                        sn_.lvl_ptr[l + 1] - sn_.lvl_ptr[l], solve_cluster_[l],
+                                        lvl_fmax_[l], st_);
+      if (used == 0) throw CudaError("k_fwd_front: no cluster configuration fits");
+      solve_cluster_[l] = used;
+    }
+    for (int l = nl - 1; l >= 0; --l) {
+      const int used = launch_bwd_front(sd_, lval_.p, d_.p, wp_.p, xp_.p,
+                                        lvl_nodes_.p + sn_.lvl_ptr[l],
+                                        sn_.lvl_ptr[l + 1] - sn_.lvl_ptr[l], solve_cluster_[l],
+                                        lvl_fmax_[l], st_);
+      if (used == 0) throw CudaError("k_bwd_front: no cluster configuration fits");
+      solve_cluster_[l] = used;
+    }
     if (npaths()) {
       CK(cudaMemsetAsync(counter_.p, 0, sizeof(int), st_));
       ++epoch_;
@@ -259,6 +272,7 @@ class LdlSystem {
     fd.d = d_.p;
     fd.upd = upd_.p;
     fd.stats = ds_.p->stats;
+    fd.dscr = dscr_.p;
     return fd;
   }
 
@@ -288,9 +302,18 @@ class LdlSystem {
     for (size_t i = 0; i < at.size(); ++i)
       at[i] = make_int4(T.asm_task[i][0], T.asm_task[i][1], T.asm_task[i][2], T.asm_task[i][3]);
     asm_task_.upload(at);
-    std::vector<int2> pt(T.pn_tasks.size());
-    for (size_t i = 0; i < pt.size(); ++i) pt[i] = make_int2(T.pn_tasks[i][0], T.pn_tasks[i][1]);
+    std::vector<int4> pt(T.pn_tasks.size());
+    for (size_t i = 0; i < pt.size(); ++i)
+      pt[i] = make_int4(T.pn_tasks[i][0], T.pn_tasks[i][1], T.pn_tasks[i][2], T.pn_tasks[i][3]);
     pn_tasks_.upload(pt);
+    dg_nodes_.upload(T.dg_nodes);
+    dscr_.alloc(static_cast<size_t>(std::max(1, T.max_dg)) * (kWidePanel * kWidePanel + kWidePanel));
+    asm_cp_.upload(T.asm_cp);
+    cc_off_.upload(T.cc_off);
+    cc_ptr_.upload(T.cc_ptr);
+    cc_ubase_.upload(T.cc_ubase);
+    cc_rbase_.upload(T.cc_rbase);
+    cc_cnt_.upload(T.cc_cnt);
     std::vector<int4> tl(T.tiles.size());
     for (size_t i = 0; i < tl.size(); ++i)
       tl[i] = make_int4(T.tiles[i][0], T.tiles[i][1], T.tiles[i][2], T.tiles[i][3]);
@@ -303,14 +326,36 @@ class LdlSystem {
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     }
     lvl_cluster_.assign(static_cast<size_t>(nlevels()), 0);
+    lvl_fmax_.assign(static_cast<size_t>(nlevels()), 0);
+    solve_cluster_.assign(static_cast<size_t>(nlevels()), 1);
     for (int l = 0; l < nlevels(); ++l) {
       int fmax = 0;
       const int nf = T.lvl_ptr[l + 1] - T.lvl_ptr[l];
       for (int q = T.lvl_ptr[l]; q < T.lvl_ptr[l + 1]; ++q) fmax = std::max(fmax, T.f[T.lvl_nodes[q]]);
+      lvl_fmax_[l] = fmax;
+      {
+        int c = 16;
+        while (c > 1 && nf * c > 2 * sms) c >>= 1;
+        solve_cluster_[l] = c;
+      }
       if (fmax > kHugeFront) continue;
       int c = 16;
       while (c > 1 && nf * c > 2 * sms) c >>= 1;
       lvl_cluster_[l] = c;
+    }
+    if (std::getenv("NCL_LEVEL_STATS")) {  // diagnostic: wide-tier level profile
+      for (int l = 0; l < nlevels(); ++l) {
+        int fmax = 0, kmax = 0;
+        double fl = 0;
+        for (int q = T.lvl_ptr[l]; q < T.lvl_ptr[l + 1]; ++q) {
+          const int s = T.lvl_nodes[q], f = T.f[s], k = T.first[s + 1] - T.first[s];
+          fmax = std::max(fmax, f);
+          kmax = std::max(kmax, k);
+          for (int j = 0; j < k; ++j) fl += double(f - j - 1) * (f - j + 1);
+        }
+        std::fprintf(stderr, "[ncl level] %d fronts %d fmax %d kmax %d flops %.3g cluster %d\n", l,
+                     T.lvl_ptr[l + 1] - T.lvl_ptr[l], fmax, kmax, fl, lvl_cluster_[l]);
+      }
     }
     if (const char* e = std::getenv("NCL_WIDE_TRACE")) {
       trace_level_ = std::atoi(e);
@@ -376,6 +421,12 @@ class LdlSystem {
     sd_.asm_ptr = asm_ptr_.p;
     sd_.asm_pos = asm_pos_.p;
     sd_.asm_slot = asm_slot_.p;
+    sd_.asm_cp = asm_cp_.p;
+    sd_.cc_off = cc_off_.p;
+    sd_.cc_ptr = cc_ptr_.p;
+    sd_.cc_ubase = cc_ubase_.p;
+    sd_.cc_rbase = cc_rbase_.p;
+    sd_.cc_cnt = cc_cnt_.p;
     sd_.ch_ptr = ch_ptr_.p;
     sd_.ch = ch_.p;
     sd_.rel_ptr = rel_ptr_.p;
@@ -384,7 +435,6 @@ class LdlSystem {
     sd_.path_nodes = path_nodes_.p;
     sd_.wide = wide_.p;
     grid_ = warp_tier_grid();
-    set_wide_smem_limit(T.max_wide_f);
     CK(cudaStreamSynchronize(st_));
   }
 
@@ -396,16 +446,19 @@ class LdlSystem {
   int grid_ = 1;
   int epoch_ = 0;
   long long launches_ = 0;
-  std::vector<int> lvl_cluster_;
+  std::vector<int> lvl_cluster_, lvl_fmax_, solve_cluster_;
   int trace_level_ = -1;
   DBuf<unsigned long long> trace_;
   SnDev sd_{};
   DBuf<int> first_, f_, sparent_, rows_ptr_, rows_, u_ld_, asm_ptr_, asm_pos_, asm_slot_,
       ch_ptr_, ch_, rel_ptr_, rel_, path_ptr_, path_nodes_, lvl_nodes_, perm_, flags_,
-      counter_, fr_ptr_, fr_col_, fr_slot_;
+      counter_, fr_ptr_, fr_col_, fr_slot_, dg_nodes_, asm_cp_, cc_off_, cc_ptr_, cc_rbase_,
+      cc_cnt_;
+  DBuf<long long> cc_ubase_;
+  DBuf<double> dscr_;
   DBuf<int8_t> wide_;
   DBuf<int4> asm_task_;
-  DBuf<int2> pn_tasks_;
+  DBuf<int4> pn_tasks_;
   DBuf<int4> tiles_;
   DBuf<long long> l_off_, u_off_;
   DBuf<double> lval_, d_, upd_, uvec_, wp_, xp_, rx_, rr_, rdx_, rxn_, rrn_;

@@ -20,6 +20,12 @@ struct SnDev {
   const int* asm_ptr;
   const int* asm_pos;
   const int* asm_slot;
+  const int* asm_cp;    // N+1: asm entries of (permuted) pivot column c
+  const int* cc_off;    // nsn: wide front -> offset into cc_ptr (-1 narrow)
+  const int* cc_ptr;
+  const long long* cc_ubase;  // U_c(j, j) offset (lval if wide, else upd)
+  const int* cc_rbase;        // rel index of child row j
+  const int* cc_cnt;          // fu_c - j | (child wide) << 30
   const int* ch_ptr;
   const int* ch;
   const int* rel_ptr;  // also the offsets of the forward-solve update vectors
@@ -39,6 +45,7 @@ struct FactorDev {
   double* d;      // N (permuted order)
   double* upd;    // u_total: warp-tier update blocks
   int* stats;     // [0] n_pos [1] n_neg [2] perturbed [3] fail
+  double* dscr;   // huge-front path: per diag task {Us[32][32], rinv[32]}
 };
 
 __device__ __forceinline__ int ld_acquire(const int* p) {

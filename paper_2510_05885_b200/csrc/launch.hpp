@@ -23,14 +23,17 @@ void launch_factor_warp(const SnDev& sd, const FactorDev& fd, const double* kval
                         int* flags, int epoch, int* counter, int npaths,
                         double eps, int grid, cudaStream_t st);
 // wide_kernels.cu
-// returns the cluster size used (0: launch impossible)
+// returns the cluster size used (0: launch impossible); max_f = largest
+// front of the level (sizes the per-warp assembly accumulators)
 int launch_wide_front(const SnDev& sd, const FactorDev& fd, const double* kval, const int* nodes,
-                      int count, int cluster, double eps, cudaStream_t st,
+                      int count, int cluster, int max_f, double eps, cudaStream_t st,
                       unsigned long long* trace = nullptr);
 void launch_wide_assemble(const SnDev& sd, const FactorDev& fd, const double* kval,
                           const int4* tasks, int count, cudaStream_t st);
-void launch_wide_panel(const SnDev& sd, const FactorDev& fd, const int2* tasks, int count,
-                       int panel, double eps, cudaStream_t st);
+void launch_wide_diag(const SnDev& sd, const FactorDev& fd, const int* fronts, int count,
+                      int panel, double eps, cudaStream_t st);
+void launch_wide_panel(const SnDev& sd, const FactorDev& fd, const int4* tasks, int count,
+                       int panel, cudaStream_t st);
 void launch_wide_update(const SnDev& sd, const FactorDev& fd, const int4* tiles, int count,
                         cudaStream_t st);
 void launch_fwd_warp(const SnDev& sd, const double* lval, double* w, double* uvec,
@@ -40,17 +43,17 @@ void launch_bwd_warp(const SnDev& sd, const double* lval, const double* d,
                      const double* w, double* x, int* flags, int epoch,
                      const int8_t* wide, int* counter, int npaths, int grid,
                      cudaStream_t st);
-void launch_fwd_wide(const SnDev& sd, const double* lval, double* w, double* uvec,
-                     const int* nodes, int count, int max_f, cudaStream_t st);
-void launch_bwd_wide(const SnDev& sd, const double* lval, const double* d,
-                     const double* w, double* x, const int* nodes, int count,
-                     int max_f, cudaStream_t st);
+// wide_solve.cu: one cluster per front of a level; return the cluster used
+int launch_fwd_front(const SnDev& sd, const double* lval, double* w, double* uvec,
+                     const int* nodes, int count, int cluster, int max_f, cudaStream_t st);
+int launch_bwd_front(const SnDev& sd, const double* lval, const double* d, const double* w,
+                     double* x, const int* nodes, int count, int cluster, int max_f,
+                     cudaStream_t st);
 void launch_permute_in(int n, const int* perm, const double* b, double* w,
                        cudaStream_t st);
 void launch_permute_out(int n, const int* perm, const double* xp, double* x,
                         cudaStream_t st);
 int warp_tier_grid();
-void set_wide_smem_limit(int max_f);
 
 // kkt_kernels.cu
 void launch_assemble(const AsmDev& a, int form, int m, int m_eq, int nt,

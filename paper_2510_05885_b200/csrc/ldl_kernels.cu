@@ -13,9 +13,8 @@
 //    path order, so a warp only ever spins on work that an already-running
 //    warp owns: no deadlock, no per-level launches, and long chains
 //    (ring-shaped power grids) run at on-chip latency.
-//  * wide tier  -- fronts above 32 rows and all their ancestors.  One launch
-//    per tree level, one CTA per front; the trailing Schur update is a tiled
-//    rank-32 FP64 update through shared memory.
+//  * wide tier  -- fronts above 32 rows and all their ancestors:
+//    wide_kernels.cu (factorization) and wide_solve.cu (solves).
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -220,112 +219,6 @@ k_bwd_warp(SnDev sd, const double* __restrict__ lval, const double* __restrict__
   }
 }
 
-// wide-tier forward solve (one CTA per front of a level)
-__global__ void __launch_bounds__(kWideThreads)
-k_fwd_wide(SnDev sd, const double* __restrict__ lval, double* w, double* uvec,
-           const int* __restrict__ nodes) {
-  extern __shared__ double T[];
-  const int s = nodes[blockIdx.x];
-  const int c0 = sd.first[s], k = sd.first[s + 1] - c0, f = sd.f[s];
-  const int tid = threadIdx.x, nth = blockDim.x;
-  for (int r = tid; r < f; r += nth) T[r] = r < k ? w[c0 + r] : 0.0;
-  __syncthreads();
-  for (int cc = sd.ch_ptr[s]; cc < sd.ch_ptr[s + 1]; ++cc) {
-    const int c = sd.ch[cc];
-    const int fu = f_minus_k(sd, c);
-    for (int i = tid; i < fu; i += nth)
-      T[sd.rel[sd.rel_ptr[c] + i]] += uvec[sd.rel_ptr[c] + i];
-    __syncthreads();
-  }
-  const double* Lb = lval + sd.l_off[s];
-  const int lane = tid & 31, warp = tid >> 5;
-  // blocked: warp 0 solves the 32x32 unit-triangular diagonal block with
-  // shuffles, then every thread updates its rows below with the 32 values
-  __shared__ double Ld[32][33];
-  for (int p0 = 0; p0 < k; p0 += 32) {
-    const int p1 = min(p0 + 32, k), nb = p1 - p0;
-    for (int idx = tid; idx < nb * nb; idx += nth) {
-      const int i = idx % nb, j = idx / nb;
-      Ld[i][j] = i > j ? Lb[(p0 + i) + static_cast<size_t>(p0 + j) * f] : 0.0;
-    }
-    __syncthreads();
-    if (warp == 0) {
-      double t = lane < nb ? T[p0 + lane] : 0.0;
-      for (int p = 0; p < nb; ++p) {
-        const double wp = __shfl_sync(0xffffffffu, t, p);
-        if (lane > p && lane < nb) t -= Ld[lane][p] * wp;
-      }
-      if (lane < nb) T[p0 + lane] = t;
-    }
-    __syncthreads();
-    for (int r = p1 + tid; r < f; r += nth) {
-      double acc = T[r];
-#pragma unroll 8
-      for (int q = 0; q < nb; ++q) acc -= Lb[r + static_cast<size_t>(p0 + q) * f] * T[p0 + q];
-      T[r] = acc;
-    }
-    __syncthreads();
-  }
-  for (int r = tid; r < f; r += nth) {
-    if (r < k)
-      w[c0 + r] = T[r];
-    else
-      uvec[sd.rel_ptr[s] + r - k] = T[r];
-  }
-}
-
-// wide-tier backward solve (one CTA per front of a level, levels top-down)
-__global__ void __launch_bounds__(kWideThreads)
-k_bwd_wide(SnDev sd, const double* __restrict__ lval, const double* __restrict__ d,
-           const double* __restrict__ w, double* x, const int* __restrict__ nodes) {
-  extern __shared__ double X[];
-  __shared__ double Ld[32][33];
-  const int s = nodes[blockIdx.x];
-  const int c0 = sd.first[s], k = sd.first[s + 1] - c0, f = sd.f[s];
-  const int tid = threadIdx.x, nth = blockDim.x;
-  const int lane = tid & 31, warp = tid >> 5, nwarps = nth >> 5;
-  const int* rows = sd.rows + sd.rows_ptr[s];
-  for (int r = tid; r < f; r += nth)
-    X[r] = r < k ? w[c0 + r] / d[c0 + r] : x[rows[r]];
-  __syncthreads();
-  const double* Lb = lval + sd.l_off[s];
-  for (int p = warp; p < k; p += nwarps) {
-    double part = 0.0;
-    for (int r = k + lane; r < f; r += 32) part += Lb[r + static_cast<size_t>(p) * f] * X[r];
-    part = warp_sum(part);
-    if (lane == 0) X[p] -= part;
-  }
-  __syncthreads();
-  // blocked from the last pivot block up: GEMV with the solved pivots below
-  // the block (warp per pivot), then warp 0 finishes the diagonal block
-  for (int p1 = k; p1 > 0;) {
-    const int p0 = max(0, p1 - 32), nb = p1 - p0;
-    for (int p = p0 + warp; p < p1; p += nwarps) {
-      double part = 0.0;
-      for (int r = p1 + lane; r < k; r += 32) part += Lb[r + static_cast<size_t>(p) * f] * X[r];
-      part = warp_sum(part);
-      if (lane == 0) X[p] -= part;
-    }
-    for (int idx = tid; idx < nb * nb; idx += nth) {
-      const int i = idx % nb, j = idx / nb;
-      Ld[i][j] = i > j ? Lb[(p0 + i) + static_cast<size_t>(p0 + j) * f] : 0.0;
-    }
-    __syncthreads();
-    if (warp == 0) {
-      double xv = lane < nb ? X[p0 + lane] : 0.0;
-      for (int p = nb - 1; p >= 0; --p) {
-        const double part = (lane > p && lane < nb) ? Ld[lane][p] * xv : 0.0;
-        const double sum = warp_sum(part);
-        if (lane == p) xv -= sum;
-      }
-      if (lane < nb) X[p0 + lane] = xv;
-    }
-    __syncthreads();
-    p1 = p0;
-  }
-  for (int r = tid; r < k; r += nth) x[c0 + r] = X[r];
-}
-
 __global__ void k_permute_in(int n, const int* __restrict__ perm,
                              const double* __restrict__ b, double* w) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -365,19 +258,6 @@ void launch_bwd_warp(const SnDev& sd, const double* lval, const double* d,
                                                 wide, counter, npaths);
 }
 
-void launch_fwd_wide(const SnDev& sd, const double* lval, double* w, double* uvec,
-                     const int* nodes, int count, int max_f, cudaStream_t st) {
-  if (count == 0) return;
-  k_fwd_wide<<<count, kWideThreads, sizeof(double) * max_f, st>>>(sd, lval, w, uvec, nodes);
-}
-
-void launch_bwd_wide(const SnDev& sd, const double* lval, const double* d,
-                     const double* w, double* x, const int* nodes, int count,
-                     int max_f, cudaStream_t st) {
-  if (count == 0) return;
-  k_bwd_wide<<<count, kWideThreads, sizeof(double) * max_f, st>>>(sd, lval, d, w, x, nodes);
-}
-
 void launch_permute_in(int n, const int* perm, const double* b, double* w,
                        cudaStream_t st) {
   if (n == 0) return;
@@ -388,14 +268,6 @@ void launch_permute_out(int n, const int* perm, const double* xp, double* x,
                         cudaStream_t st) {
   if (n == 0) return;
   k_permute_out<<<(n + 255) / 256, 256, 0, st>>>(n, perm, xp, x);
-}
-
-void set_wide_smem_limit(int max_f) {
-  const int bytes = static_cast<int>(sizeof(double)) * (max_f > 0 ? max_f : 1);
-  if (bytes > 48 * 1024) {
-    cudaFuncSetAttribute(k_fwd_wide, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-    cudaFuncSetAttribute(k_bwd_wide, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-  }
 }
 
 int warp_tier_grid() {

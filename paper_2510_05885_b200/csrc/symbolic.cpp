@@ -543,6 +543,7 @@ Supernodal build_supernodal(const LowerCsc& A, const Symbolic& S) {
   std::vector<int> mark(static_cast<size_t>(n), -1), pos(static_cast<size_t>(n), -1);
   std::vector<int> below;
   T.asm_ptr.assign(static_cast<size_t>(nsn) + 1, 0);
+  T.asm_cp.assign(static_cast<size_t>(n) + 1, 0);
   T.rel_ptr.assign(static_cast<size_t>(nsn) + 1, 0);
   for (int s = 0; s < nsn; ++s) {
     const int c0 = T.first[s], c1 = T.first[s + 1], k = c1 - c0;
@@ -575,11 +576,13 @@ Supernodal build_supernodal(const LowerCsc& A, const Symbolic& S) {
     T.rows_ptr[s + 1] = static_cast<int>(T.rows.size());
     const int* rs = T.rows.data() + T.rows_ptr[s];
     for (int i = 0; i < T.f[s]; ++i) pos[rs[i]] = i;
-    for (int c = c0; c < c1; ++c)
+    for (int c = c0; c < c1; ++c) {
+      T.asm_cp[c] = static_cast<int>(T.asm_pos.size());
       for (int q = lcp[c]; q < lcp[c + 1]; ++q) {
         T.asm_pos.push_back(pos[lri[q]] | ((c - c0) << 16));
         T.asm_slot.push_back(lsl[q]);
       }
+    }
     T.asm_ptr[s + 1] = static_cast<int>(T.asm_pos.size());
     for (int q = T.ch_ptr[s]; q < T.ch_ptr[s + 1]; ++q) {
       const int c = T.ch[q];
@@ -591,6 +594,7 @@ Supernodal build_supernodal(const LowerCsc& A, const Symbolic& S) {
     }
     T.max_f = std::max(T.max_f, T.f[s]);
   }
+  T.asm_cp[n] = static_cast<int>(T.asm_pos.size());
   // rel maps (need final row lists of parents)
   for (int c = 0; c < nsn; ++c) {
     const int kc = T.first[c + 1] - T.first[c];
@@ -699,21 +703,51 @@ Supernodal build_supernodal(const LowerCsc& A, const Symbolic& S) {
     for (int s = 0; s < nsn; ++s)
       if (T.wide[s]) T.lvl_nodes[nx[wl[s]]++] = s;
   }
-  // wide-tier launch schedule: per level, assembly tasks (front, 64-column
-  // block); per (level, panel) the fronts that factor that panel and the
-  // 64x64 tiles of their trailing lower triangle
+  // column-wise extend-add lists of the wide fronts: front column J receives
+  // child column j iff rel_c[j] == J; entries in child order so the sums are
+  // accumulated in the same (deterministic) order as a child-by-child pass
+  T.cc_off.assign(static_cast<size_t>(nsn), -1);
+  T.cc_ptr.assign(1, 0);
+  {
+    std::vector<std::vector<std::array<int, 2>>> colv;
+    auto push = [&](int c, int j) {
+      const int fu = T.f[c] - (T.first[c + 1] - T.first[c]);
+      const long long ld = T.u_ld[c];
+      T.cc_ubase.push_back(T.u_off[c] + j * ld + j);
+      T.cc_rbase.push_back(T.rel_ptr[c] + j);
+      T.cc_cnt.push_back((fu - j) | (T.wide[c] ? (1 << 30) : 0));
+    };
+    for (int s = 0; s < nsn; ++s) {
+      if (!T.wide[s]) continue;
+      T.cc_off[s] = static_cast<int>(T.cc_ptr.size()) - 1;
+      colv.assign(static_cast<size_t>(T.f[s]), {});
+      for (int q = T.ch_ptr[s]; q < T.ch_ptr[s + 1]; ++q) {
+        const int c = T.ch[q];
+        const int fu = T.f[c] - (T.first[c + 1] - T.first[c]);
+        for (int j = 0; j < fu; ++j) colv[T.rel[T.rel_ptr[c] + j]].push_back({c, j});
+      }
+      for (int J = 0; J < T.f[s]; ++J) {
+        for (const auto& e : colv[J]) push(e[0], e[1]);
+        T.cc_ptr.push_back(static_cast<int>(T.cc_cnt.size()));
+      }
+    }
+  }
+  // huge-front launch schedule: per level, assembly tasks (front, kAsmCols
+  // columns); per (level, panel) the fronts that factor that panel, their
+  // TRSM row blocks and the 32x32 tiles of their trailing lower triangle
   T.asm_task_ptr.assign(1, 0);
   T.lp_ptr.assign(static_cast<size_t>(nlev) + 1, 0);
   T.pn_ptr.assign(1, 0);
   T.tl_ptr.assign(1, 0);
+  T.dg_ptr.assign(1, 0);
   for (int l = 0; l < nlev; ++l) {
-    int maxp = 0;
-    for (int q = T.lvl_ptr[l]; q < T.lvl_ptr[l + 1]; ++q) {
+    int maxp = 0, fmax = 0;
+    for (int q = T.lvl_ptr[l]; q < T.lvl_ptr[l + 1]; ++q) fmax = std::max(fmax, T.f[T.lvl_nodes[q]]);
+    const bool huge = fmax > kHugeFront;
+    for (int q = T.lvl_ptr[l]; q < T.lvl_ptr[l + 1] && huge; ++q) {
       const int s = T.lvl_nodes[q];
       const int f = T.f[s], k = T.first[s + 1] - T.first[s];
-      for (int cb = 0; cb * kWideTile < f; ++cb)
-        for (int rb = cb; rb * kWideTile < f; ++rb)
-          T.asm_task.push_back({s, rb * kWideTile, cb * kWideTile, 0});
+      for (int cb = 0; cb < f; cb += kAsmCols) T.asm_task.push_back({s, cb, 0, 0});
       maxp = std::max(maxp, (k + kWidePanel - 1) / kWidePanel);
     }
     T.asm_task_ptr.push_back(static_cast<int>(T.asm_task.size()));
@@ -724,8 +758,10 @@ Supernodal build_supernodal(const LowerCsc& A, const Symbolic& S) {
         if (k <= p * kWidePanel) continue;
         const int p1 = std::min((p + 1) * kWidePanel, k);
         const int mt = f - p1;
-        const int nrb = std::max(1, (mt + kPanelRows - 1) / kPanelRows);
-        for (int rb = 0; rb < nrb; ++rb) T.pn_tasks.push_back({s, rb});
+        const int di = static_cast<int>(T.dg_nodes.size()) - T.dg_ptr.back();
+        T.dg_nodes.push_back(s);
+        const int nrb = (mt + kPanelRows - 1) / kPanelRows;
+        for (int rb = 0; rb < nrb; ++rb) T.pn_tasks.push_back({s, rb, di, 0});
         const int nt = (mt + kUpdTile - 1) / kUpdTile;
         for (int ti = 0; ti < nt; ++ti)
           for (int tj = 0; tj <= ti; ++tj)
@@ -734,6 +770,8 @@ Supernodal build_supernodal(const LowerCsc& A, const Symbolic& S) {
       }
       T.pn_ptr.push_back(static_cast<int>(T.pn_tasks.size()));
       T.tl_ptr.push_back(static_cast<int>(T.tiles.size()));
+      T.dg_ptr.push_back(static_cast<int>(T.dg_nodes.size()));
+      T.max_dg = std::max(T.max_dg, T.dg_ptr.back() - T.dg_ptr[T.dg_ptr.size() - 2]);
     }
     T.lp_ptr[l + 1] = T.lp_ptr[l] + maxp;
   }

@@ -66,6 +66,15 @@ struct Supernodal {
   long long u_total = 0;
   // assembly of A into the front: packed (front_row | front_col << 16), slot
   std::vector<int> asm_ptr, asm_pos, asm_slot;
+  std::vector<int> asm_cp;  // n+1: asm entries of pivot column c (global)
+  // wide fronts, column-wise extend-add: for front column J of wide front s
+  // the children's columns landing in it, in child order:
+  // cc_ent[cc_ptr[cc_off[s] + J] .. cc_ptr[cc_off[s] + J + 1]) = {child, col}
+  // entry = {element offset of U_c(j, j) in its buffer (lval if the child
+  // is wide, else upd), rel index of row j, count fu_c - j, child is wide}
+  std::vector<int> cc_off, cc_ptr;
+  std::vector<long long> cc_ubase;
+  std::vector<int> cc_rbase, cc_cnt;
   // children in increasing order and their update-row map into the parent
   std::vector<int> ch_ptr, ch;
   std::vector<int> rel_ptr, rel;  // indexed by child: f_c - k_c entries
@@ -77,13 +86,17 @@ struct Supernodal {
   std::vector<int> path_ptr, path_nodes;
   // wide tier: level lists (level 0 = deepest wide fronts)
   std::vector<int> lvl_ptr, lvl_nodes;
-  // wide-tier schedule: assembly tasks {front, column block} per level;
-  // panels of level l are lp_ptr[l]..lp_ptr[l+1]-1 (global panel index g),
-  // panel tasks {front, row block} of panel g are pn_tasks[pn_ptr[g]..],
-  // trailing-update tiles {front, row0, col0, panel} are tiles[tl_ptr[g]..]
-  std::vector<std::array<int, 4>> asm_task;  // {front, row0, col0, 0}
-  std::vector<std::array<int, 2>> pn_tasks;
-  std::vector<int> asm_task_ptr, lp_ptr, pn_ptr, tl_ptr;
+  // huge-front (three-kernel) schedule: assembly tasks {front, first
+  // column} per level (kAsmCols columns each); panels of level l are
+  // lp_ptr[l]..lp_ptr[l+1]-1 (global panel index g); the fronts factoring
+  // panel g are dg_nodes[dg_ptr[g]..]; TRSM tasks {front, row block, diag
+  // task index} are pn_tasks[pn_ptr[g]..]; trailing-update tiles {front,
+  // row0, col0, panel} are tiles[tl_ptr[g]..]
+  std::vector<std::array<int, 4>> asm_task;  // {front, col0, 0, 0}
+  std::vector<std::array<int, 4>> pn_tasks;
+  std::vector<int> dg_nodes;
+  std::vector<int> asm_task_ptr, lp_ptr, pn_ptr, tl_ptr, dg_ptr;
+  int max_dg = 0;  // most fronts in one huge panel launch
   std::vector<std::array<int, 4>> tiles;
   long long wide_update_flops = 0;
   int max_f = 0, max_wide_f = 0;
@@ -94,9 +107,9 @@ struct Supernodal {
 
 constexpr int kWarpFront = 32;
 constexpr int kWidePanel = 32;  // pivots per panel of a wide front
-constexpr int kWideTile = 64;   // assembly tile edge
+constexpr int kAsmCols = 8;     // front columns per assembly task (warp each)
 constexpr int kUpdTile = 32;    // trailing-update tile edge (one warp)
-constexpr int kPanelRows = 128; // rows below a panel staged per CTA pass
+constexpr int kPanelRows = 256; // rows below a panel solved per CTA (thread each)
 constexpr int kHugeFront = 1536;  // levels with a larger front use the
                                   // three-kernel (whole-GPU) path
 
