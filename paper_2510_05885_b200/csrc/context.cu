@@ -26,8 +26,12 @@
 #include "cuda_util.hpp"
 #include "kkt_plan.hpp"
 #include "launch.hpp"
+#include "layout.hpp"
 
 namespace nclb {
+
+// the wide-tier staging copies whole 34-row column chunks: pad the L buffer
+constexpr size_t kLvalPad = 256;
 
 std::string& last_error() {
   static thread_local std::string e;
@@ -93,7 +97,9 @@ class LdlSystem {
                                            T.lvl_ptr[l + 1] - T.lvl_ptr[l], lvl_cluster_[l],
                                            lvl_fmax_[l], eps, st_, tr);
         if (tr) dump_trace(l);
-        if (used == 0) throw CudaError("k_wide_front: no cluster configuration fits");
+        if (used == 0)
+          throw CudaError(std::string("k_wide_front: no cluster configuration fits: ") +
+                          wide_last_error);
         lvl_cluster_[l] = used;
         launches_ += 1;
         continue;
@@ -251,12 +257,13 @@ class LdlSystem {
     // column j of L: rows below j in the front of its supernode, ascending
     for (int s = 0; s < nsn; ++s) {
       const int c0 = sn_.first[s], k = sn_.first[s + 1] - c0, f = sn_.f[s];
+      const long long ld = sn_.wide[s] ? wide_ld(f) : f;
       const int* rows = sn_.rows.data() + sn_.rows_ptr[s];
       for (int p = 0; p < k; ++p) {
         int q = S_.lcol_ptr[c0 + p];
         for (int r = p + 1; r < f; ++r, ++q) {
           if (lrow_ind) lrow_ind[q] = rows[r];
-          if (lval) lval[q] = lv[static_cast<size_t>(sn_.l_off[s] + r + static_cast<long long>(p) * f)];
+          if (lval) lval[q] = lv[static_cast<size_t>(sn_.l_off[s] + r + p * ld)];
         }
       }
     }
@@ -363,7 +370,7 @@ class LdlSystem {
       trace_.zero(st_);
     }
     perm_.upload(S_.perm);
-    lval_.alloc(static_cast<size_t>(T.l_off[T.nsn]));
+    lval_.alloc(static_cast<size_t>(T.l_off[T.nsn]) + kLvalPad);
     lval_.zero(st_);
     d_.alloc(static_cast<size_t>(N_));
     upd_.alloc(static_cast<size_t>(T.u_total));

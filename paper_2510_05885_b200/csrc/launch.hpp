@@ -28,6 +28,7 @@ void launch_factor_warp(const SnDev& sd, const FactorDev& fd, const double* kval
 int launch_wide_front(const SnDev& sd, const FactorDev& fd, const double* kval, const int* nodes,
                       int count, int cluster, int max_f, double eps, cudaStream_t st,
                       unsigned long long* trace = nullptr);
+extern const char* wide_last_error;
 void launch_wide_assemble(const SnDev& sd, const FactorDev& fd, const double* kval,
                           const int4* tasks, int count, cudaStream_t st);
 void launch_wide_diag(const SnDev& sd, const FactorDev& fd, const int* fronts, int count,

@@ -1,5 +1,6 @@
 // Host symbolic analysis (see symbolic.hpp).
 #include "symbolic.hpp"
+#include "layout.hpp"
 
 #include <algorithm>
 #include <cmath>
@@ -619,8 +620,9 @@ Supernodal build_supernodal(const LowerCsc& A, const Symbolic& S) {
   }
   // storage.  Warp tier: an f x k column-major L block in lval and a compact
   // (f-k)^2 update block in upd.  Wide tier: the whole f x f column-major
-  // front lives in lval (its first k columns ARE the L block, ld = f) and the
-  // update block is the trailing (f-k)^2 corner of it (u_ld = f).
+  // front lives in lval (its first k columns ARE the L block, leading
+  // dimension wide_ld(f) = f rounded up to even) and the update block is the
+  // trailing (f-k)^2 corner of it (u_ld = wide_ld(f)).
   T.l_off.assign(static_cast<size_t>(nsn) + 1, 0);
   T.u_off.assign(static_cast<size_t>(nsn), 0);
   T.u_ld.assign(static_cast<size_t>(nsn), 0);
@@ -629,9 +631,10 @@ Supernodal build_supernodal(const LowerCsc& A, const Symbolic& S) {
     const int k = T.first[s + 1] - T.first[s];
     const int fu = T.f[s] - k;
     if (T.wide[s]) {
-      T.l_off[s + 1] = T.l_off[s] + static_cast<long long>(T.f[s]) * T.f[s];
-      T.u_off[s] = T.l_off[s] + static_cast<long long>(k) * T.f[s] + k;
-      T.u_ld[s] = T.f[s];
+      const long long ld = wide_ld(T.f[s]);
+      T.l_off[s + 1] = T.l_off[s] + ld * T.f[s];
+      T.u_off[s] = T.l_off[s] + static_cast<long long>(k) * ld + k;
+      T.u_ld[s] = static_cast<int>(ld);
       T.max_wide_f = std::max(T.max_wide_f, T.f[s]);
       T.wide_front_elems += static_cast<long long>(T.f[s]) * T.f[s];
     } else {
@@ -640,6 +643,7 @@ Supernodal build_supernodal(const LowerCsc& A, const Symbolic& S) {
       T.u_ld[s] = fu;
       uoff += static_cast<long long>(fu) * fu;
     }
+    T.l_off[s + 1] = (T.l_off[s + 1] + 1) & ~1LL;  // every block 16-byte aligned
   }
   T.u_total = uoff;
   // heights (supernodal), heavy child = child of maximal height

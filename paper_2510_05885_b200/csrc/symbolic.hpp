@@ -109,7 +109,7 @@ constexpr int kWarpFront = 32;
 constexpr int kWidePanel = 32;  // pivots per panel of a wide front
 constexpr int kAsmCols = 8;     // front columns per assembly task (warp each)
 constexpr int kUpdTile = 32;    // trailing-update tile edge (one warp)
-constexpr int kPanelRows = 256; // rows below a panel solved per CTA (thread each)
+constexpr int kPanelRows = 128; // rows below a panel solved per CTA (huge path)
 constexpr int kHugeFront = 1536;  // levels with a larger front use the
                                   // three-kernel (whole-GPU) path
 

@@ -1,28 +1,33 @@
 // Wide-tier numeric factorization (fronts above 32 rows and their ancestors).
 //
-// A wide front is f x f column-major, resident in HBM/L2 inside the L buffer
-// (its first k columns are the L block, the trailing (f-k)^2 corner the
-// update matrix the parent extend-adds from).  Building blocks, all written
-// as compact loops so the code stays resident in the instruction cache (a
-// fully unrolled 32-pivot body is tens of KB of straight-line SASS that is
-// fetched from L2 on every panel -- that, not arithmetic, was the cost):
+// A wide front is f x f column-major with leading dimension ld = wide_ld(f)
+// (even: every column starts 16-byte aligned), resident in HBM/L2 inside the
+// L buffer; its first k columns are the L block, the trailing (f-k)^2 corner
+// the update matrix the parent extend-adds from.
+//
+// Data movement: every block a kernel computes on is staged into shared
+// memory with 16-byte cp.async copies.  Measured on B200 (tools/ubench_ld.cu),
+// one warp pulls a 32x32 FP64 block out of L2 in ~1.2K cycles that way versus
+// 3.3-7K cycles with register loads (too few loads in flight per warp) -- the
+// difference between a latency-bound and a DMMA-bound trailing update.
+//
+// Building blocks:
 //   assemble_col  -- (WARP) one front column: zero, scatter A, extend-add the
 //                    children's columns that land in it, child by child
-//                    (deterministic order), accumulated in shared memory and
-//                    written once;
+//                    (deterministic order), accumulated in shared memory;
 //   diag_block    -- (WARP) static-pivot LDL^T of a <=32-pivot diagonal block
 //                    (sparse.cpp:235-247 pivot rule, inertia, perturbed
-//                    counts); a lane owns one row in registers and the row is
-//                    rotated one column per pivot, so every register index is
-//                    static while the pivot loop stays a loop;
-//   trsm_rows     -- (THREAD per row) the rows below the block against the
-//                    unscaled diagonal columns, same rotation scheme;
-//   warp_update_tile -- (WARP) F22 -= L21 D L21^T on a 32x32 tile with FP64
+//                    counts); a lane owns one row in registers, rotated one
+//                    column per pivot (static register indices, compact loop);
+//   trsm_rows     -- (THREAD per row) the rows below the block, in lockstep
+//                    with diag_block through a shared-memory progress flag;
+//   group_tile    -- (4 WARPS) F22 -= L21 D L21^T on a 32x32 tile: A, B, C
+//                    staged by cp.async, each warp an 8-row slice on FP64
 //                    tensor cores (mma.sync.m8n8k4.f64 = DMMA).
 // k_wide_front runs a whole tree level in ONE launch: one thread-block
-// cluster (1..16 CTAs) per front walks assembly -> [panel -> trailing
-// update]* with cluster barriers between phases.  Levels holding huge fronts
-// use the multi-kernel path (k_wide_assemble / k_wide_diag / k_wide_panel /
+// cluster (1..16 CTAs) per front walks assembly -> panels with one panel of
+// lookahead (see the panel loop).  Levels holding huge fronts use the
+// multi-kernel path (k_wide_assemble / k_wide_diag / k_wide_panel /
 // k_wide_update) so one front spreads over every SM.
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
@@ -30,15 +35,21 @@
 
 #include "device.cuh"
 #include "launch.hpp"
+#include "layout.hpp"
 #include "symbolic.hpp"
 
 namespace cg = cooperative_groups;
 
 namespace nclb {
 
-constexpr int kThreads = 384;
+constexpr int kThreads = 512;
 constexpr int kWarps = kThreads / 32;
-constexpr int kHugeThreads = 256;
+constexpr int kGroups = kWarps / 4;   // 4-warp tile groups
+constexpr int kSL = 40;               // smem column stride of a staged 32-row block
+constexpr int kTrsRows = 96;          // rows per TRSM round (warps 1..3)
+constexpr int kSLT = kTrsRows + 2;    // smem column stride of the TRSM stage
+constexpr int kHugeRows = 128;        // TRSM rows per CTA, huge path
+constexpr int kSLH = kHugeRows + 2;
 constexpr unsigned kFull = 0xffffffffu;
 
 // Us[p][j] = unscaled u = F(p0+p+1+j, p0+p) after the first p pivots (zero
@@ -47,7 +58,35 @@ struct PanelSmem {
   double Us[kWidePanel][kWidePanel];
   double rinv[kWidePanel];
   double Lsh[kWidePanel][kWidePanel + 1];  // scaled L11 (published late)
+  int prog;                                // pivots of the block published
+  int qctr;                                // deferred-update tile queue
+  int gq[kGroups];                         // per-group dequeued tile
 };
+
+struct GroupSmem {
+  double A[kWidePanel * kSL], B[kWidePanel * kSL], C[kWidePanel * kSL];
+  double d[kWidePanel];
+};
+
+struct RowSmem {  // per-group buffers of groups 1..3
+  GroupSmem g;
+};
+
+// dynamic shared memory of k_wide_front (the assembly accumulators alias it).
+// Group 0 (warps 0-3) computes phase-B tiles in the diagonal / TRSM stage,
+// which is idle then; groups 1-3 have their own tile buffers.
+struct StageSmem {
+  union {
+    struct {
+      double D[kWidePanel * kSL];    // diagonal block
+      double TR[kWidePanel * kSLT];  // TRSM rows
+    } p;
+    GroupSmem g0;
+  } u;
+  RowSmem r[kGroups - 1];
+};
+
+
 
 __device__ __forceinline__ unsigned long long globaltimer() {
   unsigned long long t;
@@ -55,9 +94,51 @@ __device__ __forceinline__ unsigned long long globaltimer() {
   return t;
 }
 
+__device__ __forceinline__ void cp16(void* dst, const void* src) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+__device__ __forceinline__ void named_bar(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+// rows [r0, r0+nr) x columns [c0, c0+nc) of the column-major M (ld even, base
+// 16-byte aligned) -> S with column stride SL: element (r0+i, c0+j) lands at
+// S[j*SL + i + sh], sh = r0 & 1.  Every column copies NR2 16-byte chunks from
+// the even row below r0 (a compile-time count: no integer division in the
+// issue loop; rows past the block are harmless reads -- the L buffer is
+// padded at its end).  Issued by thread t of nthr; completion: cp_wait_all /
+// cp_wait_group + a barrier.
+template <int NR2>
+__device__ __forceinline__ int stage_block(double* S, int SL, const double* M, size_t ld, int r0,
+                                           int c0, int nc, int t, int nthr) {
+  const int a = r0 & ~1;
+  const double* src = M + a + c0 * ld;
+  for (int idx = t; idx < NR2 * nc; idx += nthr) {
+    const int j = idx / NR2, ch = idx - j * NR2;
+    cp16(S + j * SL + 2 * ch, src + 2 * ch + j * ld);
+  }
+  return r0 - a;
+}
+constexpr int kNR2 = (kUpdTile + 2) / 2;  // 32 rows + shift -> 17 chunks
+
+// progress flag in shared memory: release by the diagonal warp, acquire by
+// the lockstep TRSM warps (no MEMBAR.SC / system-scope generic stores)
+__device__ __forceinline__ void st_release_smem(int* p, int v) {
+  const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(p));
+  asm volatile("st.release.cta.shared::cta.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ int ld_acquire_smem(const int* p) {
+  const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(p));
+  int v;
+  asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+  return v;
+}
+
 // lower-triangular tile index -> (row block, col block), row >= col
 __device__ __forceinline__ void tri_decode(int t, int& i, int& j) {
-  int r = static_cast<int>((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
+  int r = static_cast<int>((sqrtf(8.0f * t + 1.0f) - 1.0f) * 0.5f);
   while (r * (r + 1) / 2 > t) --r;
   while ((r + 1) * (r + 2) / 2 <= t) ++r;
   i = r;
@@ -69,9 +150,9 @@ __device__ __forceinline__ void tri_decode(int t, int& i, int& j) {
 // private to this warp, or nullptr to accumulate in place (huge fronts).
 __device__ __noinline__ void assemble_col(const SnDev& sd, const FactorDev& fd,
                                           const double* __restrict__ kval, int s, int c0, int k,
-                                          int f, double* F, int J, double* acc) {
+                                          int f, double* F, size_t ld, int J, double* acc) {
   const int lane = threadIdx.x & 31;
-  double* col = F + static_cast<size_t>(J) * f;
+  double* col = F + J * ld;
   double* a = acc ? acc : col;
   const int cb = sd.cc_off[s] + J;
   const int e0 = sd.cc_ptr[cb], e1 = sd.cc_ptr[cb + 1];
@@ -93,92 +174,178 @@ __device__ __noinline__ void assemble_col(const SnDev& sd, const FactorDev& fd,
     for (int r = J + lane; r < f; r += 32) col[r] = a[r];
 }
 
+// 1/d without the branchy slow path of __drcp_rn (which splits the pivot loop
+// into basic blocks the scheduler cannot interleave across): MUFU.RCP64H
+// seed + two Newton steps, within 1 ulp for the pivot magnitudes static
+// pivoting admits (|d| >= eps; NaN/Inf propagate and are flagged).
+__device__ __forceinline__ double rcp_nr(double d) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
+  double e = fma(-d, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-d, r, 1.0);
+  return fma(r, e, r);
+}
+
 // ---------------------------------------------------------------------------
-// static-pivot LDL^T of the nb-pivot diagonal block at p0 (one warp).  Fills
-// sm.Us / sm.rinv (and sm.Lsh with the scaled L11).  With `dout` (publisher
-// only) writes D and adds the inertia / perturbed / failure counts.
-__device__ __noinline__ void diag_block(const double* F, int f, int p0, int nb, double eps,
-                                        PanelSmem& sm, double* dout, int* stats) {
+// Pivots [pb, pe) of the diagonal block with a rotation width of W registers:
+// after p pivots only columns p..31 of the block are live, so the later
+// quarters rotate 24 / 16 / 8 registers instead of 32.  Branch-free: lanes
+// that are not below the pivot write zeros to slots nobody reads.
+template <int W>
+__device__ __forceinline__ void diag_pivot(int p, int nb, double eps, double (&a)[kWidePanel],
+                                           double& dnext, double& myd, int& pf, int& bad, int lane,
+                                           PanelSmem& sm) {
+  double dp = dnext;
+  const bool small = fabs(dp) < eps;
+  dp = small ? (dp >= 0.0 ? eps : -eps) : dp;
+  const bool below = lane > p && lane < nb;
+  const double u = below ? a[0] : 0.0;
+  const double u1 = __shfl_sync(kFull, u, (p + 1) & 31);  // u of row p+1
+  const double rp = rcp_nr(dp);
+  const double l = u * rp;
+  const double n0 = a[1] - l * u1;  // this row's entry in column p+1
+  dnext = __shfl_sync(kFull, n0, (p + 1) & 31);
+  sm.Us[p][below ? lane - p - 1 : kWidePanel - 1] = u;  // slot 31 stays zero
+  sm.Lsh[lane][p] = l;
+  sm.rinv[p] = rp;
+  myd = lane == p ? dp : myd;
+  pf |= (lane == p) & small;
+  bad |= !isfinite(l);
+  __syncwarp();
+  const double2* up = reinterpret_cast<const double2*>(sm.Us[p]);
+  a[0] = n0;
+  {
+    const double2 v = up[0];
+    a[1] = a[2] - l * v.y;
+  }
+#pragma unroll
+  for (int j = 2; j < W; j += 2) {
+    const double2 v = up[j >> 1];
+    a[j] = a[j + 1] - l * v.x;
+    a[j + 1] = (j + 2 < W ? a[j + 2] : 0.0) - l * v.y;
+  }
+}
+
+// Pivots [pb, pe) with rotation width W, four per straight-line block so the
+// scheduler overlaps pivot p+1's chain with pivot p's row update; the
+// lockstep TRSM is released after every four pivots.
+template <int W>
+__device__ __forceinline__ void diag_steps(int pb, int pe, int nb, double eps, double (&a)[kWidePanel],
+                                           double& dnext, double& myd, int& pf, int& bad, int lane,
+                                           PanelSmem& sm, int* prog) {
+  int p = pb;
+#pragma unroll 1
+  for (; p + 4 <= pe; p += 4) {
+    diag_pivot<W>(p, nb, eps, a, dnext, myd, pf, bad, lane, sm);
+    diag_pivot<W>(p + 1, nb, eps, a, dnext, myd, pf, bad, lane, sm);
+    diag_pivot<W>(p + 2, nb, eps, a, dnext, myd, pf, bad, lane, sm);
+    diag_pivot<W>(p + 3, nb, eps, a, dnext, myd, pf, bad, lane, sm);
+    if (prog && lane == 0) st_release_smem(prog, p + 4);
+  }
+#pragma unroll 1
+  for (; p < pe; ++p) {
+    diag_pivot<W>(p, nb, eps, a, dnext, myd, pf, bad, lane, sm);
+    if (prog && lane == 0) st_release_smem(prog, p + 1);
+  }
+}
+
+// static-pivot LDL^T of the nb-pivot diagonal block at p0 (one warp), staged
+// through D (32 x kSL doubles).  Fills sm.Us / sm.rinv / sm.Lsh and, when
+// `prog` is given, publishes pivot p by setting *prog = p + 1 (threads running
+// trsm_rows in lockstep wait on it).  With `dout` (publisher only) writes D
+// and adds the inertia / perturbed / failure counts.
+//
+// The pivot chain is d_p -> 1/d_p -> l = u/d_p -> next diagonal
+// a' = a(p+1, p+1) - l u(p+1) -> shuffle: the next diagonal is formed with a
+// shuffle of u from lane p+1 instead of the shared-memory row, so only ~170
+// cycles per pivot are serial and the rest of the row update overlaps it.
+__device__ __noinline__ void diag_block(const double* F, size_t ld, int p0, int nb, double eps,
+                                        PanelSmem& sm, double* D, double* dout, int* stats,
+                                        int* prog) {
   const int lane = threadIdx.x & 31;
+  const int sh = stage_block<kNR2>(D, kSL, F, ld, p0, p0, nb, lane, 32);
   double* us = &sm.Us[0][0];
   for (int i = lane; i < kWidePanel * kWidePanel; i += 32) us[i] = 0.0;
+  cp_wait_all();
+  __syncwarp();
   double a[kWidePanel];  // a[j] = current F(p0+lane, p0+p+j)
 #pragma unroll
-  for (int j = 0; j < kWidePanel; ++j)
-    a[j] = (lane < nb && j <= lane) ? __ldcg(F + (p0 + lane) + static_cast<size_t>(p0 + j) * f) : 0.0;
+  for (int j = 0; j < kWidePanel; ++j) a[j] = (lane < nb && j <= lane) ? D[j * kSL + lane + sh] : 0.0;
+  double myd = 0.0;  // lane p keeps d_p
+  int pf = 0, bad = 0;
+  double dnext = __shfl_sync(kFull, a[0], 0);
+  diag_steps<32>(0, min(nb, 8), nb, eps, a, dnext, myd, pf, bad, lane, sm, prog);
+  diag_steps<24>(8, min(nb, 16), nb, eps, a, dnext, myd, pf, bad, lane, sm, prog);
+  diag_steps<16>(16, min(nb, 24), nb, eps, a, dnext, myd, pf, bad, lane, sm, prog);
+  diag_steps<8>(24, nb, nb, eps, a, dnext, myd, pf, bad, lane, sm, prog);
   __syncwarp();
-  int npos = 0, nneg = 0, pert = 0, fail = 0;
-#pragma unroll 1
-  for (int p = 0; p < nb; ++p) {
-    double dp = __shfl_sync(kFull, a[0], p);
-    int pflag = 0;
-    if (fabs(dp) < eps) {
-      dp = (dp >= 0.0) ? eps : -eps;
-      pflag = 1;
-    }
-    const double rp = __drcp_rn(dp);
-    const bool below = lane > p && lane < nb;
-    const double u = below ? a[0] : 0.0;
-    const double l = u * rp;
-    if (below) {
-      sm.Us[p][lane - p - 1] = u;
-      sm.Lsh[lane][p] = l;
-      if (!isfinite(l)) fail = 1;
-    }
-    if (lane == 0) {
-      sm.rinv[p] = rp;
-      if (dout) dout[p] = dp;
-      pert += pflag;
-      if (!isfinite(dp) || dp == 0.0) fail = 1;
-      if (dp > 0.0)
-        npos++;
-      else
-        nneg++;
-    }
-    __syncwarp();
-    const double2* up = reinterpret_cast<const double2*>(sm.Us[p]);
-#pragma unroll
-    for (int j = 0; j < kWidePanel; j += 2) {
-      const double2 v = up[j >> 1];
-      a[j] = a[j + 1] - l * v.x;
-      a[j + 1] = (j + 2 < kWidePanel ? a[j + 2] : 0.0) - l * v.y;
-    }
-  }
-  __syncwarp();
+  if (dout && lane < nb) dout[lane] = myd;
   if (stats) {
-    fail = __any_sync(kFull, fail);
+    const bool mine = lane < nb;
+    const unsigned pos = __ballot_sync(kFull, mine && myd > 0.0);
+    const unsigned neg = __ballot_sync(kFull, mine && !(myd > 0.0));
+    const unsigned per = __ballot_sync(kFull, mine && pf);
+    const bool fail = __any_sync(kFull, bad || (mine && (!isfinite(myd) || myd == 0.0)));
     if (lane == 0) {
-      if (npos) atomicAdd(stats + 0, npos);
-      if (nneg) atomicAdd(stats + 1, nneg);
-      if (pert) atomicAdd(stats + 2, pert);
+      if (pos) atomicAdd(stats + 0, __popc(pos));
+      if (neg) atomicAdd(stats + 1, __popc(neg));
+      if (per) atomicAdd(stats + 2, __popc(per));
       if (fail) atomicOr(stats + 3, 1);
     }
   }
 }
 
-// rows [row_lo, row_hi) of panel columns [p0, p0+nb): L(r, :) from the
-// unscaled diagonal columns us (32x32) and 1/d (thread per row)
-__device__ __noinline__ void trsm_rows(double* F, int f, int p0, int nb, int row_lo, int row_hi,
-                                       const double* us, const double* rinv, int* stats) {
-  bool bad = false;
-  for (int r = row_lo + static_cast<int>(threadIdx.x); r < row_hi; r += blockDim.x) {
-    double x[kWidePanel];
-    double* row = F + r + static_cast<size_t>(p0) * f;
-#pragma unroll
-    for (int q = 0; q < kWidePanel; ++q) x[q] = q < nb ? __ldcg(row + static_cast<size_t>(q) * f) : 0.0;
+// TRSM pivots [pb, pe) for one row with rotation width W (see diag_steps)
+template <int W>
+__device__ __forceinline__ void trsm_steps(int pb, int pe, double (&x)[kWidePanel], double* row,
+                                           size_t ld, const double* us, const double* rinv,
+                                           const int* prog, bool& bad) {
 #pragma unroll 1
-    for (int p = 0; p < nb; ++p) {
-      const double l = x[0] * rinv[p];
-      row[static_cast<size_t>(p) * f] = l;
-      bad |= !isfinite(l);
-      const double2* up = reinterpret_cast<const double2*>(us + p * kWidePanel);
-#pragma unroll
-      for (int j = 0; j < kWidePanel; j += 2) {
-        const double2 v = up[j >> 1];
-        x[j] = x[j + 1] - l * v.x;
-        x[j + 1] = (j + 2 < kWidePanel ? x[j + 2] : 0.0) - l * v.y;
+  for (int p = pb; p < pe; ++p) {
+    if (prog)
+      while (ld_acquire_smem(prog) <= p) {
       }
+    const double l = x[0] * rinv[p];
+    row[p * ld] = l;
+    bad |= !isfinite(l);
+    const double2* up = reinterpret_cast<const double2*>(us + p * kWidePanel);
+#pragma unroll
+    for (int j = 0; j < W; j += 2) {
+      const double2 v = up[j >> 1];
+      x[j] = x[j + 1] - l * v.x;
+      x[j + 1] = (j + 2 < W ? x[j + 2] : 0.0) - l * v.y;
     }
+  }
+}
+
+// rows [row_lo, row_hi) of panel columns [p0, p0+nb): L(r, :) from the
+// unscaled diagonal columns us (32x32) and 1/d.  nthr threads (named barrier
+// `bar`), this one number vt; rows are staged nthr at a time into TR (column
+// stride SLT >= nthr + 2).  With `prog`, pivot p is used as soon as
+// *prog > p (lockstep with diag_block in the same CTA).
+template <int NTHR>
+__device__ __noinline__ void trsm_rows(double* F, size_t ld, int p0, int nb, int row_lo,
+                                       int row_hi, const double* us, const double* rinv,
+                                       int* stats, int vt, double* TR, const int* prog, int bar) {
+  constexpr int nthr = NTHR, SLT = NTHR + 2;
+  bool bad = false;
+  for (int base = row_lo; base < row_hi; base += nthr) {
+    const int nr = min(nthr, row_hi - base);
+    const int sh = stage_block<(NTHR + 2) / 2>(TR, SLT, F, ld, base, p0, nb, vt, nthr);
+    cp_wait_all();
+    named_bar(bar, nthr);
+    if (vt < nr) {
+      double x[kWidePanel];
+#pragma unroll
+      for (int q = 0; q < kWidePanel; ++q) x[q] = q < nb ? TR[q * SLT + vt + sh] : 0.0;
+      double* row = F + base + vt + p0 * ld;
+      trsm_steps<32>(0, min(nb, 8), x, row, ld, us, rinv, prog, bad);
+      trsm_steps<24>(8, min(nb, 16), x, row, ld, us, rinv, prog, bad);
+      trsm_steps<16>(16, min(nb, 24), x, row, ld, us, rinv, prog, bad);
+      trsm_steps<8>(24, nb, x, row, ld, us, rinv, prog, bad);
+    }
+    named_bar(bar, nthr);  // TR is reused by the next round
   }
   if (bad) atomicOr(stats + 3, 1);
 }
@@ -189,57 +356,75 @@ __device__ __forceinline__ void dmma_m8n8k4(double& c0, double& c1, double a, do
                : "d"(a), "d"(b));
 }
 
-// One warp: F[r][c] -= sum_{q in [p0,p1)} L[r][q] d_q L[c][q] on the 32x32
-// tile at (r0, q0).  A fragments (row g, k tq) and B fragments (k tq, col g)
-// of mma.m8n8k4.f64 are read directly from the column-major front.
-__device__ __noinline__ void warp_update_tile(const double* __restrict__ dv, int f, double* F,
-                                              int r0, int q0, int p0, int nb) {
-  const int lane = threadIdx.x & 31, g = lane >> 2, tq = lane & 3;
-  double acc[4][4][2];
+// DMMA core shared by the tile routines: rows gw*8..+8 of a 32x32 tile from
+// staged A (shift shA), B (shB), scaled by d, minus into C (shC) -> F.
+__device__ __forceinline__ void tile_mma_store(double* F, size_t ld, const double* A, int shA,
+                                               const double* Bs, int shB, const double* Cs, int shC,
+                                               const double* d, int nb, int r0, int nr, int q0,
+                                               int nc, int gt) {
+  const int lane = gt & 31, gw = gt >> 5, g = lane >> 2, tq = lane & 3;
+  const int rr = gw * 8 + g;
+  double acc[4][2];
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int j = 0; j < 4; ++j) acc[j][0] = acc[j][1] = 0.0;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-#pragma unroll 2
-  for (int kk = 0; kk < kWidePanel; kk += 4) {
-    if (kk >= nb) break;
-    const int q = kk + tq;
+  for (int kk = 0; kk < kWidePanel / 4; ++kk) {
+    const int q = kk * 4 + tq;
     const bool qv = q < nb;
-    const double* col = F + static_cast<size_t>(p0 + q) * f;
-    const double dq = qv ? __ldcg(dv + q) : 0.0;
-    double a[4], b[4];
+    const double a = (qv && rr < nr) ? A[q * kSL + rr + shA] : 0.0;
+    const double dq = qv ? d[q] : 0.0;
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int r = r0 + i * 8 + g;
-      a[i] = (qv && r < f) ? __ldcg(col + r) : 0.0;
-      const int c = q0 + i * 8 + g;
-      b[i] = (qv && c < f) ? __ldcg(col + c) * dq : 0.0;
+    for (int j = 0; j < 4; ++j) {
+      const int cc = j * 8 + g;
+      const double b = (qv && cc < nc) ? Bs[q * kSL + cc + shB] * dq : 0.0;
+      dmma_m8n8k4(acc[j][0], acc[j][1], a, b);
     }
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) dmma_m8n8k4(acc[i][j][0], acc[i][j][1], a[i], b[j]);
   }
-  // all 32 loads in flight before the first store
-  double cur[4][4][2];
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int j = 0; j < 4; ++j)
 #pragma unroll
-    for (int j = 0; j < 4; ++j)
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int r = r0 + i * 8 + g, c = q0 + j * 8 + tq * 2 + e;
-        cur[i][j][e] = (r < f && c < f && r >= c) ? __ldcg(F + r + static_cast<size_t>(c) * f) : 0.0;
-      }
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int j = 0; j < 4; ++j)
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int r = r0 + i * 8 + g, c = q0 + j * 8 + tq * 2 + e;
-        if (r < f && c < f && r >= c) F[r + static_cast<size_t>(c) * f] = cur[i][j][e] - acc[i][j][e];
-      }
+    for (int e = 0; e < 2; ++e) {
+      const int c = j * 8 + tq * 2 + e;
+      if (rr < nr && c < nc && r0 + rr >= q0 + c)
+        F[(r0 + rr) + (q0 + c) * ld] = Cs[c * kSL + rr + shC] - acc[j][e];
+    }
+}
+
+// 4 warps (128 threads, named barrier `bar`; gt = thread in group): the
+// trailing-update tile F[r0:r0+32, q0:q0+32] -= L21_r D L21_q^T for panel
+// columns [p0, p0+nb) (lower part only).  Warp gw computes rows gw*8..+8.
+__device__ __noinline__ void group_tile(double* F, size_t ld, int f, const double* __restrict__ dv,
+                                        int p0, int nb, int r0, int q0, GroupSmem& G, int gt,
+                                        int bar) {
+  const int nr = min(kUpdTile, f - r0), nc = min(kUpdTile, f - q0);
+  const bool dg = r0 == q0;
+  const int shA = stage_block<kNR2>(G.A, kSL, F, ld, r0, p0, nb, gt, 128);
+  const int shB = dg ? shA : stage_block<kNR2>(G.B, kSL, F, ld, q0, p0, nb, gt, 128);
+  const int shC = stage_block<kNR2>(G.C, kSL, F, ld, r0, q0, nc, gt, 128);
+  if (gt < nb) G.d[gt] = __ldcg(dv + gt);
+  cp_wait_all();
+  named_bar(bar, 128);
+  tile_mma_store(F, ld, G.A, shA, dg ? G.A : G.B, shB, G.C, shC, G.d, nb, r0, nr, q0, nc, gt);
+  named_bar(bar, 128);  // G is reused by the group's next tile
+}
+
+// the trailing update of panel [p0, p0+nb) on the grid from p1 (T blocks),
+// tiles (i, j) with 1 <= j <= i: this CTA takes tiles rank, rank + C, ...
+// from its queue, groups 1..3 pull (the group buffers overlay RowSmem)
+__device__ __forceinline__ void rest_update(double* F, size_t ld, int f, const double* dv, int p0,
+                                            int nb, int p1, int T, int rank, int C, StageSmem& st,
+                                            PanelSmem& sm, int grp, int gt) {
+  const int ntiles = T * (T - 1) / 2;
+  GroupSmem& G = *reinterpret_cast<GroupSmem*>(&st.r[grp - 1]);
+  for (;;) {
+    if (gt == 0) sm.gq[grp] = atomicAdd(&sm.qctr, 1);
+    named_bar(1 + grp, 128);
+    const int t = rank + sm.gq[grp] * C;
+    if (t >= ntiles) break;
+    int i, j;
+    tri_decode(t, i, j);
+    group_tile(F, ld, f, dv, p0, nb, p1 + (i + 1) * kUpdTile, p1 + (j + 1) * kUpdTile, G, gt, 1 + grp);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -250,25 +435,40 @@ __global__ void __launch_bounds__(kThreads, 1)
 k_wide_front(SnDev sd, FactorDev fd, const double* __restrict__ kval,
              const int* __restrict__ nodes, double eps, int acc_f, unsigned long long* trace) {
   __shared__ PanelSmem sm;
-  extern __shared__ double acc_smem[];
+  extern __shared__ __align__(16) double dyn_smem[];
+  StageSmem& st = *reinterpret_cast<StageSmem*>(dyn_smem);
   cg::cluster_group cl = cg::this_cluster();
   const int C = static_cast<int>(cl.num_blocks());
   const int rank = static_cast<int>(cl.block_rank());
   const int fi = blockIdx.x / C;
   const int s = nodes[fi];
   const int c0 = sd.first[s], k = sd.first[s + 1] - c0, f = sd.f[s];
+  const size_t ld = wide_ld(f);
   double* F = fd.lval + sd.l_off[s];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int grp = warp >> 2, gt = threadIdx.x & 127;
   const bool tr = trace && rank == 0 && threadIdx.x == 0;
   int ti = 0;
+  if (threadIdx.x == 0) {
+    sm.prog = 0;
+    sm.qctr = 0;
+  }
   if (tr) trace[fi * 128 + ti++] = globaltimer();
   {
-    double* acc = acc_smem + static_cast<size_t>(warp) * acc_f;
+    double* acc = dyn_smem + static_cast<size_t>(warp) * acc_f;
     for (int J = rank * kWarps + warp; J < f; J += C * kWarps)
-      assemble_col(sd, fd, kval, s, c0, k, f, F, J, acc);
+      assemble_col(sd, fd, kval, s, c0, k, f, F, ld, J, acc);
   }
   cl.sync();
   if (tr) trace[fi * 128 + ti++] = globaltimer();
+  // Panel loop with one panel of lookahead.  The trailing update of panel p
+  // is split: its first column block (the next panel's columns) is applied
+  // right away (phase B, all four groups); the rest is deferred into phase A
+  // of panel p+1, where groups 1..3 run it while warp 0 factors the next
+  // diagonal block and warps 1..3 solve the rows below it in lockstep.  Every
+  // trailing tile still receives its updates in panel order (the phases are
+  // separated by cluster barriers).
+  int pend_p0 = 0, pend_p1 = 0, pend_nb = 0, pend_T = 0;  // deferred update
   for (int p0 = 0; p0 < k; p0 += kWidePanel) {
     const int p1 = min(p0 + kWidePanel, k), nb = p1 - p0;
     const int rows = f - p1;
@@ -278,30 +478,54 @@ k_wide_front(SnDev sd, FactorDev fd, const double* __restrict__ kval,
     unsigned long long* dt = (tr && p0 == (k > kWidePanel ? kWidePanel : 0)) ? trace + fi * 128 + 120
                                                                              : nullptr;
     if (dt) dt[0] = globaltimer();
-    // every CTA factors the diagonal block itself (no extra cluster barrier);
-    // rank 0 publishes D and the counts now, L11 after the barrier below
-    // (other CTAs may still be reading the unfactored block until then)
-    if (warp == 0)
-      diag_block(F, f, p0, nb, eps, sm, rank == 0 ? fd.d + c0 + p0 : nullptr,
-                 rank == 0 ? fd.stats : nullptr);
-    if (dt) dt[1] = globaltimer();
+    // phase A.  Every CTA factors the diagonal block itself (no extra
+    // cluster barrier); rank 0 publishes D and the counts now, L11 after the
+    // barrier (other CTAs may still be reading the unfactored block).
+    if (warp == 0) {
+      diag_block(F, ld, p0, nb, eps, sm, st.u.p.D, rank == 0 ? fd.d + c0 + p0 : nullptr,
+                 rank == 0 ? fd.stats : nullptr, &sm.prog);
+      if (dt) dt[1] = globaltimer();
+    } else if (grp == 0) {
+      trsm_rows<kTrsRows>(F, ld, p0, nb, lo, max(lo, hi), &sm.Us[0][0], sm.rinv, fd.stats,
+                          threadIdx.x - 32, st.u.p.TR, &sm.prog, 1 + kGroups);
+    } else if (pend_T > 1) {
+      // deferred tiles (i, j), j >= 1, of the previous panel
+      rest_update(F, ld, f, fd.d + c0 + pend_p0, pend_p0, pend_nb, pend_p1, pend_T, rank, C, st, sm,
+                  grp, gt);
+    }
     __syncthreads();
     if (dt) dt[2] = globaltimer();
-    trsm_rows(F, f, p0, nb, lo, max(lo, hi), &sm.Us[0][0], sm.rinv, fd.stats);
+    if (threadIdx.x == 0) {
+      sm.prog = 0;
+      sm.qctr = 0;
+    }
     if (dt) dt[3] = globaltimer();
     cl.sync();
     if (dt) dt[4] = globaltimer();
     if (tr && ti < 119) trace[fi * 128 + ti++] = globaltimer();
-    if (rank == 0 && warp == 0)
-      for (int p = 0; p < nb; ++p)
-        if (lane > p && lane < nb) F[(p0 + lane) + static_cast<size_t>(p0 + p) * f] = sm.Lsh[lane][p];
+    if (rank == 0)  // L11 (scaled) from shared memory, one column per warp
+      for (int p = warp; p < nb; p += kWarps)
+        if (lane > p && lane < nb) F[(p0 + lane) + (p0 + p) * ld] = sm.Lsh[lane][p];
     if (dt) dt[5] = globaltimer();
+    // phase B: the next panel's column block now, the rest deferred; after
+    // the last panel, the whole trailing update
     const int T = (rows + kUpdTile - 1) / kUpdTile;
-    for (int t = rank * kWarps + warp; t < T * (T + 1) / 2; t += C * kWarps) {
-      int i, j;
-      tri_decode(t, i, j);
-      warp_update_tile(fd.d + c0 + p0, f, F, p1 + i * kUpdTile, p1 + j * kUpdTile, p0, nb);
+    const bool last = p1 >= k;
+    {
+      GroupSmem& G = grp == 0 ? st.u.g0 : *reinterpret_cast<GroupSmem*>(&st.r[grp - 1]);
+      for (int t = rank * kGroups + grp; t < T; t += C * kGroups)
+        group_tile(F, ld, f, fd.d + c0 + p0, p0, nb, p1 + t * kUpdTile, p1, G, gt, 1 + grp);
     }
+    if (last && T > 1) {  // no next panel: the rest of the update now
+      if (threadIdx.x == 0) sm.qctr = 0;
+      __syncthreads();
+      if (grp > 0)
+        rest_update(F, ld, f, fd.d + c0 + p0, p0, nb, p1, T, rank, C, st, sm, grp, gt);
+    }
+    pend_p0 = p0;
+    pend_p1 = p1;
+    pend_nb = nb;
+    pend_T = last ? 0 : T;
     if (dt) dt[6] = globaltimer();
     cl.sync();
     if (dt) dt[7] = globaltimer();
@@ -311,13 +535,14 @@ k_wide_front(SnDev sd, FactorDev fd, const double* __restrict__ kval,
 
 // ---------------------------------------------------------------------------
 // multi-kernel path for levels with huge fronts
-__global__ void __launch_bounds__(kHugeThreads)
+__global__ void __launch_bounds__(256)
 k_wide_assemble(SnDev sd, FactorDev fd, const double* __restrict__ kval,
                 const int4* __restrict__ tasks) {
   const int4 t = tasks[blockIdx.x];
   const int s = t.x, J = t.y + (threadIdx.x >> 5);
   const int c0 = sd.first[s], f = sd.f[s], k = sd.first[s + 1] - c0;
-  if (J < min(f, t.y + kAsmCols)) assemble_col(sd, fd, kval, s, c0, k, f, fd.lval + sd.l_off[s], J, nullptr);
+  if (J < min(f, t.y + kAsmCols))
+    assemble_col(sd, fd, kval, s, c0, k, f, fd.lval + sd.l_off[s], wide_ld(f), J, nullptr);
 }
 
 // one warp per front: diagonal block of panel `panel`, publishes L11, D and
@@ -325,22 +550,25 @@ k_wide_assemble(SnDev sd, FactorDev fd, const double* __restrict__ kval,
 __global__ void __launch_bounds__(32)
 k_wide_diag(SnDev sd, FactorDev fd, const int* __restrict__ fronts, int panel, double eps) {
   __shared__ PanelSmem sm;
+  __shared__ __align__(16) double D[kWidePanel * kSL];
   const int s = fronts[blockIdx.x];
   const int c0 = sd.first[s], k = sd.first[s + 1] - c0, f = sd.f[s];
+  const size_t ld = wide_ld(f);
   const int p0 = panel * kWidePanel, nb = min(p0 + kWidePanel, k) - p0;
   double* F = fd.lval + sd.l_off[s];
-  diag_block(F, f, p0, nb, eps, sm, fd.d + c0 + p0, fd.stats);
+  diag_block(F, ld, p0, nb, eps, sm, D, fd.d + c0 + p0, fd.stats, nullptr);
   const int lane = threadIdx.x;
   for (int p = 0; p < nb; ++p)
-    if (lane > p && lane < nb) F[(p0 + lane) + static_cast<size_t>(p0 + p) * f] = sm.Lsh[lane][p];
+    if (lane > p && lane < nb) F[(p0 + lane) + (p0 + p) * ld] = sm.Lsh[lane][p];
   double* scr = fd.dscr + static_cast<size_t>(blockIdx.x) * (kWidePanel * kWidePanel + kWidePanel);
   for (int i = lane; i < kWidePanel * kWidePanel; i += 32) scr[i] = (&sm.Us[0][0])[i];
   scr[kWidePanel * kWidePanel + lane] = sm.rinv[lane];
 }
 
-__global__ void __launch_bounds__(kHugeThreads)
+__global__ void __launch_bounds__(kHugeRows)
 k_wide_panel(SnDev sd, FactorDev fd, const int4* __restrict__ tasks, int panel) {
   __shared__ __align__(16) double us[kWidePanel * kWidePanel + kWidePanel];
+  __shared__ __align__(16) double TR[kWidePanel * kSLH];
   const int4 task = tasks[blockIdx.x];
   const int s = task.x, rb = task.y;
   const int c0 = sd.first[s], k = sd.first[s + 1] - c0, f = sd.f[s];
@@ -348,24 +576,26 @@ k_wide_panel(SnDev sd, FactorDev fd, const int4* __restrict__ tasks, int panel) 
   const double* scr = fd.dscr + static_cast<size_t>(task.z) * (kWidePanel * kWidePanel + kWidePanel);
   for (int i = threadIdx.x; i < kWidePanel * kWidePanel + kWidePanel; i += blockDim.x) us[i] = scr[i];
   __syncthreads();
-  const int lo = p1 + rb * kPanelRows, hi = min(f, lo + kPanelRows);
-  trsm_rows(fd.lval + sd.l_off[s], f, p0, p1 - p0, lo, max(lo, hi), us,
-            us + kWidePanel * kWidePanel, fd.stats);
+  const int lo = p1 + rb * kHugeRows, hi = min(f, lo + kHugeRows);
+  trsm_rows<kHugeRows>(fd.lval + sd.l_off[s], wide_ld(f), p0, p1 - p0, lo, max(lo, hi), us,
+                       us + kWidePanel * kWidePanel, fd.stats, threadIdx.x, TR, nullptr, 1);
 }
 
-// 8 warps per CTA, one 32x32 tile per warp
-__global__ void __launch_bounds__(kHugeThreads)
-k_wide_update(SnDev sd, FactorDev fd, const int4* __restrict__ tiles, int count) {
-  const int w = blockIdx.x * (kHugeThreads / 32) + (threadIdx.x >> 5);
-  if (w >= count) return;
-  const int4 t = tiles[w];
+// one 4-warp group (CTA) per 32x32 tile
+__global__ void __launch_bounds__(128)
+k_wide_update(SnDev sd, FactorDev fd, const int4* __restrict__ tiles) {
+  __shared__ __align__(16) GroupSmem G;
+  const int4 t = tiles[blockIdx.x];
   const int s = t.x;
   const int c0 = sd.first[s], k = sd.first[s + 1] - c0, f = sd.f[s];
   const int p0 = t.w * kWidePanel, p1 = min(p0 + kWidePanel, k);
-  warp_update_tile(fd.d + c0 + p0, f, fd.lval + sd.l_off[s], t.y, t.z, p0, p1 - p0);
+  group_tile(fd.lval + sd.l_off[s], wide_ld(f), f, fd.d + c0 + p0, p0, p1 - p0, t.y, t.z, G,
+             threadIdx.x, 1);
 }
 
 // ---------------------------------------------------------------------------
+const char* wide_last_error = "";
+
 static void wide_init() {
   static bool done = false;
   if (done) return;
@@ -373,13 +603,17 @@ static void wide_init() {
   int dev = 0, optin = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  cudaFuncAttributes fa = {};
+  cudaFuncGetAttributes(&fa, k_wide_front);
   cudaFuncSetAttribute(k_wide_front, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       optin - static_cast<int>(sizeof(PanelSmem)));
+                       optin - static_cast<int>(fa.sharedSizeBytes));
+  cudaGetLastError();
   done = true;
 }
 
 int wide_front_smem(int max_f) {
-  return static_cast<int>(sizeof(double)) * kWarps * (max_f > 0 ? max_f : 1);
+  const size_t acc = sizeof(double) * kWarps * static_cast<size_t>(max_f > 0 ? max_f : 1);
+  return static_cast<int>(acc > sizeof(StageSmem) ? acc : sizeof(StageSmem));
 }
 
 int launch_wide_front(const SnDev& sd, const FactorDev& fd, const double* kval, const int* nodes,
@@ -401,14 +635,15 @@ int launch_wide_front(const SnDev& sd, const FactorDev& fd, const double* kval, 
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     int nclusters = 0;
-    if (cudaOccupancyMaxActiveClusters(&nclusters, k_wide_front, &cfg) != cudaSuccess ||
-        nclusters < 1) {
+    cudaError_t e = cudaOccupancyMaxActiveClusters(&nclusters, k_wide_front, &cfg);
+    if (e != cudaSuccess || nclusters < 1) {
+      wide_last_error = e != cudaSuccess ? cudaGetErrorString(e) : "occupancy 0";
       cudaGetLastError();
       continue;
     }
-    if (cudaLaunchKernelEx(&cfg, k_wide_front, sd, fd, kval, nodes, eps, max_f, trace) ==
-        cudaSuccess)
-      return cluster;
+    e = cudaLaunchKernelEx(&cfg, k_wide_front, sd, fd, kval, nodes, eps, max_f, trace);
+    if (e == cudaSuccess) return cluster;
+    wide_last_error = cudaGetErrorString(e);
     cudaGetLastError();
   }
   return 0;
@@ -416,7 +651,7 @@ int launch_wide_front(const SnDev& sd, const FactorDev& fd, const double* kval, 
 
 void launch_wide_assemble(const SnDev& sd, const FactorDev& fd, const double* kval,
                           const int4* tasks, int count, cudaStream_t st) {
-  if (count) k_wide_assemble<<<count, kHugeThreads, 0, st>>>(sd, fd, kval, tasks);
+  if (count) k_wide_assemble<<<count, 256, 0, st>>>(sd, fd, kval, tasks);
 }
 
 void launch_wide_diag(const SnDev& sd, const FactorDev& fd, const int* fronts, int count,
@@ -426,14 +661,12 @@ void launch_wide_diag(const SnDev& sd, const FactorDev& fd, const int* fronts, i
 
 void launch_wide_panel(const SnDev& sd, const FactorDev& fd, const int4* tasks, int count,
                        int panel, cudaStream_t st) {
-  if (count) k_wide_panel<<<count, kHugeThreads, 0, st>>>(sd, fd, tasks, panel);
+  if (count) k_wide_panel<<<count, kHugeRows, 0, st>>>(sd, fd, tasks, panel);
 }
 
 void launch_wide_update(const SnDev& sd, const FactorDev& fd, const int4* tiles, int count,
                         cudaStream_t st) {
-  if (count)
-    k_wide_update<<<(count + kHugeThreads / 32 - 1) / (kHugeThreads / 32), kHugeThreads, 0, st>>>(
-        sd, fd, tiles, count);
+  if (count) k_wide_update<<<count, 128, 0, st>>>(sd, fd, tiles);
 }
 
 }  // namespace nclb

@@ -26,6 +26,7 @@
 #include "device.cuh"
 #include "launch.hpp"
 #include "symbolic.hpp"
+#include "layout.hpp"
 
 namespace cg = cooperative_groups;
 
@@ -50,6 +51,7 @@ k_fwd_front(SnDev sd, const double* __restrict__ lval, double* w, double* uvec,
   const int rank = static_cast<int>(cl.block_rank());
   const int s = nodes[blockIdx.x / C];
   const int c0 = sd.first[s], k = sd.first[s + 1] - c0, f = sd.f[s];
+  const size_t ld = wide_ld(f);
   const double* L = lval + sd.l_off[s];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   double* u = uvec + sd.rel_ptr[s];
@@ -70,7 +72,7 @@ k_fwd_front(SnDev sd, const double* __restrict__ lval, double* w, double* uvec,
         // lane owns row p0+lane of L11: L(p0+lane, p0+q), q < lane
 #pragma unroll
         for (int q = 0; q < kBlk; ++q)
-          lv[q] = (q < lane && lane < nb) ? __ldcg(L + (p0 + lane) + static_cast<size_t>(p0 + q) * f) : 0.0;
+          lv[q] = (q < lane && lane < nb) ? __ldcg(L + (p0 + lane) + (p0 + q) * ld) : 0.0;
         double t = lane < nb ? T[p0 + lane] : 0.0;
 #pragma unroll
         for (int q = 0; q < kBlk; ++q) {
@@ -85,7 +87,7 @@ k_fwd_front(SnDev sd, const double* __restrict__ lval, double* w, double* uvec,
         r = p1 + tid - 32;
         if (r < k) {
 #pragma unroll
-          for (int q = 0; q < kBlk; ++q) lv[q] = q < nb ? __ldcg(L + r + static_cast<size_t>(p0 + q) * f) : 0.0;
+          for (int q = 0; q < kBlk; ++q) lv[q] = q < nb ? __ldcg(L + r + (p0 + q) * ld) : 0.0;
         }
       }
       __syncthreads();
@@ -93,7 +95,7 @@ k_fwd_front(SnDev sd, const double* __restrict__ lval, double* w, double* uvec,
         for (; r < k; r += kSolveThreads - 32) {
           if (r >= p1 + kSolveThreads - 32) {  // rows beyond the prefetched one
 #pragma unroll
-            for (int q = 0; q < kBlk; ++q) lv[q] = q < nb ? __ldcg(L + r + static_cast<size_t>(p0 + q) * f) : 0.0;
+            for (int q = 0; q < kBlk; ++q) lv[q] = q < nb ? __ldcg(L + r + (p0 + q) * ld) : 0.0;
           }
           double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
 #pragma unroll
@@ -130,12 +132,12 @@ k_fwd_front(SnDev sd, const double* __restrict__ lval, double* w, double* uvec,
     const double* Lr = L + r;
     int q = 0;
     for (; q + 4 <= k; q += 4) {
-      a0 += __ldcg(Lr + static_cast<size_t>(q) * f) * T[q];
-      a1 += __ldcg(Lr + static_cast<size_t>(q + 1) * f) * T[q + 1];
-      a2 += __ldcg(Lr + static_cast<size_t>(q + 2) * f) * T[q + 2];
-      a3 += __ldcg(Lr + static_cast<size_t>(q + 3) * f) * T[q + 3];
+      a0 += __ldcg(Lr + q * ld) * T[q];
+      a1 += __ldcg(Lr + (q + 1) * ld) * T[q + 1];
+      a2 += __ldcg(Lr + (q + 2) * ld) * T[q + 2];
+      a3 += __ldcg(Lr + (q + 3) * ld) * T[q + 3];
     }
-    for (; q < k; ++q) a0 += __ldcg(Lr + static_cast<size_t>(q) * f) * T[q];
+    for (; q < k; ++q) a0 += __ldcg(Lr + q * ld) * T[q];
     u[r - k] = __ldcg(u + (r - k)) - ((a0 + a1) + (a2 + a3));
   }
 }
@@ -149,6 +151,7 @@ k_bwd_front(SnDev sd, const double* __restrict__ lval, const double* __restrict_
   const int rank = static_cast<int>(cl.block_rank());
   const int s = nodes[blockIdx.x / C];
   const int c0 = sd.first[s], k = sd.first[s + 1] - c0, f = sd.f[s];
+  const size_t ld = wide_ld(f);
   const double* L = lval + sd.l_off[s];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int* rows = sd.rows + sd.rows_ptr[s];
@@ -156,7 +159,7 @@ k_bwd_front(SnDev sd, const double* __restrict__ lval, const double* __restrict_
   __syncthreads();
   // z_p = w_p / d_p - sum_{r >= k} L(r, p) x_r, warp per pivot column
   for (int p = rank * kSolveWarps + warp; p < k; p += C * kSolveWarps) {
-    const double* Lp = L + static_cast<size_t>(p) * f;
+    const double* Lp = L + p * ld;
     double part = 0.0;
     for (int r = k + lane; r < f; r += 32) part += __ldcg(Lp + r) * X[r];
     part = wsum(part);
@@ -174,11 +177,11 @@ k_bwd_front(SnDev sd, const double* __restrict__ lval, const double* __restrict_
       // lane owns column p0+lane of L11: L(p0+j, p0+lane), j > lane
 #pragma unroll
       for (int j = 0; j < kBlk; ++j)
-        lc[j] = (j > lane && j < nb) ? __ldcg(L + (p0 + j) + static_cast<size_t>(p0 + lane) * f) : 0.0;
+        lc[j] = (j > lane && j < nb) ? __ldcg(L + (p0 + j) + (p0 + lane) * ld) : 0.0;
     } else {
       // later pivots of this front: x_p -= sum_{r in [p1, k)} L(r, p) x_r
       for (int p = p0 + warp - 1; p < p1; p += kSolveWarps - 1) {
-        const double* Lp = L + static_cast<size_t>(p) * f;
+        const double* Lp = L + p * ld;
         double part = 0.0;
         for (int r = p1 + lane; r < k; r += 32) part += __ldcg(Lp + r) * X[r];
         part = wsum(part);
