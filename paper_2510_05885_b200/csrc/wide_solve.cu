@@ -35,17 +35,53 @@ namespace nclb {
 constexpr int kSolveThreads = 512;
 constexpr int kSolveWarps = kSolveThreads / 32;
 constexpr int kBlk = 32;
+constexpr int kRows = 240;        // rows per staged panel chunk
+constexpr int kSLP = kRows + 2;   // its column stride in shared memory
+constexpr unsigned kFull = 0xffffffffu;
+
+// dynamic shared memory: the front vector (f doubles) after two panel buffers
+struct SolveSmem {
+  double P[2][kBlk * kSLP];
+  double Z[kBlk];
+};
 
 __device__ __forceinline__ double wsum(double v) {
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
   return v;
+}
+
+__device__ __forceinline__ void cp16(void* dst, const void* src) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// rows [r0, r0+nr) x columns [c0, c0+nc) of L (ld even) -> S, element
+// (r0+i, c0+j) at S[j*kSLP + i + sh], sh = r0 & 1; warp per column, lanes
+// along it in 16-byte chunks (cp.async: many copies in flight per warp --
+// register loads from L2 stall on too few outstanding requests).
+__device__ __forceinline__ int stage_cols(double* S, const double* L, size_t ld, int r0, int nr,
+                                          int c0, int nc, int warp, int lane) {
+  const int a = r0 & ~1, sh = r0 - a, n2 = (nr + sh + 1) >> 1;
+  for (int j = warp; j < nc; j += kSolveWarps) {
+    const double* src = L + a + (c0 + j) * ld;
+    double* dst = S + j * kSLP;
+    for (int ch = lane; ch < n2; ch += 32) cp16(dst + 2 * ch, src + 2 * ch);
+  }
+  return r0 - a;
 }
 
 __global__ void __launch_bounds__(kSolveThreads, 1)
 k_fwd_front(SnDev sd, const double* __restrict__ lval, double* w, double* uvec,
             const int* __restrict__ nodes) {
-  extern __shared__ double T[];
+  extern __shared__ __align__(16) double dyn[];
+  SolveSmem& sm = *reinterpret_cast<SolveSmem*>(dyn);
+  double* T = dyn + sizeof(SolveSmem) / sizeof(double);
   cg::cluster_group cl = cg::this_cluster();
   const int C = static_cast<int>(cl.num_blocks());
   const int rank = static_cast<int>(cl.block_rank());
@@ -55,7 +91,16 @@ k_fwd_front(SnDev sd, const double* __restrict__ lval, double* w, double* uvec,
   const double* L = lval + sd.l_off[s];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   double* u = uvec + sd.rel_ptr[s];
-  if (rank == 0) {
+  if (rank == 0 && k > 0) {
+    // stages: block b (columns [32b, 32b+nb)), rows [32b, k) in chunks of kRows
+    int sb = 0, sr = 0, buf = 0;
+    int shv[2];
+    auto issue = [&](int b, int r0, int bf) {
+      const int p0 = b * kBlk, nb = min(kBlk, k - p0);
+      shv[bf] = stage_cols(sm.P[bf], L, ld, r0, min(kRows, k - r0), p0, nb, warp, lane);
+      cp_commit();
+    };
+    issue(0, 0, 0);
     for (int r = tid; r < f; r += kSolveThreads) T[r] = r < k ? __ldcg(w + c0 + r) : 0.0;
     __syncthreads();
     for (int cc = sd.ch_ptr[s]; cc < sd.ch_ptr[s + 1]; ++cc) {
@@ -64,51 +109,59 @@ k_fwd_front(SnDev sd, const double* __restrict__ lval, double* w, double* uvec,
       for (int i = tid; i < fu; i += kSolveThreads) T[sd.rel[rp + i]] += __ldcg(uvec + rp + i);
       __syncthreads();
     }
-    for (int p0 = 0; p0 < k; p0 += kBlk) {
-      const int p1 = min(p0 + kBlk, k), nb = p1 - p0;
-      double lv[kBlk];
-      int r = -1;
-      if (warp == 0) {
-        // lane owns row p0+lane of L11: L(p0+lane, p0+q), q < lane
-#pragma unroll
-        for (int q = 0; q < kBlk; ++q)
-          lv[q] = (q < lane && lane < nb) ? __ldcg(L + (p0 + lane) + (p0 + q) * ld) : 0.0;
-        double t = lane < nb ? T[p0 + lane] : 0.0;
-#pragma unroll
-        for (int q = 0; q < kBlk; ++q) {
-          if (q < nb) {
-            const double wq = __shfl_sync(0xffffffffu, t, q);
-            if (lane > q) t -= lv[q] * wq;
-          }
-        }
-        if (lane < nb) T[p0 + lane] = t;
+    for (;;) {
+      const int p0 = sb * kBlk, p1 = min(p0 + kBlk, k), nb = p1 - p0;
+      const int nr = min(kRows, k - sr);
+      // next stage into the other buffer
+      int nbk = sb, nr0 = sr + kRows;
+      if (nr0 >= k) {
+        ++nbk;
+        nr0 = nbk * kBlk;
+      }
+      const bool more = nbk * kBlk < k;
+      if (more) {
+        issue(nbk, nr0, buf ^ 1);
+        cp_wait<1>();
       } else {
-        // prefetch this thread's row below the block while the chain runs
-        r = p1 + tid - 32;
-        if (r < k) {
-#pragma unroll
-          for (int q = 0; q < kBlk; ++q) lv[q] = q < nb ? __ldcg(L + r + (p0 + q) * ld) : 0.0;
-        }
+        cp_wait<0>();
       }
       __syncthreads();
-      if (warp != 0) {
-        for (; r < k; r += kSolveThreads - 32) {
-          if (r >= p1 + kSolveThreads - 32) {  // rows beyond the prefetched one
+      const double* P = sm.P[buf];
+      const int sh = shv[buf];
+      if (sr == p0) {  // chunk holding L11: the substitution chain first
+        if (warp == 0) {
+          double lv[kBlk];
 #pragma unroll
-            for (int q = 0; q < kBlk; ++q) lv[q] = q < nb ? __ldcg(L + r + (p0 + q) * ld) : 0.0;
-          }
-          double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+          for (int q = 0; q < kBlk; ++q) lv[q] = (q < lane && lane < nb) ? P[q * kSLP + lane + sh] : 0.0;
+          double t = lane < nb ? T[p0 + lane] : 0.0;
 #pragma unroll
-          for (int q = 0; q < kBlk; q += 4) {
-            a0 += lv[q] * T[p0 + q];
-            a1 += lv[q + 1] * T[p0 + q + 1];
-            a2 += lv[q + 2] * T[p0 + q + 2];
-            a3 += lv[q + 3] * T[p0 + q + 3];
+          for (int q = 0; q < kBlk; ++q) {
+            if (q < nb) {
+              const double wq = __shfl_sync(kFull, t, q);
+              if (lane > q) t -= lv[q] * wq;
+            }
           }
-          T[r] -= (a0 + a1) + (a2 + a3);
+          if (lane < nb) T[p0 + lane] = t;
         }
+        __syncthreads();
+      }
+      // rows of this chunk below the block: T[r] -= L(r, block) w_block
+      for (int r = max(sr, p1) + tid; r < sr + nr; r += kSolveThreads) {
+        const int i = r - sr + sh;
+        double a0 = 0.0, a1 = 0.0;
+        int q = 0;
+        for (; q + 2 <= nb; q += 2) {
+          a0 += P[q * kSLP + i] * T[p0 + q];
+          a1 += P[(q + 1) * kSLP + i] * T[p0 + q + 1];
+        }
+        if (q < nb) a0 += P[q * kSLP + i] * T[p0 + q];
+        T[r] -= a0 + a1;
       }
       __syncthreads();
+      if (!more) break;
+      sb = nbk;
+      sr = nr0;
+      buf ^= 1;
     }
     for (int q = tid; q < f; q += kSolveThreads) {
       if (q < k)
@@ -118,34 +171,57 @@ k_fwd_front(SnDev sd, const double* __restrict__ lval, double* w, double* uvec,
     }
   }
   cl.sync();
-  // update vector rows [k, f): u_r -= sum_{q<k} L(r, q) w_q, rows split over the cluster
+  // update vector rows [k, f): u_r -= sum_{q<k} L(r, q) w_q, rows split over
+  // the cluster; column chunks of 32 streamed through the two buffers
   const int rows = f - k;
-  if (rows == 0) return;
+  if (rows == 0 || k == 0) return;
   if (rank != 0) {
     for (int q = tid; q < k; q += kSolveThreads) T[q] = __ldcg(w + c0 + q);
-    __syncthreads();
   }
   const int chunk = (rows + C - 1) / C;
   const int lo = k + rank * chunk, hi = min(f, lo + chunk);
-  for (int r = lo + tid; r < hi; r += kSolveThreads) {
-    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-    const double* Lr = L + r;
-    int q = 0;
-    for (; q + 4 <= k; q += 4) {
-      a0 += __ldcg(Lr + q * ld) * T[q];
-      a1 += __ldcg(Lr + (q + 1) * ld) * T[q + 1];
-      a2 += __ldcg(Lr + (q + 2) * ld) * T[q + 2];
-      a3 += __ldcg(Lr + (q + 3) * ld) * T[q + 3];
+  const int ncc = (k + kBlk - 1) / kBlk;
+  for (int base = lo; base < hi; base += kRows) {
+    const int nr = min(kRows, hi - base);
+    int shv[2];
+    shv[0] = stage_cols(sm.P[0], L, ld, base, nr, 0, min(kBlk, k), warp, lane);
+    cp_commit();
+    double acc = 0.0;
+    for (int cb = 0; cb < ncc; ++cb) {
+      const int bf = cb & 1;
+      if (cb + 1 < ncc) {
+        shv[bf ^ 1] = stage_cols(sm.P[bf ^ 1], L, ld, base, nr, (cb + 1) * kBlk,
+                                 min(kBlk, k - (cb + 1) * kBlk), warp, lane);
+        cp_commit();
+        cp_wait<1>();
+      } else {
+        cp_wait<0>();
+      }
+      __syncthreads();
+      if (tid < nr) {
+        const double* P = sm.P[bf];
+        const int i = tid + shv[bf], q0 = cb * kBlk, nq = min(kBlk, k - q0);
+        double a1 = 0.0;
+        int q = 0;
+        for (; q + 2 <= nq; q += 2) {
+          acc += P[q * kSLP + i] * T[q0 + q];
+          a1 += P[(q + 1) * kSLP + i] * T[q0 + q + 1];
+        }
+        if (q < nq) acc += P[q * kSLP + i] * T[q0 + q];
+        acc += a1;
+      }
+      __syncthreads();
     }
-    for (; q < k; ++q) a0 += __ldcg(Lr + q * ld) * T[q];
-    u[r - k] = __ldcg(u + (r - k)) - ((a0 + a1) + (a2 + a3));
+    if (tid < nr) u[base + tid - k] = __ldcg(u + (base + tid - k)) - acc;
   }
 }
 
 __global__ void __launch_bounds__(kSolveThreads, 1)
 k_bwd_front(SnDev sd, const double* __restrict__ lval, const double* __restrict__ d,
             const double* __restrict__ w, double* x, const int* __restrict__ nodes) {
-  extern __shared__ double X[];
+  extern __shared__ __align__(16) double dyn[];
+  SolveSmem& sm = *reinterpret_cast<SolveSmem*>(dyn);
+  double* X = dyn + sizeof(SolveSmem) / sizeof(double);
   cg::cluster_group cl = cg::this_cluster();
   const int C = static_cast<int>(cl.num_blocks());
   const int rank = static_cast<int>(cl.block_rank());
@@ -155,52 +231,118 @@ k_bwd_front(SnDev sd, const double* __restrict__ lval, const double* __restrict_
   const double* L = lval + sd.l_off[s];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int* rows = sd.rows + sd.rows_ptr[s];
+  if (k == 0) return;
   for (int r = k + tid; r < f; r += kSolveThreads) X[r] = __ldcg(x + rows[r]);
   __syncthreads();
-  // z_p = w_p / d_p - sum_{r >= k} L(r, p) x_r, warp per pivot column
-  for (int p = rank * kSolveWarps + warp; p < k; p += C * kSolveWarps) {
-    const double* Lp = L + p * ld;
-    double part = 0.0;
-    for (int r = k + lane; r < f; r += 32) part += __ldcg(Lp + r) * X[r];
-    part = wsum(part);
-    if (lane == 0) x[c0 + p] = __ldcg(w + c0 + p) / __ldcg(d + c0 + p) - part;
+  // z_p = w_p / d_p - sum_{r >= k} L(r, p) x_r for this CTA's pivot columns,
+  // 32 columns x kRows rows per staged chunk, two columns per warp
+  {
+    const int pc = (k + C - 1) / C;
+    const int pa = rank * pc, pb = min(k, pa + pc);
+    for (int q0 = pa; q0 < pb; q0 += kBlk) {
+      const int nq = min(kBlk, pb - q0);
+      double part0 = 0.0, part1 = 0.0;
+      int shv[2];
+      const int nch = (f - k + kRows - 1) / kRows;
+      if (nch > 0) {
+        shv[0] = stage_cols(sm.P[0], L, ld, k, min(kRows, f - k), q0, nq, warp, lane);
+        cp_commit();
+      }
+      for (int ci = 0; ci < nch; ++ci) {
+        const int bf = ci & 1, r0 = k + ci * kRows, nr = min(kRows, f - r0);
+        if (ci + 1 < nch) {
+          shv[bf ^ 1] = stage_cols(sm.P[bf ^ 1], L, ld, r0 + kRows, min(kRows, f - r0 - kRows), q0,
+                                   nq, warp, lane);
+          cp_commit();
+          cp_wait<1>();
+        } else {
+          cp_wait<0>();
+        }
+        __syncthreads();
+        const double* P = sm.P[bf];
+        for (int i = lane; i < nr; i += 32) {
+          const double xv = X[r0 + i];
+          if (warp < nq) part0 += P[warp * kSLP + i + shv[bf]] * xv;
+          if (warp + kSolveWarps < nq) part1 += P[(warp + kSolveWarps) * kSLP + i + shv[bf]] * xv;
+        }
+        __syncthreads();
+      }
+      part0 = wsum(part0);
+      part1 = wsum(part1);
+      if (lane == 0) {
+        int p = q0 + warp;
+        if (warp < nq) x[c0 + p] = __ldcg(w + c0 + p) / __ldcg(d + c0 + p) - part0;
+        p += kSolveWarps;
+        if (warp + kSolveWarps < nq) x[c0 + p] = __ldcg(w + c0 + p) / __ldcg(d + c0 + p) - part1;
+      }
+    }
   }
   cl.sync();
   if (rank != 0) return;
   for (int p = tid; p < k; p += kSolveThreads) X[p] = __ldcg(x + c0 + p);
   __syncthreads();
+  // blocked L11^T solve from the last block up; block b's chunks (rows
+  // [32b, k) in kRows pieces) are visited last-first so the chunk holding
+  // L11 is still resident for the chain
   const int nblk = (k + kBlk - 1) / kBlk;
-  for (int b = nblk - 1; b >= 0; --b) {
+  auto nchunks = [&](int b) { return (k - b * kBlk + kRows - 1) / kRows; };
+  int b = nblk - 1, ci = nchunks(b) - 1, buf = 0;
+  int shv[2];
+  auto issue = [&](int bb, int cc, int bf) {
+    const int p0 = bb * kBlk, r0 = p0 + cc * kRows;
+    shv[bf] = stage_cols(sm.P[bf], L, ld, r0, min(kRows, k - r0), p0, min(kBlk, k - p0), warp, lane);
+    cp_commit();
+  };
+  issue(b, ci, 0);
+  if (tid < kBlk) sm.Z[tid] = 0.0;
+  for (;;) {
     const int p0 = b * kBlk, p1 = min(p0 + kBlk, k), nb = p1 - p0;
-    double lc[kBlk];
-    if (warp == 0) {
-      // lane owns column p0+lane of L11: L(p0+j, p0+lane), j > lane
-#pragma unroll
-      for (int j = 0; j < kBlk; ++j)
-        lc[j] = (j > lane && j < nb) ? __ldcg(L + (p0 + j) + (p0 + lane) * ld) : 0.0;
+    const int r0 = p0 + ci * kRows, nr = min(kRows, k - r0);
+    int nb2 = b, nc2 = ci - 1;
+    if (nc2 < 0) {
+      --nb2;
+      nc2 = nb2 >= 0 ? nchunks(nb2) - 1 : 0;
+    }
+    const bool more = nb2 >= 0;
+    if (more) {
+      issue(nb2, nc2, buf ^ 1);
+      cp_wait<1>();
     } else {
-      // later pivots of this front: x_p -= sum_{r in [p1, k)} L(r, p) x_r
-      for (int p = p0 + warp - 1; p < p1; p += kSolveWarps - 1) {
-        const double* Lp = L + p * ld;
-        double part = 0.0;
-        for (int r = p1 + lane; r < k; r += 32) part += __ldcg(Lp + r) * X[r];
-        part = wsum(part);
-        if (lane == 0) X[p] -= part;
-      }
+      cp_wait<0>();
     }
     __syncthreads();
-    if (warp == 0) {
-      double xv = lane < nb ? X[p0 + lane] : 0.0;
+    const double* P = sm.P[buf];
+    const int sh = shv[buf];
+    // later pivots of this front: z_p -= sum_{r in chunk, r >= p1} L(r, p) x_r
+    for (int j = warp; j < nb; j += kSolveWarps) {
+      double part = 0.0;
+      for (int r = max(r0, p1) + lane; r < r0 + nr; r += 32) part += P[j * kSLP + r - r0 + sh] * X[r];
+      part = wsum(part);
+      if (lane == 0) sm.Z[j] += part;
+    }
+    __syncthreads();
+    if (ci == 0) {  // all chunks of block b done; P holds L11
+      if (warp == 0) {
+        double lc[kBlk];  // lane owns column p0+lane of L11: L(p0+j, p0+lane), j > lane
 #pragma unroll
-      for (int p = kBlk - 1; p >= 0; --p) {
-        if (p < nb) {
-          const double xp = __shfl_sync(0xffffffffu, xv, p);
-          if (lane < p) xv -= lc[p] * xp;
+        for (int j = 0; j < kBlk; ++j) lc[j] = (j > lane && j < nb) ? P[lane * kSLP + j + sh] : 0.0;
+        double xv = lane < nb ? X[p0 + lane] - sm.Z[lane] : 0.0;
+#pragma unroll
+        for (int p = kBlk - 1; p >= 0; --p) {
+          if (p < nb) {
+            const double xp = __shfl_sync(kFull, xv, p);
+            if (lane < p) xv -= lc[p] * xp;
+          }
         }
+        if (lane < nb) X[p0 + lane] = xv;
+        sm.Z[lane] = 0.0;
       }
-      if (lane < nb) X[p0 + lane] = xv;
+      __syncthreads();
     }
-    __syncthreads();
+    if (!more) break;
+    b = nb2;
+    ci = nc2;
+    buf ^= 1;
   }
   for (int p = tid; p < k; p += kSolveThreads) x[c0 + p] = X[p];
 }
@@ -250,8 +392,8 @@ int launch_fwd_front(const SnDev& sd, const double* lval, double* w, double* uve
                      const int* nodes, int count, int cluster, int max_f, cudaStream_t st) {
   if (count == 0) return cluster;
   solve_init();
-  return launch_clustered(k_fwd_front, count, cluster, sizeof(double) * max_f, st, sd, lval, w,
-                          uvec, nodes);
+  return launch_clustered(k_fwd_front, count, cluster, sizeof(SolveSmem) + sizeof(double) * max_f,
+                          st, sd, lval, w, uvec, nodes);
 }
 
 int launch_bwd_front(const SnDev& sd, const double* lval, const double* d, const double* w,
@@ -259,8 +401,8 @@ int launch_bwd_front(const SnDev& sd, const double* lval, const double* d, const
                      cudaStream_t st) {
   if (count == 0) return cluster;
   solve_init();
-  return launch_clustered(k_bwd_front, count, cluster, sizeof(double) * max_f, st, sd, lval, d,
-                          w, x, nodes);
+  return launch_clustered(k_bwd_front, count, cluster, sizeof(SolveSmem) + sizeof(double) * max_f,
+                          st, sd, lval, d, w, x, nodes);
 }
 
 }  // namespace nclb
