@@ -215,6 +215,50 @@ void ncl_initial_outer_state(double mu0, double rho0, double rho_max,
                              double* state5);
 int ncl_outer_update(double* state5, double rnorm);
 
+
+/* ---- Schur mode: one rank's share of a block-arrowhead problem ----------
+ * (SCOPF with contingency blocks; no reference counterpart --
+ * the reference factors the whole KKT on one core).  The sub-problem's first
+ * n0 variables couple the blocks; they are ordered last and not eliminated:
+ * the factorization leaves the rank's Schur contribution
+ * S_g = A00_g - sum_k A0k Akk^-1 Ak0, which the caller sums over ranks
+ * (NCCL allreduce) and factors densely on every rank.  K1s form only.  All
+ * vectors are DEVICE pointers; every call returns after its work finished.
+ * stats4 = n_pos, n_neg, perturbed, fail. */
+typedef struct ncl_schur ncl_schur;
+int ncl_schur_create(int nt, const int* hp_ptr, const int* hp_idx, int m,
+                     const int* jp_ptr, const int* jp_idx, int ns, int m_eq,
+                     int n0, const ncl_kkt_opts* opt, ncl_schur** out);
+void ncl_schur_destroy(ncl_schur* h);
+int ncl_schur_info(const ncl_schur* h, ncl_kkt_info* info);
+int ncl_schur_n0(const ncl_schur* h);
+/* refill (kkt.cpp:149-186) + factorization of the blocks; S: n0 x n0
+ * column-major, lower part = S_g, upper zero */
+int ncl_schur_factor(ncl_schur* h, const double* hval, const double* jval,
+                     const double* sigma, double rho, double delta,
+                     int* stats4, double* S);
+/* dense static-pivot LDL^T of S (+ diag_shift on its diagonal) */
+int ncl_schur_factor_dense(ncl_schur* h, const double* S, double diag_shift,
+                           int* stats4);
+/* K1s right-hand side (kkt.cpp:188-222) of the sub-problem */
+int ncl_schur_rhs(ncl_schur* h, const double* jval, const double* sigma,
+                  const double* rbar1, const double* rbar2, const double* rbar3,
+                  double rho, double delta, double* b);
+/* forward solve through the blocks: b0 = this rank's reduced coupling rhs */
+int ncl_schur_forward(ncl_schur* h, const double* b, double* b0);
+/* x0 = S^-1 b0 with the dense factors */
+int ncl_schur_solve0(ncl_schur* h, const double* b0, double* x0);
+/* backward solve through the blocks given the coupling solution x0 */
+int ncl_schur_backward(ncl_schur* h, const double* x0, double* x);
+/* r = b - K_g x with the sub-problem's matrix of the last refill */
+int ncl_schur_residual(ncl_schur* h, const double* x, const double* b,
+                       double* r);
+/* recover (kkt.cpp:224-264) of the sub-problem's rows */
+int ncl_schur_recover(ncl_schur* h, const double* jval, const double* sol,
+                      const double* rbar2, double rho, double delta, double* dx,
+                      double* dr, double* dy);
+int ncl_schur_launch_count(const ncl_schur* h, long long* count);
+
 #ifdef __cplusplus
 }
 #endif

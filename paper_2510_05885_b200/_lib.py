@@ -94,6 +94,19 @@ SIGS = {
     "ncl_nlp_clip_duals": ([_p, _p, _d, _p, _p], _i),
     "ncl_nlp_outer": ([_p, _p, _p, _d, _i, _dp], _i),
     "ncl_initial_outer_state": ([_d, _d, _d, _dp], None),
+    "ncl_schur_create": ([_i, _ip, _ip, _i, _ip, _ip, _i, _i, _i, C.POINTER(KktOpts), C.POINTER(_p)], _i),
+    "ncl_schur_destroy": ([_p], None),
+    "ncl_schur_info": ([_p, C.POINTER(KktInfo)], _i),
+    "ncl_schur_n0": ([_p], _i),
+    "ncl_schur_factor": ([_p, _p, _p, _p, _d, _d, _ip, _p], _i),
+    "ncl_schur_factor_dense": ([_p, _p, _d, _ip], _i),
+    "ncl_schur_rhs": ([_p, _p, _p, _p, _p, _p, _d, _d, _p], _i),
+    "ncl_schur_forward": ([_p, _p, _p], _i),
+    "ncl_schur_solve0": ([_p, _p, _p], _i),
+    "ncl_schur_backward": ([_p, _p, _p], _i),
+    "ncl_schur_residual": ([_p, _p, _p, _p], _i),
+    "ncl_schur_recover": ([_p, _p, _p, _p, _d, _d, _p, _p, _p], _i),
+    "ncl_schur_launch_count": ([_p, C.POINTER(_ll)], _i),
     "ncl_outer_update": ([_dp, _d], _i),
 }
 

@@ -58,9 +58,9 @@ struct FactorInfo {
 // ---------------------------------------------------------------------------
 class LdlSystem {
  public:
-  LdlSystem(const LowerCsc& K, const Symbolic& S, cudaStream_t st)
+  LdlSystem(const LowerCsc& K, const Symbolic& S, cudaStream_t st, int schur_n0 = 0)
       : K_(K), S_(S), st_(st) {
-    sn_ = build_supernodal(K_, S_);
+    sn_ = build_supernodal(K_, S_, schur_n0);
     N_ = K_.n;
     upload();
   }
@@ -152,6 +152,51 @@ class LdlSystem {
     fi.ok = hs_->stats[3] == 0;
     return fi;
   }
+
+  // Schur mode: the forward half (b -> permuted w, coupling rows assembled
+  // at the tail of wp) and the backward half (coupling solution at the tail
+  // of xp -> x); solve_async = both
+  void solve_fwd_async(const double* b) {
+    launch_permute_in(N_, perm_.p, b, wp_.p, st_);
+    if (npaths()) {
+      CK(cudaMemsetAsync(counter_.p, 0, sizeof(int), st_));
+      ++epoch_;
+      launch_fwd_warp(sd_, lval_.p, wp_.p, uvec_.p, flags_.p, epoch_, counter_.p, npaths(),
+                      grid_, st_);
+    }
+    for (int l = 0; l < nlevels(); ++l) {
+      const int used = launch_fwd_front(sd_, lval_.p, wp_.p, uvec_.p, lvl_nodes_.p + sn_.lvl_ptr[l],
+                                        sn_.lvl_ptr[l + 1] - sn_.lvl_ptr[l], solve_cluster_[l],
+                                        lvl_fmax_[l], st_);
+      if (used == 0) throw CudaError("k_fwd_front: no cluster configuration fits");
+      solve_cluster_[l] = used;
+    }
+    launches_ += 1 + (npaths() > 0 ? 1 : 0) + nlevels();
+    CK(cudaGetLastError());
+  }
+  void solve_bwd_async(double* x) {
+    for (int l = nlevels() - 1; l >= 0; --l) {
+      const int used = launch_bwd_front(sd_, lval_.p, d_.p, wp_.p, xp_.p,
+                                        lvl_nodes_.p + sn_.lvl_ptr[l],
+                                        sn_.lvl_ptr[l + 1] - sn_.lvl_ptr[l], solve_cluster_[l],
+                                        lvl_fmax_[l], st_);
+      if (used == 0) throw CudaError("k_bwd_front: no cluster configuration fits");
+      solve_cluster_[l] = used;
+    }
+    if (npaths()) {
+      CK(cudaMemsetAsync(counter_.p, 0, sizeof(int), st_));
+      ++epoch_;
+      launch_bwd_warp(sd_, lval_.p, d_.p, wp_.p, xp_.p, flags_.p, epoch_, wide_.p,
+                      counter_.p, npaths(), grid_, st_);
+    }
+    launch_permute_out(N_, perm_.p, xp_.p, x, st_);
+    launches_ += 1 + (npaths() > 0 ? 1 : 0) + nlevels();
+    CK(cudaGetLastError());
+  }
+  int schur_n0() const { return sn_.schur >= 0 ? N_ - sn_.first[sn_.schur] : 0; }
+  const double* schur_front() const { return lval_.p + sn_.l_off[sn_.schur]; }
+  double* w_tail() { return wp_.p + (N_ - schur_n0()); }
+  double* x_tail() { return xp_.p + (N_ - schur_n0()); }
 
   // x = P^T L^-T D^-1 L^-1 P b (device vectors, async)
   void solve_async(const double* b, double* x) {
@@ -441,6 +486,7 @@ class LdlSystem {
     sd_.path_ptr = path_ptr_.p;
     sd_.path_nodes = path_nodes_.p;
     sd_.wide = wide_.p;
+    sd_.schur = T.schur;
     grid_ = warp_tier_grid();
     CK(cudaStreamSynchronize(st_));
   }
@@ -479,7 +525,8 @@ class KktSystem {
   KktSystem(KktPlan plan, const ncl_kkt_opts& opt)
       : P_(std::move(plan)), opt_(opt) {
     CK(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
-    ldl_ = std::make_unique<LdlSystem>(P_.K, P_.sym, st_);
+    ldl_ = std::make_unique<LdlSystem>(
+        P_.K, P_.sym, st_, P_.sn.schur >= 0 ? P_.N - P_.sn.first[P_.sn.schur] : 0);
     c_ptr_.upload(P_.c_ptr);
     c_code_.upload(P_.c_code);
     pair_row_.upload(P_.pair_row);
@@ -649,6 +696,21 @@ class KktSystem {
     CK(cudaStreamSynchronize(st_));
   }
 
+  // pieces of solve_device for the distributed (Schur-mode) driver
+  double* kval() { return kval_.p; }
+  void rhs_async(const double* jv, const double* sg, const double* r1, const double* r2,
+                 const double* r3, double rho, double delta, double* out) {
+    launch_rhs(P_, jt_ptr_.p, jt_row_.p, jt_slot_.p, jv, sg, r1, r2, r3, rho, delta, v_.p, wk_.p,
+               rs_.p, pk_.p, out, st_);
+    launches_ += P_.form == kK1s ? 2 : 1;
+  }
+  void recover_async(const double* jv, const double* sol, const double* r2, double rho,
+                     double delta, double* dx, double* dr, double* dy) {
+    launch_recover(P_, jp_ptr_.p, jp_idx_.p, jv, sol, v_.p, rs_.p, pk_.p, r2, rho, delta, dx, dr,
+                   dy, st_);
+    launches_ += 1;
+  }
+
   void matrix(int* cp, int* ri, double* val) const {
     if (cp) std::copy(P_.K.col_ptr.begin(), P_.K.col_ptr.end(), cp);
     if (ri) std::copy(P_.K.row_ind.begin(), P_.K.row_ind.end(), ri);
@@ -708,6 +770,120 @@ class KktSystem {
   double ms_[6] = {0, 0, 0, 0, 0, 0};
   long long launches_ = 0;
 };
+
+// ---------------------------------------------------------------------------
+// Schur-mode KKT of one rank's share of a block-arrowhead problem (SCOPF,
+// SURVEY.md 8(e)).  The rank's sub-problem (coupling variables first, then
+// its contingency blocks) is assembled with the ordinary bit-exact refill;
+// the multifrontal factorization eliminates the blocks and leaves the
+// assembled coupling front -- the rank's Schur contribution
+// S_g = A00_g - sum_k A0k Akk^-1 Ak0 -- which the caller sums over ranks
+// (NCCL allreduce); every rank then factors the dense S the same way.
+__global__ void k_front_to_dense(int n0, size_t ld, const double* __restrict__ F, double* S) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x, j = blockIdx.y;
+  if (i < n0) S[i + static_cast<size_t>(j) * n0] = i >= j ? F[i + j * ld] : 0.0;
+}
+__global__ void k_dense_to_slots(int n0, const double* __restrict__ S, const int* __restrict__ cp,
+                                 double shift, double* kv) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x, j = blockIdx.y;
+  if (i < n0 && i >= j)
+    kv[cp[j] + (i - j)] = S[i + static_cast<size_t>(j) * n0] + (i == j ? shift : 0.0);
+}
+
+class SchurSystem {
+ public:
+  SchurSystem(KktPlan plan, const ncl_kkt_opts& opt) : ks_(std::move(plan), opt), opt_(opt) {
+    n0_ = ks_.ldl().schur_n0();
+    if (n0_ <= 0) throw std::invalid_argument("schur: no coupling variables");
+    LowerCsc D;
+    D.n = n0_;
+    D.col_ptr.assign(static_cast<size_t>(n0_) + 1, 0);
+    for (int j = 0; j < n0_; ++j) {
+      for (int i = j; i < n0_; ++i) D.row_ind.push_back(i);
+      D.col_ptr[j + 1] = static_cast<int>(D.row_ind.size());
+    }
+    std::vector<int> id(static_cast<size_t>(n0_));
+    for (int i = 0; i < n0_; ++i) id[i] = i;
+    dense_ = std::make_unique<LdlSystem>(D, analyze_with_permutation(D, id), ks_.stream());
+    dcp_.upload(D.col_ptr);
+    dkval_.alloc(static_cast<size_t>(D.nnz()));
+    norm_.alloc(2);
+    CK(cudaStreamSynchronize(ks_.stream()));
+  }
+  KktSystem& kkt() { return ks_; }
+  int n0() const { return n0_; }
+  cudaStream_t stream() { return ks_.stream(); }
+
+  // refill + local factorization; stats4 = n_pos, n_neg, perturbed, fail of
+  // the block pivots; S (device, n0 x n0, lower filled, upper zero)
+  void factor(const double* hv, const double* jv, const double* sg, double rho, double delta,
+              int* stats4, double* S) {
+    cudaStream_t st = stream();
+    ks_.refill_async(hv, jv, sg, rho, delta);
+    ks_.ldl().factorize_async(ks_.kval(), opt_.pivot_eps);
+    const size_t ld = wide_ld(n0_);
+    k_front_to_dense<<<dim3((n0_ + 127) / 128, n0_), 128, 0, st>>>(n0_, ld, ks_.ldl().schur_front(),
+                                                                    S);
+    const FactorInfo F = ks_.ldl().read_factor_info();  // synchronises
+    stats4[0] = F.n_pos;
+    stats4[1] = F.n_neg;
+    stats4[2] = F.perturbed;
+    stats4[3] = F.ok ? 0 : 1;
+  }
+  void factor_dense(const double* S, double shift, int* stats4) {
+    cudaStream_t st = stream();
+    k_dense_to_slots<<<dim3((n0_ + 127) / 128, n0_), 128, 0, st>>>(n0_, S, dcp_.p, shift,
+                                                                    dkval_.p);
+    dense_->factorize_async(dkval_.p, opt_.pivot_eps);
+    const FactorInfo F = dense_->read_factor_info();
+    stats4[0] = F.n_pos;
+    stats4[1] = F.n_neg;
+    stats4[2] = F.perturbed;
+    stats4[3] = F.ok ? 0 : 1;
+  }
+  void forward(const double* b, double* b0) {
+    ks_.ldl().solve_fwd_async(b);
+    CK(cudaMemcpyAsync(b0, ks_.ldl().w_tail(), sizeof(double) * n0_, cudaMemcpyDeviceToDevice,
+                       stream()));
+    CK(cudaStreamSynchronize(stream()));
+  }
+  void solve0(const double* b0, double* x0) {
+    dense_->solve_async(b0, x0);
+    CK(cudaStreamSynchronize(stream()));
+  }
+  void backward(const double* x0, double* x) {
+    CK(cudaMemcpyAsync(ks_.ldl().x_tail(), x0, sizeof(double) * n0_, cudaMemcpyDeviceToDevice,
+                       stream()));
+    ks_.ldl().solve_bwd_async(x);
+    CK(cudaStreamSynchronize(stream()));
+  }
+  // r = b - K_g x (local matrix of the last refill)
+  void residual(const double* x, const double* b, double* r) {
+    CK(cudaMemsetAsync(norm_.p, 0, sizeof(double), stream()));
+    ks_.ldl().residual_async(ks_.kval(), x, b, r, norm_.p);
+    CK(cudaStreamSynchronize(stream()));
+  }
+  void rhs(const double* jv, const double* sg, const double* r1, const double* r2, const double* r3,
+           double rho, double delta, double* b) {
+    ks_.rhs_async(jv, sg, r1, r2, r3, rho, delta, b);
+    CK(cudaStreamSynchronize(stream()));
+  }
+  void recover(const double* jv, const double* sol, const double* r2, double rho, double delta,
+               double* dx, double* dr, double* dy) {
+    ks_.recover_async(jv, sol, r2, rho, delta, dx, dr, dy);
+    CK(cudaStreamSynchronize(stream()));
+  }
+  long long launches() { return ks_.launches() + dense_->launches(); }
+
+ private:
+  KktSystem ks_;
+  ncl_kkt_opts opt_;
+  int n0_ = 0;
+  std::unique_ptr<LdlSystem> dense_;
+  DBuf<int> dcp_;
+  DBuf<double> dkval_, norm_;
+};
+
 
 // ---------------------------------------------------------------------------
 // plain sparse system (sparse.hpp API on the device LDL^T)
@@ -792,6 +968,9 @@ struct ncl_kkt {
 };
 struct ncl_sparse {
   std::unique_ptr<nclb::SparseSystem> sys;
+};
+struct ncl_schur {
+  std::unique_ptr<nclb::SchurSystem> sys;
 };
 struct ncl_plan {
   nclb::KktPlan plan;
@@ -1116,5 +1295,101 @@ int ncl_sparse_matvec(ncl_sparse* sp, const double* x, double* y) {
     }
   return NCL_OK;
 }
+
+/* ---- Schur mode (block-arrowhead sub-problems) ---------- */
+int ncl_schur_create(int nt, const int* hp_ptr, const int* hp_idx, int m, const int* jp_ptr,
+                     const int* jp_idx, int ns, int m_eq, int n0, const ncl_kkt_opts* opt,
+                     ncl_schur** out) {
+  if (!out || !hp_ptr || !jp_ptr || n0 <= 0) {
+    nclb::last_error() = "ncl_schur_create: invalid argument";
+    return NCL_EINVAL;
+  }
+  *out = nullptr;
+  return guard([&] {
+    nclb::KktPlan plan = nclb::make_kkt_plan(nt, hp_ptr, hp_idx, m, jp_ptr, jp_idx, ns, m_eq,
+                                             nclb::kK1s, n0);
+    auto* c = new ncl_schur;
+    try {
+      c->sys = std::make_unique<nclb::SchurSystem>(std::move(plan), opt ? *opt : default_opts());
+    } catch (...) {
+      delete c;
+      throw;
+    }
+    *out = c;
+  });
+}
+
+void ncl_schur_destroy(ncl_schur* h) { delete h; }
+
+int ncl_schur_info(const ncl_schur* h, ncl_kkt_info* info) {
+  if (!h || !info) return NCL_EINVAL;
+  auto& K = h->sys->kkt();
+  const auto& P = K.plan();
+  const auto& T = K.ldl().sn();
+  info->n = P.N;
+  info->nnz = P.K.nnz();
+  info->l_nnz = P.sym.l_nnz();
+  info->flops = T.flops;
+  info->n_supernodes = T.nsn;
+  info->sn_height = T.sn_height;
+  info->n_paths = static_cast<int>(T.path_ptr.size()) - 1;
+  info->n_wide = static_cast<int>(T.lvl_nodes.size());
+  info->n_levels = static_cast<int>(T.lvl_ptr.size()) - 1;
+  info->max_front = T.max_f;
+  info->npairs = static_cast<long long>(P.pair_slot.size());
+  return NCL_OK;
+}
+
+int ncl_schur_n0(const ncl_schur* h) { return h ? h->sys->n0() : NCL_EINVAL; }
+
+int ncl_schur_factor(ncl_schur* h, const double* hval, const double* jval, const double* sigma,
+                     double rho, double delta, int* stats4, double* S) {
+  if (!h || !stats4 || !S) return NCL_EINVAL;
+  return guard([&] { h->sys->factor(hval, jval, sigma, rho, delta, stats4, S); });
+}
+
+int ncl_schur_factor_dense(ncl_schur* h, const double* S, double diag_shift, int* stats4) {
+  if (!h || !stats4 || !S) return NCL_EINVAL;
+  return guard([&] { h->sys->factor_dense(S, diag_shift, stats4); });
+}
+
+int ncl_schur_rhs(ncl_schur* h, const double* jval, const double* sigma, const double* rbar1,
+                  const double* rbar2, const double* rbar3, double rho, double delta, double* b) {
+  if (!h || !b) return NCL_EINVAL;
+  return guard([&] { h->sys->rhs(jval, sigma, rbar1, rbar2, rbar3, rho, delta, b); });
+}
+
+int ncl_schur_forward(ncl_schur* h, const double* b, double* b0) {
+  if (!h || !b || !b0) return NCL_EINVAL;
+  return guard([&] { h->sys->forward(b, b0); });
+}
+
+int ncl_schur_solve0(ncl_schur* h, const double* b0, double* x0) {
+  if (!h || !b0 || !x0) return NCL_EINVAL;
+  return guard([&] { h->sys->solve0(b0, x0); });
+}
+
+int ncl_schur_backward(ncl_schur* h, const double* x0, double* x) {
+  if (!h || !x0 || !x) return NCL_EINVAL;
+  return guard([&] { h->sys->backward(x0, x); });
+}
+
+int ncl_schur_residual(ncl_schur* h, const double* x, const double* b, double* r) {
+  if (!h || !x || !b || !r) return NCL_EINVAL;
+  return guard([&] { h->sys->residual(x, b, r); });
+}
+
+int ncl_schur_recover(ncl_schur* h, const double* jval, const double* sol, const double* rbar2,
+                      double rho, double delta, double* dx, double* dr, double* dy) {
+  if (!h || !sol) return NCL_EINVAL;
+  return guard([&] { h->sys->recover(jval, sol, rbar2, rho, delta, dx, dr, dy); });
+}
+
+int ncl_schur_launch_count(const ncl_schur* h, long long* count) {
+  if (!h || !count) return NCL_EINVAL;
+  *count = h->sys->launches();
+  return NCL_OK;
+}
+
 
 }  // extern "C"

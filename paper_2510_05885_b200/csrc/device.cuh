@@ -33,6 +33,7 @@ struct SnDev {
   const int* path_ptr;
   const int* path_nodes;
   const int8_t* wide;        // 1: wide-tier front (stored f x f in lval)
+  int schur;                 // Schur-mode coupling supernode (assembled only), or -1
 };
 
 __device__ __forceinline__ int f_minus_k(const SnDev& sd, int s) {

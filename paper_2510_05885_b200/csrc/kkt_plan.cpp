@@ -21,7 +21,7 @@ int slot_of(const LowerCsc& A, int i, int j) {
 
 KktPlan make_kkt_plan(int nt, const int* hp_ptr, const int* hp_idx, int m,
                       const int* jp_ptr, const int* jp_idx, int ns, int m_eq,
-                      int form) {
+                      int form, int schur_n0) {
   KktPlan P;
   if (form < 0 || form > 2) throw std::invalid_argument("unknown kkt form");
   if (nt < 0 || m < 0 || ns < 0 || m_eq < 0 || m - m_eq != ns)
@@ -175,8 +175,25 @@ KktPlan make_kkt_plan(int nt, const int* hp_ptr, const int* hp_idx, int m,
     P.inertia_target[1] = 0;
   }
   // symbolic analysis (kkt.cpp:94 -> sparse.cpp:178-180)
-  P.sym = analyze_with_permutation(K, amd_order(K));
-  P.sn = build_supernodal(K, P.sym);
+  if (schur_n0 > 0) {
+    if (form != kK1s || schur_n0 > N) throw std::invalid_argument("schur: K1s and n0 <= N only");
+    // AMD on the block part K[n0:, n0:], coupling columns last in their order
+    LowerCsc B;
+    B.n = N - schur_n0;
+    B.col_ptr.assign(static_cast<size_t>(B.n) + 1, 0);
+    for (int j = schur_n0; j < N; ++j) {
+      for (int p = K.col_ptr[j]; p < K.col_ptr[j + 1]; ++p) B.row_ind.push_back(K.row_ind[p] - schur_n0);
+      B.col_ptr[j - schur_n0 + 1] = static_cast<int>(B.row_ind.size());
+    }
+    std::vector<int> perm = amd_order(B);
+    for (int& v : perm) v += schur_n0;
+    for (int j = 0; j < schur_n0; ++j) perm.push_back(j);
+    P.sym = analyze_with_permutation(K, perm);
+    P.sn = build_supernodal(K, P.sym, schur_n0);
+  } else {
+    P.sym = analyze_with_permutation(K, amd_order(K));
+    P.sn = build_supernodal(K, P.sym);
+  }
   return P;
 }
 

@@ -47,8 +47,11 @@ struct KktPlan {
 };
 
 // throws std::invalid_argument on inconsistent shapes (kkt.cpp:52-53)
+// schur_n0 > 0 (K1s only): Schur mode for a block-arrowhead sub-problem whose
+// first schur_n0 variables couple the blocks -- they are ordered last (AMD on
+// the rest) and form the unfactored coupling supernode
 KktPlan make_kkt_plan(int nt, const int* hp_ptr, const int* hp_idx, int m,
                       const int* jp_ptr, const int* jp_idx, int ns, int m_eq,
-                      int form);
+                      int form, int schur_n0 = 0);
 
 }  // namespace nclb

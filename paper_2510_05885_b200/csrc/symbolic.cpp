@@ -477,7 +477,7 @@ Symbolic analyze_with_permutation(const LowerCsc& A,
 
 // ---------------------------------------------------------------------------
 // Fundamental supernodes, front structures, maps and schedules.
-Supernodal build_supernodal(const LowerCsc& A, const Symbolic& S) {
+Supernodal build_supernodal(const LowerCsc& A, const Symbolic& S, int schur_n0) {
   const int n = S.n;
   Supernodal T;
   T.n = n;
@@ -496,8 +496,13 @@ Supernodal build_supernodal(const LowerCsc& A, const Symbolic& S) {
                       (j - T.first.back()) < 1024;
     if (!cont) T.first.push_back(j);
   }
+  if (schur_n0 > 0 && schur_n0 <= n) {  // one supernode for the coupling columns
+    while (!T.first.empty() && T.first.back() > n - schur_n0) T.first.pop_back();
+    if (T.first.empty() || T.first.back() < n - schur_n0) T.first.push_back(n - schur_n0);
+  }
   if (n > 0) T.first.push_back(n);
   T.nsn = n > 0 ? static_cast<int>(T.first.size()) - 1 : 0;
+  if (schur_n0 > 0 && schur_n0 <= n) T.schur = T.nsn - 1;
   if (n == 0) T.first.assign(1, 0);
   const int nsn = T.nsn;
   std::vector<int> col2sn(static_cast<size_t>(n));
@@ -615,7 +620,7 @@ Supernodal build_supernodal(const LowerCsc& A, const Symbolic& S) {
   // tiers: wide = front above the warp limit, closed upward
   T.wide.assign(static_cast<size_t>(nsn), 0);
   for (int s = 0; s < nsn; ++s) {
-    if (T.f[s] > kWarpFront) T.wide[s] = 1;
+    if (T.f[s] > kWarpFront || s == T.schur) T.wide[s] = 1;
     if (T.wide[s] && T.sparent[s] >= 0) T.wide[T.sparent[s]] = 1;
   }
   // storage.  Warp tier: an f x k column-major L block in lval and a compact
@@ -750,7 +755,7 @@ Supernodal build_supernodal(const LowerCsc& A, const Symbolic& S) {
     const bool huge = fmax > kHugeFront;
     for (int q = T.lvl_ptr[l]; q < T.lvl_ptr[l + 1] && huge; ++q) {
       const int s = T.lvl_nodes[q];
-      const int f = T.f[s], k = T.first[s + 1] - T.first[s];
+      const int f = T.f[s], k = s == T.schur ? 0 : T.first[s + 1] - T.first[s];
       for (int cb = 0; cb < f; cb += kAsmCols) T.asm_task.push_back({s, cb, 0, 0});
       maxp = std::max(maxp, (k + kWidePanel - 1) / kWidePanel);
     }
@@ -758,7 +763,7 @@ Supernodal build_supernodal(const LowerCsc& A, const Symbolic& S) {
     for (int p = 0; p < maxp; ++p) {
       for (int q = T.lvl_ptr[l]; q < T.lvl_ptr[l + 1]; ++q) {
         const int s = T.lvl_nodes[q];
-        const int f = T.f[s], k = T.first[s + 1] - T.first[s];
+        const int f = T.f[s], k = s == T.schur ? 0 : T.first[s + 1] - T.first[s];
         if (k <= p * kWidePanel) continue;
         const int p1 = std::min((p + 1) * kWidePanel, k);
         const int mt = f - p1;

@@ -99,6 +99,7 @@ struct Supernodal {
   int max_dg = 0;  // most fronts in one huge panel launch
   std::vector<std::array<int, 4>> tiles;
   long long wide_update_flops = 0;
+  int schur = -1;  // Schur mode: the coupling supernode (assembled, not factored)
   int max_f = 0, max_wide_f = 0;
   long long flops = 0;      // sum_j c_j (c_j + 2), the SURVEY 8(d) figure
   long long wide_front_elems = 0;
@@ -113,6 +114,9 @@ constexpr int kPanelRows = 128; // rows below a panel solved per CTA (huge path)
 constexpr int kHugeFront = 1536;  // levels with a larger front use the
                                   // three-kernel (whole-GPU) path
 
-Supernodal build_supernodal(const LowerCsc& A, const Symbolic& S);
+// schur_n0 > 0 (Schur mode): the last schur_n0 columns of the elimination
+// order form one supernode that is assembled (extend-add of every child) but
+// not factored; its front is the local Schur complement.
+Supernodal build_supernodal(const LowerCsc& A, const Symbolic& S, int schur_n0 = 0);
 
 }  // namespace nclb

@@ -469,7 +469,8 @@ k_wide_front(SnDev sd, FactorDev fd, const double* __restrict__ kval,
   // trailing tile still receives its updates in panel order (the phases are
   // separated by cluster barriers).
   int pend_p0 = 0, pend_p1 = 0, pend_nb = 0, pend_T = 0;  // deferred update
-  for (int p0 = 0; p0 < k; p0 += kWidePanel) {
+  const int kp = s == sd.schur ? 0 : k;  // Schur mode: the coupling front is only assembled
+  for (int p0 = 0; p0 < kp; p0 += kWidePanel) {
     const int p1 = min(p0 + kWidePanel, k), nb = p1 - p0;
     const int rows = f - p1;
     const int chunk = (rows + C - 1) / C;

@@ -91,6 +91,7 @@ k_fwd_front(SnDev sd, const double* __restrict__ lval, double* w, double* uvec,
   const double* L = lval + sd.l_off[s];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   double* u = uvec + sd.rel_ptr[s];
+  const int kp = s == sd.schur ? 0 : k;  // Schur mode: assemble the coupling rhs only
   if (rank == 0 && k > 0) {
     // stages: block b (columns [32b, 32b+nb)), rows [32b, k) in chunks of kRows
     int sb = 0, sr = 0, buf = 0;
@@ -100,7 +101,7 @@ k_fwd_front(SnDev sd, const double* __restrict__ lval, double* w, double* uvec,
       shv[bf] = stage_cols(sm.P[bf], L, ld, r0, min(kRows, k - r0), p0, nb, warp, lane);
       cp_commit();
     };
-    issue(0, 0, 0);
+    if (kp > 0) issue(0, 0, 0);
     for (int r = tid; r < f; r += kSolveThreads) T[r] = r < k ? __ldcg(w + c0 + r) : 0.0;
     __syncthreads();
     for (int cc = sd.ch_ptr[s]; cc < sd.ch_ptr[s + 1]; ++cc) {
@@ -109,7 +110,7 @@ k_fwd_front(SnDev sd, const double* __restrict__ lval, double* w, double* uvec,
       for (int i = tid; i < fu; i += kSolveThreads) T[sd.rel[rp + i]] += __ldcg(uvec + rp + i);
       __syncthreads();
     }
-    for (;;) {
+    for (; kp > 0;) {
       const int p0 = sb * kBlk, p1 = min(p0 + kBlk, k), nb = p1 - p0;
       const int nr = min(kRows, k - sr);
       // next stage into the other buffer
@@ -231,7 +232,7 @@ k_bwd_front(SnDev sd, const double* __restrict__ lval, const double* __restrict_
   const double* L = lval + sd.l_off[s];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int* rows = sd.rows + sd.rows_ptr[s];
-  if (k == 0) return;
+  if (k == 0 || s == sd.schur) return;  // Schur mode: coupling solution set by the host
   for (int r = k + tid; r < f; r += kSolveThreads) X[r] = __ldcg(x + rows[r]);
   __syncthreads();
   // z_p = w_p / d_p - sum_{r >= k} L(r, p) x_r for this CTA's pivot columns,
