@@ -259,6 +259,22 @@ int ncl_schur_recover(ncl_schur* h, const double* jval, const double* sol,
                       double* dr, double* dy);
 int ncl_schur_launch_count(const ncl_schur* h, long long* count);
 
+
+/* ---- init_multipliers (proj/src/solver.cpp:43-91) ------------------------
+ * least-squares multiplier estimate (JJ^T + 1e-8 I [+1 on slack rows]) y =
+ * J grad, clipped to +-1e3, HOST buffers.  Same triplets as the reference's
+ * all-pairs loop (nonzero dots only, bit-identical values), found from the
+ * rows sharing a column instead of all m^2 pairs; factored on the device with
+ * eps = 1e-14, unrefined solve.  seconds4 (optional): candidate pairs, device
+ * dots, symbolic analysis, numeric factor+solve. */
+int ncl_init_multipliers(int m, int m_eq, int nt, const int* jp_ptr,
+                         const int* jp_idx, const double* jval,
+                         const double* grad, double* y, double* seconds4);
+/* host-only: the candidate pairs (i, j <= i sharing a column, ascending);
+ * count always set, pairs written when cap >= count */
+int ncl_jjt_candidates(int m, int nt, const int* jp_ptr, const int* jp_idx,
+                       long long cap, long long* count, int* pi, int* pj);
+
 #ifdef __cplusplus
 }
 #endif

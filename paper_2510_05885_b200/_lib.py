@@ -94,6 +94,8 @@ SIGS = {
     "ncl_nlp_clip_duals": ([_p, _p, _d, _p, _p], _i),
     "ncl_nlp_outer": ([_p, _p, _p, _d, _i, _dp], _i),
     "ncl_initial_outer_state": ([_d, _d, _d, _dp], None),
+    "ncl_init_multipliers": ([_i, _i, _i, _ip, _ip, _dp, _dp, _dp, _dp], _i),
+    "ncl_jjt_candidates": ([_i, _i, _ip, _ip, _ll, C.POINTER(_ll), _ip, _ip], _i),
     "ncl_schur_create": ([_i, _ip, _ip, _i, _ip, _ip, _i, _i, _i, C.POINTER(KktOpts), C.POINTER(_p)], _i),
     "ncl_schur_destroy": ([_p], None),
     "ncl_schur_info": ([_p, C.POINTER(KktInfo)], _i),

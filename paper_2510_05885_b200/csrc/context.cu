@@ -12,6 +12,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <array>
 #include <cmath>
 #include <cstdio>
@@ -959,6 +960,141 @@ class SparseSystem {
   DBuf<double> kval_, b_, x_;
 };
 
+// ---------------------------------------------------------------------------
+// init_multipliers (solver.cpp:43-91) without the O(m^2) row-pair loop: the
+// candidate pairs are the rows that share a Jacobian column (host, once per
+// pattern), their dots run on the device one pair per thread with the
+// reference's ascending-column merge and separate rounding of every product
+// and sum (__dmul_rn/__dadd_rn: bit-identical to the -ffp-contract=off
+// reference), exact-zero dots are dropped as the reference drops them, and
+// the system goes through the same static-pivot LDL^T (eps 1e-14, no
+// refinement, sparse.cpp:182-276) on the device.
+__global__ void k_jjt_dots(long long npairs, const int* __restrict__ pi, const int* __restrict__ pj,
+                           const int* __restrict__ jp_ptr, const int* __restrict__ jp_idx,
+                           const double* __restrict__ jv, int m_eq, double* out) {
+  const long long q = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (q >= npairs) return;
+  const int i = pi[q], j = pj[q];
+  double dot = 0.0;
+  int pa = jp_ptr[i], pb = jp_ptr[j];
+  const int ea = jp_ptr[i + 1], eb = jp_ptr[j + 1];
+  while (pa < ea && pb < eb) {
+    const int ca = jp_idx[pa], cb = jp_idx[pb];
+    if (ca < cb) {
+      ++pa;
+    } else if (ca > cb) {
+      ++pb;
+    } else {
+      dot = __dadd_rn(dot, __dmul_rn(jv[pa], jv[pb]));
+      ++pa;
+      ++pb;
+    }
+  }
+  if (i == j) {
+    if (i >= m_eq) dot = __dadd_rn(dot, 1.0);  // slack column
+    dot = __dadd_rn(dot, 1e-8);
+  }
+  out[q] = dot;
+}
+
+// rows sharing a column with row i, j <= i, ascending (rows of J^T merged)
+void jjt_candidates(int m, int nt, const int* jp_ptr, const int* jp_idx, std::vector<int>& pi,
+                    std::vector<int>& pj) {
+  std::vector<int> cnt(static_cast<size_t>(nt) + 1, 0);
+  for (int p = 0; p < jp_ptr[m]; ++p) cnt[jp_idx[p] + 1]++;
+  for (int c = 0; c < nt; ++c) cnt[c + 1] += cnt[c];
+  std::vector<int> rows(static_cast<size_t>(cnt[nt]));
+  std::vector<int> nx(cnt.begin(), cnt.end() - 1);
+  for (int i = 0; i < m; ++i)
+    for (int p = jp_ptr[i]; p < jp_ptr[i + 1]; ++p) rows[nx[jp_idx[p]]++] = i;
+  std::vector<int> mark(static_cast<size_t>(m), -1), tmp;
+  pi.clear();
+  pj.clear();
+  for (int i = 0; i < m; ++i) {
+    tmp.clear();
+    mark[i] = i;
+    tmp.push_back(i);  // the diagonal is always kept
+    for (int p = jp_ptr[i]; p < jp_ptr[i + 1]; ++p) {
+      const int c = jp_idx[p];
+      for (int q = cnt[c]; q < cnt[c + 1]; ++q) {
+        const int j = rows[q];
+        if (j > i) break;  // rows of a column ascend
+        if (mark[j] != i) {
+          mark[j] = i;
+          tmp.push_back(j);
+        }
+      }
+    }
+    std::sort(tmp.begin(), tmp.end());
+    for (int j : tmp) {
+      pi.push_back(i);
+      pj.push_back(j);
+    }
+  }
+}
+
+struct InitMultipliersTiming {
+  double pairs = 0, dots = 0, symbolic = 0, numeric = 0;
+};
+
+void init_multipliers(int m, int m_eq, int nt, const int* jp_ptr, const int* jp_idx,
+                      const double* jv, const double* g, double* y, InitMultipliersTiming* tm) {
+  using clk = std::chrono::steady_clock;
+  auto secs = [](clk::time_point a, clk::time_point b) {
+    return std::chrono::duration<double>(b - a).count();
+  };
+  if (m == 0) return;
+  const auto t0 = clk::now();
+  std::vector<int> pi, pj;
+  jjt_candidates(m, nt, jp_ptr, jp_idx, pi, pj);
+  const auto t1 = clk::now();
+  const long long np = static_cast<long long>(pi.size());
+  const int nnzj = jp_ptr[m];
+  cudaStream_t st;
+  CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  std::vector<double> dots(static_cast<size_t>(np));
+  {
+    DBuf<int> dpi, dpj, dptr, didx;
+    DBuf<double> djv, dout;
+    dpi.upload(pi);
+    dpj.upload(pj);
+    dptr.upload(std::vector<int>(jp_ptr, jp_ptr + m + 1));
+    didx.upload(std::vector<int>(jp_idx, jp_idx + nnzj));
+    djv.upload(std::vector<double>(jv, jv + nnzj));
+    dout.alloc(static_cast<size_t>(np));
+    k_jjt_dots<<<static_cast<unsigned>((np + 255) / 256), 256, 0, st>>>(np, dpi.p, dpj.p, dptr.p, didx.p,
+                                                                       djv.p, m_eq, dout.p);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(dots.data(), dout.p, sizeof(double) * np, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+  }
+  CK(cudaStreamDestroy(st));
+  std::vector<int> rows, cols;
+  std::vector<double> vals;
+  for (long long q = 0; q < np; ++q)
+    if (pi[q] == pj[q] || dots[q] != 0.0) {
+      rows.push_back(pi[q]);
+      cols.push_back(pj[q]);
+      vals.push_back(dots[q]);
+    }
+  const auto t2 = clk::now();
+  SparseSystem A(m, rows, cols, vals, nullptr);
+  const auto t3 = clk::now();
+  A.factorize(1e-14);
+  std::vector<double> rhs(static_cast<size_t>(m), 0.0);
+  for (int i = 0; i < m; ++i)
+    for (int p = jp_ptr[i]; p < jp_ptr[i + 1]; ++p) rhs[i] += jv[p] * g[jp_idx[p]];
+  A.solve(rhs.data(), y);
+  for (int i = 0; i < m; ++i) y[i] = std::min(1e3, std::max(-1e3, y[i]));
+  const auto t4 = clk::now();
+  if (tm) {
+    tm->pairs = secs(t0, t1);
+    tm->dots = secs(t1, t2);
+    tm->symbolic = secs(t2, t3);
+    tm->numeric = secs(t3, t4);
+  }
+}
+
 }  // namespace nclb
 
 // ===========================================================================
@@ -1391,5 +1527,35 @@ int ncl_schur_launch_count(const ncl_schur* h, long long* count) {
   return NCL_OK;
 }
 
+
+/* ---- init_multipliers (solver.cpp:43-91) --------------------------------- */
+int ncl_init_multipliers(int m, int m_eq, int nt, const int* jp_ptr, const int* jp_idx,
+                         const double* jval, const double* grad, double* y, double* seconds4) {
+  if (m < 0 || m_eq < 0 || m_eq > m || (m > 0 && (!jp_ptr || !y))) return NCL_EINVAL;
+  return guard([&] {
+    nclb::InitMultipliersTiming tm;
+    nclb::init_multipliers(m, m_eq, nt, jp_ptr, jp_idx, jval, grad, y, &tm);
+    if (seconds4) {
+      seconds4[0] = tm.pairs;
+      seconds4[1] = tm.dots;
+      seconds4[2] = tm.symbolic;
+      seconds4[3] = tm.numeric;
+    }
+  });
+}
+
+int ncl_jjt_candidates(int m, int nt, const int* jp_ptr, const int* jp_idx, long long cap,
+                       long long* count, int* pi, int* pj) {
+  if (!jp_ptr || !count || m < 0) return NCL_EINVAL;
+  return guard([&] {
+    std::vector<int> a, b;
+    nclb::jjt_candidates(m, nt, jp_ptr, jp_idx, a, b);
+    *count = static_cast<long long>(a.size());
+    if (pi && pj && cap >= *count) {
+      std::copy(a.begin(), a.end(), pi);
+      std::copy(b.begin(), b.end(), pj);
+    }
+  });
+}
 
 }  // extern "C"
