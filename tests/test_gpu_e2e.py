@@ -88,3 +88,16 @@ def test_drop_in_matches_golden_solve_logs():
                  kkt_residual=float(z["kkt_residual"]),
                  extrapolation_accepts=g["extrapolation_accepts"])  # not in the fixture
         compare(g, r, degenerate="mpcc" in stem)
+
+
+@pytest.mark.skipif(not (drop.available() and O.ref_available()), reason="prebuilt libraries missing")
+@pytest.mark.parametrize("spec,form", [("opf-toy-200", "k1s"), ("convex-qp-50", "k1s"), ("hs35", "k2r"),
+                                       ("opf_mesh:10:10:3", "k1s"), ("mpcc-basic", "k2r")])
+def test_drop_in_with_device_init_multipliers(spec, form, monkeypatch):
+    """the drop-in build with init_multipliers (solver.cpp:43-91) on the device
+    (NCL_B200_INIT_MULTIPLIERS=1, integration/init_multipliers_b200.cpp): same
+    status and outer sequence, converged solution within 1e-8"""
+    r = O.RefModel(spec).solve(form=form, tol=1e-8)
+    monkeypatch.setenv("NCL_B200_INIT_MULTIPLIERS", "1")
+    g = drop.DropModel(spec).solve(form=form, tol=1e-8)
+    compare(g, r, degenerate="mpcc" in spec)
