@@ -490,11 +490,31 @@ Supernodal build_supernodal(const LowerCsc& A, const Symbolic& S, int schur_n0) 
   // fundamental supernodes: j+1 continues j iff parent[j] == j+1, j+1 has
   // j as its only child and count(j) == count(j+1) + 1
   T.first.push_back(0);
+  // Schur mode also relaxes them: column j joins its child j-1's supernode
+  // whenever the explicit zeros that adds keep the dense front within 25 % of
+  // the true nonzeros (column j-1's pattern minus j lies inside column j's, so
+  // the front is still k + count(last)) -- up to as many zeros as nonzeros, at
+  // most 96 pivots.  Block-arrowhead problems carry the
+  // coupling rows through every block front, and chains of 4-pivot fronts
+  // collapse into a few wide ones.  (Not in the default mode: the reference's
+  // L pattern is read back from the fronts there.)
+  const bool relax = schur_n0 > 0;
+  long long sn_true = n > 0 ? cnt[0] + 1 : 0;  // true nonzeros of the open supernode
   for (int j = 1; j < n; ++j) {
-    const bool cont = S.parent[j - 1] == j && nchild[j] == 1 &&
-                      cnt[j - 1] == cnt[j] + 1 &&
-                      (j - T.first.back()) < 1024;
-    if (!cont) T.first.push_back(j);
+    const int k = j - T.first.back();
+    bool cont = S.parent[j - 1] == j && nchild[j] == 1 && cnt[j - 1] == cnt[j] + 1 && k < 1024;
+    if (!cont && relax && S.parent[j - 1] == j && k < 96) {
+      const long long f = k + 1 + cnt[j];                    // front with j joined
+      const long long dense = (2 * f - k) * (k + 1) / 2;     // sum_{i<=k} (f - i)
+      const long long truenz = sn_true + cnt[j] + 1;
+      cont = dense - truenz <= truenz;
+    }
+    if (cont) {
+      sn_true += cnt[j] + 1;
+    } else {
+      T.first.push_back(j);
+      sn_true = cnt[j] + 1;
+    }
   }
   if (schur_n0 > 0 && schur_n0 <= n) {  // one supernode for the coupling columns
     while (!T.first.empty() && T.first.back() > n - schur_n0) T.first.pop_back();
