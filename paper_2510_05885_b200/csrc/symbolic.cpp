@@ -487,8 +487,8 @@ Supernodal build_supernodal(const LowerCsc& A, const Symbolic& S, int schur_n0) 
     if (S.parent[j] >= 0) nchild[S.parent[j]]++;
     T.flops += static_cast<long long>(cnt[j]) * (cnt[j] + 2);
   }
-  // fundamental supernodes: j+1 continues j iff parent[j] == j+1, j+1 has
-  // j as its only child and count(j) == count(j+1) + 1
+  // supernodes: j+1 continues j iff parent[j] == j+1 and count(j) ==
+  // count(j+1) + 1 (column j's pattern is exactly {j+1} + column j+1's)
   T.first.push_back(0);
   // Schur mode also relaxes them: column j joins its child j-1's supernode
   // whenever the explicit zeros that adds keep the dense front within 25 % of
@@ -502,7 +502,9 @@ Supernodal build_supernodal(const LowerCsc& A, const Symbolic& S, int schur_n0) 
   long long sn_true = n > 0 ? cnt[0] + 1 : 0;  // true nonzeros of the open supernode
   for (int j = 1; j < n; ++j) {
     const int k = j - T.first.back();
-    bool cont = S.parent[j - 1] == j && nchild[j] == 1 && cnt[j - 1] == cnt[j] + 1 && k < 1024;
+    // exact nesting (no explicit zeros); other children of j may hang off the
+    // supernode's interior columns -- their updates land in its front rows
+    bool cont = S.parent[j - 1] == j && cnt[j - 1] == cnt[j] + 1 && k < 1024;
     if (!cont && relax && S.parent[j - 1] == j && k < 96) {
       const long long f = k + 1 + cnt[j];                    // front with j joined
       const long long dense = (2 * f - k) * (k + 1) / 2;     // sum_{i<=k} (f - i)

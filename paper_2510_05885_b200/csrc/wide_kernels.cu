@@ -303,9 +303,8 @@ __device__ __forceinline__ void trsm_steps(int pb, int pe, double (&x)[kWidePane
                                            const int* prog, bool& bad) {
 #pragma unroll 1
   for (int p = pb; p < pe; ++p) {
-    if (prog)
-      while (ld_acquire_smem(prog) <= p) {
-      }
+    if (prog)  // back off between polls: the diagonal warp shares the LSU
+      while (ld_acquire_smem(prog) <= p) __nanosleep(64);
     const double l = x[0] * rinv[p];
     row[p * ld] = l;
     bad |= !isfinite(l);

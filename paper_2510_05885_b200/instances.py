@@ -323,6 +323,74 @@ def mpcc_sep(pairs: int) -> Instance:
     return inst
 
 
+class _ElecEval:
+    """COPS 'elec' (integration/instances.hpp elec): Coulomb potential of np
+    points, sum_{i<j} 1 / |p_i - p_j|, constraints |p_i|^2 - 1 = 0.  The
+    Hessian pattern is the dense lower triangle (every pair of points shares
+    a nonlinear element)."""
+
+    def __init__(self, npt, inst):
+        self.np = npt
+        self.inst = inst
+        n = 3 * npt
+        c = np.arange(n, dtype=np.int64)
+        self.colstart = c * n - c * (c - 1) // 2  # slot of (c, c) in the dense lower CSC
+
+    def eval(self, t, y):
+        npt, n = self.np, 3 * self.np
+        P = t.reshape(npt, 3)
+        H = np.zeros((n, n))
+        grad = np.zeros(n)
+        for i in range(npt):
+            d = P[i] - P            # (np, 3)
+            r2 = (d * d).sum(1)
+            r2[i] = 1.0
+            r = np.sqrt(r2)
+            inv3, inv5 = 1.0 / (r2 * r), 1.0 / (r2 * r2 * r)
+            B = 3.0 * d[:, :, None] * d[:, None, :] * inv5[:, None, None] - \
+                np.eye(3)[None] * inv3[:, None, None]
+            B[i] = 0.0
+            H[3 * i:3 * i + 3, 3 * i:3 * i + 3] += B.sum(0)
+            H[3 * i:3 * i + 3, :] -= B.transpose(1, 0, 2).reshape(3, n)
+            g = -d * inv3[:, None]
+            g[i] = 0.0
+            grad[3 * i:3 * i + 3] = g.sum(0)
+        for i in range(npt):  # -y_i * grad^2 (|p_i|^2 - 1) = -2 y_i I
+            H[3 * i + np.arange(3), 3 * i + np.arange(3)] += -2.0 * y[i]
+        hval = np.concatenate([H[c:, c] for c in range(n)])
+        jval = (2.0 * P).reshape(-1)
+        cval = (P * P).sum(1) - 1.0
+        return hval, jval, grad, cval
+
+
+def elec(npt: int, seed: int) -> Instance:
+    """integration/instances.hpp elec (COPS 3.0): seeded start on the sphere
+    (problems.cpp:17-24 Rng draws th, ph per point in order)."""
+    n = 3 * npt
+    u = rng_bits(seed, 2 * npt)
+    th = 0.0 + (2.0 * 3.14159265358979323846 - 0.0) * u[0::2]
+    ph = 0.0 + (3.14159265358979323846 - 0.0) * u[1::2]
+    start = np.empty(n)
+    start[0::3] = np.cos(th) * np.sin(ph)
+    start[1::3] = np.sin(th) * np.sin(ph)
+    start[2::3] = np.cos(ph)
+    hp_ptr = np.zeros(n + 1, np.int32)
+    hp_ptr[1:] = np.cumsum(np.arange(n, 0, -1))
+    hp_idx = np.concatenate([np.arange(c, n, dtype=np.int32) for c in range(n)])
+    jp_ptr = (3 * np.arange(npt + 1)).astype(np.int32)
+    jp_idx = np.arange(n, dtype=np.int32)
+    inst = Instance(f"elec:{npt}:{seed}", n, 0, npt, npt, hp_ptr, hp_idx, jp_ptr, jp_idx,
+                    np.full(n, -np.inf), np.full(n, np.inf), start)
+    inst.evaluator = _ElecEval(npt, inst)
+    return inst
+
+
+def rng_bits(seed: int, k: int) -> np.ndarray:
+    """k draws of problems.cpp:20-23's u = (gen() >> 11) * 2^-53"""
+    g = MT19937_64(seed)
+    return (g.raw(k) >> np.uint64(11)).astype(np.float64) * (1.0 / 9007199254740992.0)
+
+
 def build(spec: str) -> Instance:
     t = spec.split(":")
     if t[0] == "opf_toy":
@@ -331,6 +399,8 @@ def build(spec: str) -> Instance:
         return opf_mesh(int(t[1]), int(t[2]), int(t[3]))
     if t[0] == "mpcc_sep":
         return mpcc_sep(int(t[1]))
+    if t[0] == "elec":
+        return elec(int(t[1]), int(t[2]))
     raise ValueError(f"unknown instance spec {spec}")
 
 
