@@ -112,10 +112,10 @@ class LdlSystem {
         const int nd = T.dg_ptr[g + 1] - T.dg_ptr[g];
         const int np = T.pn_ptr[g + 1] - T.pn_ptr[g];
         const int nt = T.tl_ptr[g + 1] - T.tl_ptr[g];
-        launch_wide_diag(sd_, fd, dg_nodes_.p + T.dg_ptr[g], nd, g - T.lp_ptr[l], eps, st_);
-        launch_wide_panel(sd_, fd, pn_tasks_.p + T.pn_ptr[g], np, g - T.lp_ptr[l], st_);
-        launch_wide_update(sd_, fd, tiles_.p + T.tl_ptr[g], nt, st_);
-        launches_ += (nd > 0) + (np > 0) + (nt > 0);
+        launch_wide_panel(sd_, fd, pn_tasks_.p + T.pn_ptr[g], np, g - T.lp_ptr[l], eps, st_);
+        launch_wide_update(sd_, fd, tiles_.p + T.tl_ptr[g], nt, dg_nodes_.p + T.dg_ptr[g], nd,
+                           g - T.lp_ptr[l], st_);
+        launches_ += (np > 0) + (nt > 0 || nd > 0);
       }
     }
     CK(cudaGetLastError());
@@ -168,7 +168,7 @@ class LdlSystem {
     for (int l = 0; l < nlevels(); ++l) {
       const int used = launch_fwd_front(sd_, lval_.p, wp_.p, uvec_.p, lvl_nodes_.p + sn_.lvl_ptr[l],
                                         sn_.lvl_ptr[l + 1] - sn_.lvl_ptr[l], solve_cluster_[l],
-                                        lvl_fmax_[l], st_);
+                                        lvl_fmax_[l], lvl_kmax_[l] >= solve_par_k(), st_);
       if (used == 0) throw CudaError("k_fwd_front: no cluster configuration fits");
       solve_cluster_[l] = used;
     }
@@ -180,7 +180,7 @@ class LdlSystem {
       const int used = launch_bwd_front(sd_, lval_.p, d_.p, wp_.p, xp_.p,
                                         lvl_nodes_.p + sn_.lvl_ptr[l],
                                         sn_.lvl_ptr[l + 1] - sn_.lvl_ptr[l], solve_cluster_[l],
-                                        lvl_fmax_[l], st_);
+                                        lvl_fmax_[l], bscr_.p, lvl_kmax_[l] >= solve_par_k(), st_);
       if (used == 0) throw CudaError("k_bwd_front: no cluster configuration fits");
       solve_cluster_[l] = used;
     }
@@ -212,7 +212,7 @@ class LdlSystem {
     for (int l = 0; l < nl; ++l) {
       const int used = launch_fwd_front(sd_, lval_.p, wp_.p, uvec_.p, lvl_nodes_.p + sn_.lvl_ptr[l],
                                         sn_.lvl_ptr[l + 1] - sn_.lvl_ptr[l], solve_cluster_[l],
-                                        lvl_fmax_[l], st_);
+                                        lvl_fmax_[l], lvl_kmax_[l] >= solve_par_k(), st_);
       if (used == 0) throw CudaError("k_fwd_front: no cluster configuration fits");
       solve_cluster_[l] = used;
     }
@@ -220,7 +220,7 @@ class LdlSystem {
       const int used = launch_bwd_front(sd_, lval_.p, d_.p, wp_.p, xp_.p,
                                         lvl_nodes_.p + sn_.lvl_ptr[l],
                                         sn_.lvl_ptr[l + 1] - sn_.lvl_ptr[l], solve_cluster_[l],
-                                        lvl_fmax_[l], st_);
+                                        lvl_fmax_[l], bscr_.p, lvl_kmax_[l] >= solve_par_k(), st_);
       if (used == 0) throw CudaError("k_bwd_front: no cluster configuration fits");
       solve_cluster_[l] = used;
     }
@@ -360,7 +360,7 @@ class LdlSystem {
       pt[i] = make_int4(T.pn_tasks[i][0], T.pn_tasks[i][1], T.pn_tasks[i][2], T.pn_tasks[i][3]);
     pn_tasks_.upload(pt);
     dg_nodes_.upload(T.dg_nodes);
-    dscr_.alloc(static_cast<size_t>(std::max(1, T.max_dg)) * (kWidePanel * kWidePanel + kWidePanel));
+    dscr_.alloc(static_cast<size_t>(std::max(1, T.max_dg)) * (kWidePanel * kWidePanel));
     asm_cp_.upload(T.asm_cp);
     cc_off_.upload(T.cc_off);
     cc_ptr_.upload(T.cc_ptr);
@@ -380,18 +380,21 @@ class LdlSystem {
     }
     lvl_cluster_.assign(static_cast<size_t>(nlevels()), 0);
     lvl_fmax_.assign(static_cast<size_t>(nlevels()), 0);
+    lvl_kmax_.assign(static_cast<size_t>(nlevels()), 0);
     solve_cluster_.assign(static_cast<size_t>(nlevels()), 1);
     for (int l = 0; l < nlevels(); ++l) {
       int fmax = 0;
       const int nf = T.lvl_ptr[l + 1] - T.lvl_ptr[l];
       for (int q = T.lvl_ptr[l]; q < T.lvl_ptr[l + 1]; ++q) fmax = std::max(fmax, T.f[T.lvl_nodes[q]]);
       lvl_fmax_[l] = fmax;
+      for (int q = T.lvl_ptr[l]; q < T.lvl_ptr[l + 1]; ++q)
+        lvl_kmax_[l] = std::max(lvl_kmax_[l], T.first[T.lvl_nodes[q] + 1] - T.first[T.lvl_nodes[q]]);
       {
         int c = 16;
         while (c > 1 && nf * c > 2 * sms) c >>= 1;
         solve_cluster_[l] = c;
       }
-      if (fmax > kHugeFront) continue;
+      if (level_is_huge(fmax, nf)) continue;  // multi-kernel path
       int c = 16;
       while (c > 1 && nf * c > 2 * sms) c >>= 1;
       lvl_cluster_[l] = c;
@@ -421,6 +424,11 @@ class LdlSystem {
     d_.alloc(static_cast<size_t>(N_));
     upd_.alloc(static_cast<size_t>(T.u_total));
     uvec_.alloc(static_cast<size_t>(T.rel_ptr[T.nsn]));
+    {
+      int maxw = 1;
+      for (int l = 0; l < nlevels(); ++l) maxw = std::max(maxw, T.lvl_ptr[l + 1] - T.lvl_ptr[l]);
+      bscr_.alloc(static_cast<size_t>(maxw) * 16 * 32);
+    }
     flags_.alloc(static_cast<size_t>(std::max(T.nsn, 1)));
     flags_.zero(st_);
     counter_.alloc(1);
@@ -500,7 +508,7 @@ class LdlSystem {
   int grid_ = 1;
   int epoch_ = 0;
   long long launches_ = 0;
-  std::vector<int> lvl_cluster_, lvl_fmax_, solve_cluster_;
+  std::vector<int> lvl_cluster_, lvl_fmax_, lvl_kmax_, solve_cluster_;
   int trace_level_ = -1;
   DBuf<unsigned long long> trace_;
   SnDev sd_{};
@@ -515,7 +523,7 @@ class LdlSystem {
   DBuf<int4> pn_tasks_;
   DBuf<int4> tiles_;
   DBuf<long long> l_off_, u_off_;
-  DBuf<double> lval_, d_, upd_, uvec_, wp_, xp_, rx_, rr_, rdx_, rxn_, rrn_;
+  DBuf<double> lval_, d_, upd_, uvec_, wp_, xp_, rx_, rr_, rdx_, rxn_, rrn_, bscr_;
   DBuf<Scalars> ds_;
   Scalars* hs_ = nullptr;
 };

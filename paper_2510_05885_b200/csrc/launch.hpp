@@ -31,12 +31,10 @@ int launch_wide_front(const SnDev& sd, const FactorDev& fd, const double* kval, 
 extern const char* wide_last_error;
 void launch_wide_assemble(const SnDev& sd, const FactorDev& fd, const double* kval,
                           const int4* tasks, int count, cudaStream_t st);
-void launch_wide_diag(const SnDev& sd, const FactorDev& fd, const int* fronts, int count,
-                      int panel, double eps, cudaStream_t st);
 void launch_wide_panel(const SnDev& sd, const FactorDev& fd, const int4* tasks, int count,
-                       int panel, cudaStream_t st);
+                       int panel, double eps, cudaStream_t st);
 void launch_wide_update(const SnDev& sd, const FactorDev& fd, const int4* tiles, int count,
-                        cudaStream_t st);
+                        const int* fronts, int nd, int panel, cudaStream_t st);
 void launch_fwd_warp(const SnDev& sd, const double* lval, double* w, double* uvec,
                      int* flags, int epoch, int* counter, int npaths, int grid,
                      cudaStream_t st);
@@ -46,10 +44,13 @@ void launch_bwd_warp(const SnDev& sd, const double* lval, const double* d,
                      cudaStream_t st);
 // wide_solve.cu: one cluster per front of a level; return the cluster used
 int launch_fwd_front(const SnDev& sd, const double* lval, double* w, double* uvec,
-                     const int* nodes, int count, int cluster, int max_f, cudaStream_t st);
-int launch_bwd_front(const SnDev& sd, const double* lval, const double* d, const double* w,
-                     double* x, const int* nodes, int count, int cluster, int max_f,
+                     const int* nodes, int count, int cluster, int max_f, bool par,
                      cudaStream_t st);
+// scr: 16 x 32 doubles per front of the level (cluster-parallel L11^T partials)
+int launch_bwd_front(const SnDev& sd, const double* lval, const double* d, const double* w,
+                     double* x, const int* nodes, int count, int cluster, int max_f, double* scr,
+                     bool par, cudaStream_t st);
+int solve_par_k();  // pivot count from which a front's L11 solve is cluster-parallel
 void launch_permute_in(int n, const int* perm, const double* b, double* w,
                        cudaStream_t st);
 void launch_permute_out(int n, const int* perm, const double* xp, double* x,

@@ -3,6 +3,7 @@
 #include "layout.hpp"
 
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <numeric>
@@ -477,6 +478,14 @@ Symbolic analyze_with_permutation(const LowerCsc& A,
 
 // ---------------------------------------------------------------------------
 // Fundamental supernodes, front structures, maps and schedules.
+bool level_is_huge(int fmax, int nfronts) {
+  static const int huge_min_f = [] {
+    const char* e = std::getenv("NCL_HUGE_MIN_F");
+    return e ? std::atoi(e) : kHugeMinF;
+  }();
+  return fmax > kHugeFront || (fmax >= huge_min_f && nfronts <= 4);
+}
+
 Supernodal build_supernodal(const LowerCsc& A, const Symbolic& S, int schur_n0) {
   const int n = S.n;
   Supernodal T;
@@ -504,7 +513,7 @@ Supernodal build_supernodal(const LowerCsc& A, const Symbolic& S, int schur_n0) 
     const int k = j - T.first.back();
     // exact nesting (no explicit zeros); other children of j may hang off the
     // supernode's interior columns -- their updates land in its front rows
-    bool cont = S.parent[j - 1] == j && cnt[j - 1] == cnt[j] + 1 && k < 1024;
+    bool cont = S.parent[j - 1] == j && cnt[j - 1] == cnt[j] + 1 && k < 65535;
     if (!cont && relax && S.parent[j - 1] == j && k < 96) {
       const long long f = k + 1 + cnt[j];                    // front with j joined
       const long long dense = (2 * f - k) * (k + 1) / 2;     // sum_{i<=k} (f - i)
@@ -774,7 +783,7 @@ Supernodal build_supernodal(const LowerCsc& A, const Symbolic& S, int schur_n0) 
   for (int l = 0; l < nlev; ++l) {
     int maxp = 0, fmax = 0;
     for (int q = T.lvl_ptr[l]; q < T.lvl_ptr[l + 1]; ++q) fmax = std::max(fmax, T.f[T.lvl_nodes[q]]);
-    const bool huge = fmax > kHugeFront;
+    const bool huge = level_is_huge(fmax, T.lvl_ptr[l + 1] - T.lvl_ptr[l]);
     for (int q = T.lvl_ptr[l]; q < T.lvl_ptr[l + 1] && huge; ++q) {
       const int s = T.lvl_nodes[q];
       const int f = T.f[s], k = s == T.schur ? 0 : T.first[s + 1] - T.first[s];
@@ -791,7 +800,7 @@ Supernodal build_supernodal(const LowerCsc& A, const Symbolic& S, int schur_n0) 
         const int mt = f - p1;
         const int di = static_cast<int>(T.dg_nodes.size()) - T.dg_ptr.back();
         T.dg_nodes.push_back(s);
-        const int nrb = (mt + kPanelRows - 1) / kPanelRows;
+        const int nrb = std::max(1, (mt + kPanelRows - 1) / kPanelRows);  // >= 1: the diag
         for (int rb = 0; rb < nrb; ++rb) T.pn_tasks.push_back({s, rb, di, 0});
         const int nt = (mt + kUpdTile - 1) / kUpdTile;
         for (int ti = 0; ti < nt; ++ti)

@@ -27,7 +27,7 @@
 // k_wide_front runs a whole tree level in ONE launch: one thread-block
 // cluster (1..16 CTAs) per front walks assembly -> panels with one panel of
 // lookahead (see the panel loop).  Levels holding huge fronts use the
-// multi-kernel path (k_wide_assemble / k_wide_diag / k_wide_panel /
+// multi-kernel path (k_wide_assemble, then per panel k_wide_panel /
 // k_wide_update) so one front spreads over every SM.
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
@@ -49,7 +49,6 @@ constexpr int kSL = 40;               // smem column stride of a staged 32-row b
 constexpr int kTrsRows = 96;          // rows per TRSM round (warps 1..3)
 constexpr int kSLT = kTrsRows + 2;    // smem column stride of the TRSM stage
 constexpr int kHugeRows = 128;        // TRSM rows per CTA, huge path
-constexpr int kSLH = kHugeRows + 2;
 constexpr unsigned kFull = 0xffffffffu;
 
 // Us[p][j] = unscaled u = F(p0+p+1+j, p0+p) after the first p pivots (zero
@@ -545,46 +544,61 @@ k_wide_assemble(SnDev sd, FactorDev fd, const double* __restrict__ kval,
     assemble_col(sd, fd, kval, s, c0, k, f, fd.lval + sd.l_off[s], wide_ld(f), J, nullptr);
 }
 
-// one warp per front: diagonal block of panel `panel`, publishes L11, D and
-// the counts, and leaves {Us, rinv} in the scratch slot of the task
-__global__ void __launch_bounds__(32)
-k_wide_diag(SnDev sd, FactorDev fd, const int* __restrict__ fronts, int panel, double eps) {
+// one CTA per (front, 128-row block below the panel): warp 0 factors the
+// diagonal block (every CTA redundantly: no extra launch), warps 1..3 solve
+// the block's rows in lockstep with it.  The CTA of row block 0 publishes D
+// and the counts, and leaves the scaled L11 in the scratch slot of its front;
+// k_wide_update writes it into the front (other CTAs of this launch may
+// still be reading the unfactored diagonal block).
+__global__ void __launch_bounds__(kHugeRows)
+k_wide_panel(SnDev sd, FactorDev fd, const int4* __restrict__ tasks, int panel, double eps) {
   __shared__ PanelSmem sm;
   __shared__ __align__(16) double D[kWidePanel * kSL];
-  const int s = fronts[blockIdx.x];
-  const int c0 = sd.first[s], k = sd.first[s + 1] - c0, f = sd.f[s];
-  const size_t ld = wide_ld(f);
-  const int p0 = panel * kWidePanel, nb = min(p0 + kWidePanel, k) - p0;
-  double* F = fd.lval + sd.l_off[s];
-  diag_block(F, ld, p0, nb, eps, sm, D, fd.d + c0 + p0, fd.stats, nullptr);
-  const int lane = threadIdx.x;
-  for (int p = 0; p < nb; ++p)
-    if (lane > p && lane < nb) F[(p0 + lane) + (p0 + p) * ld] = sm.Lsh[lane][p];
-  double* scr = fd.dscr + static_cast<size_t>(blockIdx.x) * (kWidePanel * kWidePanel + kWidePanel);
-  for (int i = lane; i < kWidePanel * kWidePanel; i += 32) scr[i] = (&sm.Us[0][0])[i];
-  scr[kWidePanel * kWidePanel + lane] = sm.rinv[lane];
-}
-
-__global__ void __launch_bounds__(kHugeRows)
-k_wide_panel(SnDev sd, FactorDev fd, const int4* __restrict__ tasks, int panel) {
-  __shared__ __align__(16) double us[kWidePanel * kWidePanel + kWidePanel];
-  __shared__ __align__(16) double TR[kWidePanel * kSLH];
+  extern __shared__ __align__(16) double TR[];  // kWidePanel * (kTrsRows + 2)
   const int4 task = tasks[blockIdx.x];
   const int s = task.x, rb = task.y;
   const int c0 = sd.first[s], k = sd.first[s + 1] - c0, f = sd.f[s];
-  const int p0 = panel * kWidePanel, p1 = min(p0 + kWidePanel, k);
-  const double* scr = fd.dscr + static_cast<size_t>(task.z) * (kWidePanel * kWidePanel + kWidePanel);
-  for (int i = threadIdx.x; i < kWidePanel * kWidePanel + kWidePanel; i += blockDim.x) us[i] = scr[i];
-  __syncthreads();
+  const size_t ld = wide_ld(f);
+  const int p0 = panel * kWidePanel, p1 = min(p0 + kWidePanel, k), nb = p1 - p0;
+  double* F = fd.lval + sd.l_off[s];
   const int lo = p1 + rb * kHugeRows, hi = min(f, lo + kHugeRows);
-  trsm_rows<kHugeRows>(fd.lval + sd.l_off[s], wide_ld(f), p0, p1 - p0, lo, max(lo, hi), us,
-                       us + kWidePanel * kWidePanel, fd.stats, threadIdx.x, TR, nullptr, 1);
+  if (threadIdx.x == 0) sm.prog = 0;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    diag_block(F, ld, p0, nb, eps, sm, D, rb == 0 ? fd.d + c0 + p0 : nullptr,
+               rb == 0 ? fd.stats : nullptr, &sm.prog);
+    if (rb == 0) {
+      double* scr = fd.dscr + static_cast<size_t>(task.z) * (kWidePanel * kWidePanel);
+      for (int i = threadIdx.x; i < kWidePanel * kWidePanel; i += 32)
+        scr[i] = sm.Lsh[i / kWidePanel][i % kWidePanel];
+    }
+  } else {
+    trsm_rows<kTrsRows>(F, ld, p0, nb, lo, max(lo, hi), &sm.Us[0][0], sm.rinv, fd.stats,
+                        threadIdx.x - 32, TR, &sm.prog, 1);
+  }
 }
 
-// one 4-warp group (CTA) per 32x32 tile
+// one 4-warp group (CTA) per 32x32 tile; block 0 also writes the panel's L11
+// blocks from the scratch slots of the nd fronts
 __global__ void __launch_bounds__(128)
-k_wide_update(SnDev sd, FactorDev fd, const int4* __restrict__ tiles) {
+k_wide_update(SnDev sd, FactorDev fd, const int4* __restrict__ tiles, int count,
+              const int* __restrict__ fronts, int nd, int panel) {
   __shared__ __align__(16) GroupSmem G;
+  if (blockIdx.x == 0) {
+    for (int di = 0; di < nd; ++di) {
+      const int s = fronts[di];
+      const int c0 = sd.first[s], k = sd.first[s + 1] - c0, f = sd.f[s];
+      const size_t ld = wide_ld(f);
+      const int p0 = panel * kWidePanel, nb = min(p0 + kWidePanel, k) - p0;
+      const double* scr = fd.dscr + static_cast<size_t>(di) * (kWidePanel * kWidePanel);
+      double* F = fd.lval + sd.l_off[s];
+      for (int idx = threadIdx.x; idx < kWidePanel * kWidePanel; idx += blockDim.x) {
+        const int i = idx / kWidePanel, p = idx % kWidePanel;
+        if (i > p && i < nb) F[(p0 + i) + (p0 + p) * ld] = scr[idx];
+      }
+    }
+  }
+  if (static_cast<int>(blockIdx.x) >= count) return;
   const int4 t = tiles[blockIdx.x];
   const int s = t.x;
   const int c0 = sd.first[s], k = sd.first[s + 1] - c0, f = sd.f[s];
@@ -654,19 +668,21 @@ void launch_wide_assemble(const SnDev& sd, const FactorDev& fd, const double* kv
   if (count) k_wide_assemble<<<count, 256, 0, st>>>(sd, fd, kval, tasks);
 }
 
-void launch_wide_diag(const SnDev& sd, const FactorDev& fd, const int* fronts, int count,
-                      int panel, double eps, cudaStream_t st) {
-  if (count) k_wide_diag<<<count, 32, 0, st>>>(sd, fd, fronts, panel, eps);
-}
-
 void launch_wide_panel(const SnDev& sd, const FactorDev& fd, const int4* tasks, int count,
-                       int panel, cudaStream_t st) {
-  if (count) k_wide_panel<<<count, kHugeRows, 0, st>>>(sd, fd, tasks, panel);
+                       int panel, double eps, cudaStream_t st) {
+  static bool init = false;
+  constexpr int tr_bytes = static_cast<int>(sizeof(double)) * kWidePanel * (kTrsRows + 2);
+  if (!init) {
+    cudaFuncSetAttribute(k_wide_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, tr_bytes);
+    init = true;
+  }
+  if (count) k_wide_panel<<<count, kHugeRows, tr_bytes, st>>>(sd, fd, tasks, panel, eps);
 }
 
 void launch_wide_update(const SnDev& sd, const FactorDev& fd, const int4* tiles, int count,
-                        cudaStream_t st) {
-  if (count) k_wide_update<<<count, 128, 0, st>>>(sd, fd, tiles);
+                        const int* fronts, int nd, int panel, cudaStream_t st) {
+  const int blocks = count > 0 ? count : (nd > 0 ? 1 : 0);
+  if (blocks) k_wide_update<<<blocks, 128, 0, st>>>(sd, fd, tiles, count, fronts, nd, panel);
 }
 
 }  // namespace nclb

@@ -38,6 +38,7 @@ constexpr int kBlk = 32;
 constexpr int kRows = 240;        // rows per staged panel chunk
 constexpr int kSLP = kRows + 2;   // its column stride in shared memory
 constexpr unsigned kFull = 0xffffffffu;
+constexpr int kParK = 2048;       // pivot blocks from which the L11 solve is cluster-parallel
 
 // dynamic shared memory: the front vector (f doubles) after two panel buffers
 struct SolveSmem {
@@ -66,9 +67,9 @@ __device__ __forceinline__ void cp_wait() {
 // along it in 16-byte chunks (cp.async: many copies in flight per warp --
 // register loads from L2 stall on too few outstanding requests).
 __device__ __forceinline__ int stage_cols(double* S, const double* L, size_t ld, int r0, int nr,
-                                          int c0, int nc, int warp, int lane) {
+                                          int c0, int nc, int warp, int lane, int nwarps = kSolveWarps) {
   const int a = r0 & ~1, sh = r0 - a, n2 = (nr + sh + 1) >> 1;
-  for (int j = warp; j < nc; j += kSolveWarps) {
+  for (int j = warp; j < nc; j += nwarps) {
     const double* src = L + a + (c0 + j) * ld;
     double* dst = S + j * kSLP;
     for (int ch = lane; ch < n2; ch += 32) cp16(dst + 2 * ch, src + 2 * ch);
@@ -76,6 +77,7 @@ __device__ __forceinline__ int stage_cols(double* S, const double* L, size_t ld,
   return r0 - a;
 }
 
+template <bool PAR>
 __global__ void __launch_bounds__(kSolveThreads, 1)
 k_fwd_front(SnDev sd, const double* __restrict__ lval, double* w, double* uvec,
             const int* __restrict__ nodes) {
@@ -92,6 +94,9 @@ k_fwd_front(SnDev sd, const double* __restrict__ lval, double* w, double* uvec,
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   double* u = uvec + sd.rel_ptr[s];
   const int kp = s == sd.schur ? 0 : k;  // Schur mode: assemble the coupling rhs only
+  // big pivot blocks: the L11 solve itself is spread over the cluster
+  // (per 32-block: rank 0's chain, then every CTA's share of the rows below)
+  const bool par = PAR && kp >= kParK && C > 1;
   if (rank == 0 && k > 0) {
     // stages: block b (columns [32b, 32b+nb)), rows [32b, k) in chunks of kRows
     int sb = 0, sr = 0, buf = 0;
@@ -101,7 +106,7 @@ k_fwd_front(SnDev sd, const double* __restrict__ lval, double* w, double* uvec,
       shv[bf] = stage_cols(sm.P[bf], L, ld, r0, min(kRows, k - r0), p0, nb, warp, lane);
       cp_commit();
     };
-    if (kp > 0) issue(0, 0, 0);
+    if (kp > 0 && !par) issue(0, 0, 0);
     for (int r = tid; r < f; r += kSolveThreads) T[r] = r < k ? __ldcg(w + c0 + r) : 0.0;
     __syncthreads();
     for (int cc = sd.ch_ptr[s]; cc < sd.ch_ptr[s + 1]; ++cc) {
@@ -110,7 +115,7 @@ k_fwd_front(SnDev sd, const double* __restrict__ lval, double* w, double* uvec,
       for (int i = tid; i < fu; i += kSolveThreads) T[sd.rel[rp + i]] += __ldcg(uvec + rp + i);
       __syncthreads();
     }
-    for (; kp > 0;) {
+    for (; kp > 0 && !par;) {
       const int p0 = sb * kBlk, p1 = min(p0 + kBlk, k), nb = p1 - p0;
       const int nr = min(kRows, k - sr);
       // next stage into the other buffer
@@ -172,11 +177,56 @@ k_fwd_front(SnDev sd, const double* __restrict__ lval, double* w, double* uvec,
     }
   }
   cl.sync();
+  if (par) {
+    const int ch = (k + C - 1) / C;
+    const int mlo = rank * ch, mhi = min(k, mlo + ch);  // this CTA's rows of the L11 part
+    for (int p0 = 0; p0 < k; p0 += kBlk) {
+      const int p1 = min(p0 + kBlk, k), nb = p1 - p0;
+      const int r0 = max(p1, mlo), nr = mhi - r0;
+      int sh = 0;
+      if (nr > 0) sh = stage_cols(sm.P[1], L, ld, r0, nr, p0, nb, warp, lane);  // rows below, prefetched
+      cp_commit();
+      if (rank == 0 && warp == 0) {
+        const int sd0 = stage_cols(sm.P[0], L, ld, p0, nb, p0, nb, 0, lane, 1);
+        cp_commit();
+        cp_wait<0>();
+        __syncwarp();
+        double lv[kBlk];
+#pragma unroll
+        for (int q = 0; q < kBlk; ++q) lv[q] = (q < lane && lane < nb) ? sm.P[0][q * kSLP + lane + sd0] : 0.0;
+        double t = lane < nb ? __ldcg(w + c0 + p0 + lane) : 0.0;
+#pragma unroll
+        for (int q = 0; q < kBlk; ++q) {
+          if (q < nb) {
+            const double wq = __shfl_sync(kFull, t, q);
+            if (lane > q) t -= lv[q] * wq;
+          }
+        }
+        if (lane < nb) w[c0 + p0 + lane] = t;
+      }
+      cl.sync();
+      cp_wait<0>();
+      __syncthreads();
+      if (tid < kBlk) sm.Z[tid] = tid < nb ? __ldcg(w + c0 + p0 + tid) : 0.0;
+      __syncthreads();
+      for (int r = tid; r < nr; r += kSolveThreads) {
+        double a0 = 0.0, a1 = 0.0;
+        int q = 0;
+        for (; q + 2 <= nb; q += 2) {
+          a0 += sm.P[1][q * kSLP + r + sh] * sm.Z[q];
+          a1 += sm.P[1][(q + 1) * kSLP + r + sh] * sm.Z[q + 1];
+        }
+        if (q < nb) a0 += sm.P[1][q * kSLP + r + sh] * sm.Z[q];
+        w[c0 + r0 + r] = __ldcg(w + c0 + r0 + r) - (a0 + a1);
+      }
+      cl.sync();
+    }
+  }
   // update vector rows [k, f): u_r -= sum_{q<k} L(r, q) w_q, rows split over
   // the cluster; column chunks of 32 streamed through the two buffers
   const int rows = f - k;
   if (rows == 0 || k == 0) return;
-  if (rank != 0) {
+  if (rank != 0 || par) {
     for (int q = tid; q < k; q += kSolveThreads) T[q] = __ldcg(w + c0 + q);
   }
   const int chunk = (rows + C - 1) / C;
@@ -217,9 +267,10 @@ k_fwd_front(SnDev sd, const double* __restrict__ lval, double* w, double* uvec,
   }
 }
 
+template <bool PAR>
 __global__ void __launch_bounds__(kSolveThreads, 1)
 k_bwd_front(SnDev sd, const double* __restrict__ lval, const double* __restrict__ d,
-            const double* __restrict__ w, double* x, const int* __restrict__ nodes) {
+            const double* __restrict__ w, double* x, const int* __restrict__ nodes, double* scr) {
   extern __shared__ __align__(16) double dyn[];
   SolveSmem& sm = *reinterpret_cast<SolveSmem*>(dyn);
   double* X = dyn + sizeof(SolveSmem) / sizeof(double);
@@ -279,6 +330,52 @@ k_bwd_front(SnDev sd, const double* __restrict__ lval, const double* __restrict_
     }
   }
   cl.sync();
+  if (PAR && k >= kParK && C > 1) {  // big pivot blocks: the L11^T solve spread over the cluster
+    const int ch = (k + C - 1) / C;
+    const int mlo = rank * ch, mhi = min(k, mlo + ch);
+    double* part = scr + static_cast<size_t>(blockIdx.x / C) * (16 * kBlk);  // [rank][32]
+    for (int p1 = k; p1 > 0;) {
+      const int p0 = ((p1 - 1) / kBlk) * kBlk, nb = p1 - p0;
+      const int r0 = max(p1, mlo), nr = mhi - r0;
+      int sh = 0;
+      if (nr > 0) sh = stage_cols(sm.P[1], L, ld, r0, nr, p0, nb, warp, lane);
+      cp_commit();
+      for (int r = tid; r < nr; r += kSolveThreads) X[r] = __ldcg(x + c0 + r0 + r);
+      cp_wait<0>();
+      __syncthreads();
+      for (int j = warp; j < kBlk; j += kSolveWarps) {
+        double a = 0.0;
+        if (j < nb)
+          for (int r = lane; r < nr; r += 32) a += sm.P[1][j * kSLP + r + sh] * X[r];
+        a = wsum(a);
+        if (lane == 0) part[rank * kBlk + j] = a;
+      }
+      cl.sync();
+      if (rank == 0 && warp == 0) {
+        const int sd0 = stage_cols(sm.P[0], L, ld, p0, nb, p0, nb, 0, lane, 1);
+        cp_commit();
+        double z = 0.0;
+        for (int c = 0; c < C; ++c) z += __ldcg(part + c * kBlk + lane);  // fixed order
+        double xv = lane < nb ? __ldcg(x + c0 + p0 + lane) - z : 0.0;
+        cp_wait<0>();
+        __syncwarp();
+        double lc[kBlk];
+#pragma unroll
+        for (int j = 0; j < kBlk; ++j) lc[j] = (j > lane && j < nb) ? sm.P[0][lane * kSLP + j + sd0] : 0.0;
+#pragma unroll
+        for (int p = kBlk - 1; p >= 0; --p) {
+          if (p < nb) {
+            const double xp = __shfl_sync(kFull, xv, p);
+            if (lane < p) xv -= lc[p] * xp;
+          }
+        }
+        if (lane < nb) x[c0 + p0 + lane] = xv;
+      }
+      cl.sync();
+      p1 = p0;
+    }
+    return;
+  }
   if (rank != 0) return;
   for (int p = tid; p < k; p += kSolveThreads) X[p] = __ldcg(x + c0 + p);
   __syncthreads();
@@ -376,34 +473,46 @@ static int launch_clustered(Kern kern, int count, int cluster, size_t smem, cuda
   return 0;
 }
 
+template <bool PAR>
+static void solve_init_one(int optin) {
+  cudaFuncSetAttribute(k_fwd_front<PAR>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  cudaFuncSetAttribute(k_bwd_front<PAR>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  cudaFuncSetAttribute(k_fwd_front<PAR>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
+  cudaFuncSetAttribute(k_bwd_front<PAR>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
+}
+
 static void solve_init() {
   static bool done = false;
   if (done) return;
   int dev = 0, optin = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-  cudaFuncSetAttribute(k_fwd_front, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-  cudaFuncSetAttribute(k_bwd_front, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-  cudaFuncSetAttribute(k_fwd_front, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
-  cudaFuncSetAttribute(k_bwd_front, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
+  solve_init_one<false>(optin);
+  solve_init_one<true>(optin);
   done = true;
 }
 
+// par: the level holds a front with >= kParK pivots (cluster-parallel L11)
 int launch_fwd_front(const SnDev& sd, const double* lval, double* w, double* uvec,
-                     const int* nodes, int count, int cluster, int max_f, cudaStream_t st) {
-  if (count == 0) return cluster;
-  solve_init();
-  return launch_clustered(k_fwd_front, count, cluster, sizeof(SolveSmem) + sizeof(double) * max_f,
-                          st, sd, lval, w, uvec, nodes);
-}
-
-int launch_bwd_front(const SnDev& sd, const double* lval, const double* d, const double* w,
-                     double* x, const int* nodes, int count, int cluster, int max_f,
+                     const int* nodes, int count, int cluster, int max_f, bool par,
                      cudaStream_t st) {
   if (count == 0) return cluster;
   solve_init();
-  return launch_clustered(k_bwd_front, count, cluster, sizeof(SolveSmem) + sizeof(double) * max_f,
-                          st, sd, lval, d, w, x, nodes);
+  const size_t smem = sizeof(SolveSmem) + sizeof(double) * max_f;
+  return par ? launch_clustered(k_fwd_front<true>, count, cluster, smem, st, sd, lval, w, uvec, nodes)
+             : launch_clustered(k_fwd_front<false>, count, cluster, smem, st, sd, lval, w, uvec, nodes);
 }
+
+int launch_bwd_front(const SnDev& sd, const double* lval, const double* d, const double* w,
+                     double* x, const int* nodes, int count, int cluster, int max_f, double* scr,
+                     bool par, cudaStream_t st) {
+  if (count == 0) return cluster;
+  solve_init();
+  const size_t smem = sizeof(SolveSmem) + sizeof(double) * max_f;
+  return par ? launch_clustered(k_bwd_front<true>, count, cluster, smem, st, sd, lval, d, w, x, nodes, scr)
+             : launch_clustered(k_bwd_front<false>, count, cluster, smem, st, sd, lval, d, w, x, nodes, scr);
+}
+
+int solve_par_k() { return kParK; }
 
 }  // namespace nclb

@@ -22,7 +22,8 @@ def load(path):
             v = float(r[vi].replace(',', ''))
         except (ValueError, IndexError):
             continue
-        d = launches.setdefault(r[idi], {"name": r[ki].split('(')[0].replace('nclb::', ''), "grid": r[gi]})
+        nm = r[ki].split('(')[0].replace('nclb::', '').replace('void ', '').strip()
+        d = launches.setdefault(r[idi], {"name": nm, "grid": r[gi]})
         d[r[mi]] = v
     return list(launches.values())
 
