@@ -75,19 +75,60 @@ class LdlSystem {
   cudaStream_t stream() const { return st_; }
 
   ~LdlSystem() {
+    if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
+    if (solve_exec_) cudaGraphExecDestroy(solve_exec_);
     if (hs_) cudaFreeHost(hs_);
   }
 
   // numeric factorization of the values kval (device, lower-CSC slot order);
   // the stats land in dev_scalars()->stats (not synchronised)
+  // The launch sequence is fixed by the symbolic analysis, so from the second
+  // factorization on it is replayed as one CUDA graph (~230 launches for the
+  // 78k-bus mesh: per-launch overhead off the critical path).  The warp tier's
+  // flags are cleared in the sequence and the factorization always uses epoch
+  // 1 (solves use epochs >= 2), so the graph has no per-call arguments.
   void factorize_async(const double* kval, double eps) {
+    if (graph_exec_ && kval == g_kval_ && eps == g_eps_) {
+      CK(cudaGraphLaunch(graph_exec_, st_));
+      launches_ += g_launches_;
+      return;
+    }
+    const bool capture = use_graph_ && nfact_ >= 1 && !graph_exec_ && trace_level_ < 0;
+    ++nfact_;
+    if (capture && cudaStreamBeginCapture(st_, cudaStreamCaptureModeRelaxed) != cudaSuccess) {
+      cudaGetLastError();
+      use_graph_ = false;
+      factorize_direct(kval, eps);
+      return;
+    }
+    const long long l0 = launches_;
+    factorize_direct(kval, eps);
+    if (!capture) return;
+    cudaGraph_t g = nullptr;
+    cudaGraphExec_t ex = nullptr;
+    cudaError_t e = cudaStreamEndCapture(st_, &g);
+    if (e == cudaSuccess) e = cudaGraphInstantiate(&ex, g, 0);
+    if (g) cudaGraphDestroy(g);
+    if (e != cudaSuccess) {  // fall back to direct launches for good
+      cudaGetLastError();
+      use_graph_ = false;
+      factorize_direct(kval, eps);
+      return;
+    }
+    graph_exec_ = ex;
+    g_kval_ = kval;
+    g_eps_ = eps;
+    g_launches_ = launches_ - l0;
+    CK(cudaGraphLaunch(graph_exec_, st_));
+  }
+
+  void factorize_direct(const double* kval, double eps) {
     CK(cudaMemsetAsync(ds_.p, 0, sizeof(int) * 4, st_));
     FactorDev fd = factor_dev();
     if (sn_.path_ptr.size() > 1) {
       CK(cudaMemsetAsync(counter_.p, 0, sizeof(int), st_));
-      ++epoch_;
-      launch_factor_warp(sd_, fd, kval, flags_.p, epoch_, counter_.p, npaths(), eps,
-                         grid_, st_);
+      CK(cudaMemsetAsync(flags_.p, 0, sizeof(int) * flags_.n, st_));
+      launch_factor_warp(sd_, fd, kval, flags_.p, 1, counter_.p, npaths(), eps, grid_, st_);
     }
     launches_ += npaths() > 0 ? 1 : 0;
     const auto& T = sn_;
@@ -154,16 +195,16 @@ class LdlSystem {
     return fi;
   }
 
-  // Schur mode: the forward half (b -> permuted w, coupling rows assembled
-  // at the tail of wp) and the backward half (coupling solution at the tail
-  // of xp -> x); solve_async = both
-  void solve_fwd_async(const double* b) {
+  // Solves.  Epochs are fixed (forward 2, backward 3; the factorization uses
+  // 1) and the warp-tier flags are cleared at the start of every forward
+  // pass, so a whole solve is one argument-free CUDA graph from the second
+  // call on; the caller's vectors are copied in / out around it.
+  void fwd_seq(const double* b) {
     launch_permute_in(N_, perm_.p, b, wp_.p, st_);
     if (npaths()) {
       CK(cudaMemsetAsync(counter_.p, 0, sizeof(int), st_));
-      ++epoch_;
-      launch_fwd_warp(sd_, lval_.p, wp_.p, uvec_.p, flags_.p, epoch_, counter_.p, npaths(),
-                      grid_, st_);
+      CK(cudaMemsetAsync(flags_.p, 0, sizeof(int) * flags_.n, st_));
+      launch_fwd_warp(sd_, lval_.p, wp_.p, uvec_.p, flags_.p, 2, counter_.p, npaths(), grid_, st_);
     }
     for (int l = 0; l < nlevels(); ++l) {
       const int used = launch_fwd_front(sd_, lval_.p, wp_.p, uvec_.p, lvl_nodes_.p + sn_.lvl_ptr[l],
@@ -175,7 +216,7 @@ class LdlSystem {
     launches_ += 1 + (npaths() > 0 ? 1 : 0) + nlevels();
     CK(cudaGetLastError());
   }
-  void solve_bwd_async(double* x) {
+  void bwd_seq(double* x) {
     for (int l = nlevels() - 1; l >= 0; --l) {
       const int used = launch_bwd_front(sd_, lval_.p, d_.p, wp_.p, xp_.p,
                                         lvl_nodes_.p + sn_.lvl_ptr[l],
@@ -186,14 +227,19 @@ class LdlSystem {
     }
     if (npaths()) {
       CK(cudaMemsetAsync(counter_.p, 0, sizeof(int), st_));
-      ++epoch_;
-      launch_bwd_warp(sd_, lval_.p, d_.p, wp_.p, xp_.p, flags_.p, epoch_, wide_.p,
-                      counter_.p, npaths(), grid_, st_);
+      launch_bwd_warp(sd_, lval_.p, d_.p, wp_.p, xp_.p, flags_.p, 3, wide_.p, counter_.p,
+                      npaths(), grid_, st_);
     }
     launch_permute_out(N_, perm_.p, xp_.p, x, st_);
     launches_ += 1 + (npaths() > 0 ? 1 : 0) + nlevels();
     CK(cudaGetLastError());
   }
+
+  // Schur mode: the forward half (b -> permuted w, coupling rows assembled
+  // at the tail of wp) and the backward half (coupling solution at the tail
+  // of xp -> x)
+  void solve_fwd_async(const double* b) { fwd_seq(b); }
+  void solve_bwd_async(double* x) { bwd_seq(x); }
   int schur_n0() const { return sn_.schur >= 0 ? N_ - sn_.first[sn_.schur] : 0; }
   const double* schur_front() const { return lval_.p + sn_.l_off[sn_.schur]; }
   double* w_tail() { return wp_.p + (N_ - schur_n0()); }
@@ -201,38 +247,42 @@ class LdlSystem {
 
   // x = P^T L^-T D^-1 L^-1 P b (device vectors, async)
   void solve_async(const double* b, double* x) {
-    launch_permute_in(N_, perm_.p, b, wp_.p, st_);
-    if (npaths()) {
-      CK(cudaMemsetAsync(counter_.p, 0, sizeof(int), st_));
-      ++epoch_;
-      launch_fwd_warp(sd_, lval_.p, wp_.p, uvec_.p, flags_.p, epoch_, counter_.p, npaths(),
-                      grid_, st_);
+    if (!use_graph_ || trace_level_ >= 0) {
+      fwd_seq(b);
+      bwd_seq(x);
+      return;
     }
-    const int nl = nlevels();
-    for (int l = 0; l < nl; ++l) {
-      const int used = launch_fwd_front(sd_, lval_.p, wp_.p, uvec_.p, lvl_nodes_.p + sn_.lvl_ptr[l],
-                                        sn_.lvl_ptr[l + 1] - sn_.lvl_ptr[l], solve_cluster_[l],
-                                        lvl_fmax_[l], lvl_kmax_[l] >= solve_par_k(), st_);
-      if (used == 0) throw CudaError("k_fwd_front: no cluster configuration fits");
-      solve_cluster_[l] = used;
+    CK(cudaMemcpyAsync(bin_.p, b, sizeof(double) * N_, cudaMemcpyDeviceToDevice, st_));
+    if (!solve_exec_ && nsolve_ >= 1) {  // capture the second solve
+      if (cudaStreamBeginCapture(st_, cudaStreamCaptureModeRelaxed) == cudaSuccess) {
+        const long long l0 = launches_;
+        fwd_seq(bin_.p);
+        bwd_seq(xout_.p);
+        cudaGraph_t g = nullptr;
+        cudaError_t e = cudaStreamEndCapture(st_, &g);
+        if (e == cudaSuccess) e = cudaGraphInstantiate(&solve_exec_, g, 0);
+        if (g) cudaGraphDestroy(g);
+        if (e != cudaSuccess) {
+          cudaGetLastError();
+          solve_exec_ = nullptr;
+          use_graph_ = false;
+        }
+        s_launches_ = launches_ - l0;
+        launches_ = l0;
+      } else {
+        cudaGetLastError();
+        use_graph_ = false;
+      }
     }
-    for (int l = nl - 1; l >= 0; --l) {
-      const int used = launch_bwd_front(sd_, lval_.p, d_.p, wp_.p, xp_.p,
-                                        lvl_nodes_.p + sn_.lvl_ptr[l],
-                                        sn_.lvl_ptr[l + 1] - sn_.lvl_ptr[l], solve_cluster_[l],
-                                        lvl_fmax_[l], bscr_.p, lvl_kmax_[l] >= solve_par_k(), st_);
-      if (used == 0) throw CudaError("k_bwd_front: no cluster configuration fits");
-      solve_cluster_[l] = used;
+    ++nsolve_;
+    if (solve_exec_) {
+      CK(cudaGraphLaunch(solve_exec_, st_));
+      launches_ += s_launches_;
+    } else {
+      fwd_seq(bin_.p);
+      bwd_seq(xout_.p);
     }
-    if (npaths()) {
-      CK(cudaMemsetAsync(counter_.p, 0, sizeof(int), st_));
-      ++epoch_;
-      launch_bwd_warp(sd_, lval_.p, d_.p, wp_.p, xp_.p, flags_.p, epoch_, wide_.p,
-                      counter_.p, npaths(), grid_, st_);
-    }
-    launch_permute_out(N_, perm_.p, xp_.p, x, st_);
-    launches_ += 2 + (npaths() > 0 ? 2 : 0) + 2 * nlevels();
-    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(x, xout_.p, sizeof(double) * N_, cudaMemcpyDeviceToDevice, st_));
   }
 
   // r = b - A x; norm slot (device) receives max|r| (must be zeroed by caller)
@@ -433,6 +483,8 @@ class LdlSystem {
     flags_.zero(st_);
     counter_.alloc(1);
     wp_.alloc(static_cast<size_t>(N_));
+    bin_.alloc(static_cast<size_t>(N_));
+    xout_.alloc(static_cast<size_t>(N_));
     xp_.alloc(static_cast<size_t>(N_));
     rx_.alloc(static_cast<size_t>(N_));
     rr_.alloc(static_cast<size_t>(N_));
@@ -506,7 +558,17 @@ class LdlSystem {
   cudaStream_t st_;
   int N_ = 0;
   int grid_ = 1;
-  int epoch_ = 0;
+  int epoch_ = 1;  // the factorization uses epoch 1, solves 2, 3, ...
+  bool use_graph_ = std::getenv("NCL_NO_GRAPH") == nullptr;
+  int nfact_ = 0;
+  cudaGraphExec_t graph_exec_ = nullptr;
+  const double* g_kval_ = nullptr;
+  double g_eps_ = 0.0;
+  long long g_launches_ = 0;
+  cudaGraphExec_t solve_exec_ = nullptr;
+  int nsolve_ = 0;
+  long long s_launches_ = 0;
+  DBuf<double> bin_, xout_;
   long long launches_ = 0;
   std::vector<int> lvl_cluster_, lvl_fmax_, lvl_kmax_, solve_cluster_;
   int trace_level_ = -1;
