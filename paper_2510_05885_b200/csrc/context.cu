@@ -77,6 +77,8 @@ class LdlSystem {
   ~LdlSystem() {
     if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
     if (solve_exec_) cudaGraphExecDestroy(solve_exec_);
+    for (auto e : evs_) cudaEventDestroy(e);
+    if (st2_) cudaStreamDestroy(st2_);
     if (hs_) cudaFreeHost(hs_);
   }
 
@@ -149,15 +151,28 @@ class LdlSystem {
       const int na = T.asm_task_ptr[l + 1] - T.asm_task_ptr[l];
       launch_wide_assemble(sd_, fd, kval, asm_task_.p + T.asm_task_ptr[l], na, st_);
       launches_ += na > 0;
-      for (int g = T.lp_ptr[l]; g < T.lp_ptr[l + 1]; ++g) {
+      // one panel of lookahead across two streams: the panel kernel of g+1
+      // runs as soon as the strip update of g is in, the rest of g's update
+      // overlaps it on st2_ (every tile still sees the panels in order: the
+      // strip of g waits for the rest of g-1, the panel of g for the rest of g-2)
+      const int g0 = T.lp_ptr[l], g1 = T.lp_ptr[l + 1];
+      for (int g = g0; g < g1; ++g) {
         const int nd = T.dg_ptr[g + 1] - T.dg_ptr[g];
         const int np = T.pn_ptr[g + 1] - T.pn_ptr[g];
         const int nt = T.tl_ptr[g + 1] - T.tl_ptr[g];
-        launch_wide_panel(sd_, fd, pn_tasks_.p + T.pn_ptr[g], np, g - T.lp_ptr[l], eps, st_);
-        launch_wide_update(sd_, fd, tiles_.p + T.tl_ptr[g], nt, dg_nodes_.p + T.dg_ptr[g], nd,
-                           g - T.lp_ptr[l], st_);
-        launches_ += (np > 0) + (nt > 0 || nd > 0);
+        const int ns = T.ts_ptr[g + 1] - T.ts_ptr[g];
+        if (g - 2 >= g0) CK(cudaStreamWaitEvent(st_, ev_rest(g - 2), 0));
+        launch_wide_panel(sd_, fd, pn_tasks_.p + T.pn_ptr[g], np, g - g0, eps, st_);
+        CK(cudaEventRecord(ev_panel(g), st_));
+        if (g - 1 >= g0) CK(cudaStreamWaitEvent(st_, ev_rest(g - 1), 0));
+        launch_wide_update(sd_, fd, tiles_s_.p + T.ts_ptr[g], ns, dg_nodes_.p + T.dg_ptr[g], nd,
+                           g - g0, st_);
+        CK(cudaStreamWaitEvent(st2_, ev_panel(g), 0));
+        launch_wide_update(sd_, fd, tiles_.p + T.tl_ptr[g], nt, nullptr, 0, g - g0, st2_);
+        CK(cudaEventRecord(ev_rest(g), st2_));
+        launches_ += (np > 0) + (ns > 0 || nd > 0) + (nt > 0);
       }
+      if (g1 > g0) CK(cudaStreamWaitEvent(st_, ev_rest(g1 - 1), 0));  // join before the next level
     }
     CK(cudaGetLastError());
   }
@@ -417,6 +432,16 @@ class LdlSystem {
     cc_ubase_.upload(T.cc_ubase);
     cc_rbase_.upload(T.cc_rbase);
     cc_cnt_.upload(T.cc_cnt);
+    {
+      std::vector<int4> ts(T.tiles_s.size());
+      for (size_t i = 0; i < ts.size(); ++i)
+        ts[i] = make_int4(T.tiles_s[i][0], T.tiles_s[i][1], T.tiles_s[i][2], T.tiles_s[i][3]);
+      tiles_s_.upload(ts);
+      const int ng = T.lp_ptr.empty() ? 0 : T.lp_ptr.back();
+      evs_.resize(static_cast<size_t>(2 * ng));
+      for (auto& e : evs_) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      CK(cudaStreamCreateWithFlags(&st2_, cudaStreamNonBlocking));
+    }
     std::vector<int4> tl(T.tiles.size());
     for (size_t i = 0; i < tl.size(); ++i)
       tl[i] = make_int4(T.tiles[i][0], T.tiles[i][1], T.tiles[i][2], T.tiles[i][3]);
@@ -583,7 +608,11 @@ class LdlSystem {
   DBuf<int8_t> wide_;
   DBuf<int4> asm_task_;
   DBuf<int4> pn_tasks_;
-  DBuf<int4> tiles_;
+  DBuf<int4> tiles_, tiles_s_;
+  cudaStream_t st2_ = nullptr;        // huge-level lookahead stream
+  std::vector<cudaEvent_t> evs_;      // per huge panel: panel done, rest done
+  cudaEvent_t ev_panel(int g) { return evs_[2 * g]; }
+  cudaEvent_t ev_rest(int g) { return evs_[2 * g + 1]; }
   DBuf<long long> l_off_, u_off_;
   DBuf<double> lval_, d_, upd_, uvec_, wp_, xp_, rx_, rr_, rdx_, rxn_, rrn_, bscr_;
   DBuf<Scalars> ds_;

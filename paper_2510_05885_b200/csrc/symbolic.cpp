@@ -779,6 +779,7 @@ Supernodal build_supernodal(const LowerCsc& A, const Symbolic& S, int schur_n0) 
   T.lp_ptr.assign(static_cast<size_t>(nlev) + 1, 0);
   T.pn_ptr.assign(1, 0);
   T.tl_ptr.assign(1, 0);
+  T.ts_ptr.assign(1, 0);
   T.dg_ptr.assign(1, 0);
   for (int l = 0; l < nlev; ++l) {
     int maxp = 0, fmax = 0;
@@ -803,13 +804,16 @@ Supernodal build_supernodal(const LowerCsc& A, const Symbolic& S, int schur_n0) 
         const int nrb = std::max(1, (mt + kPanelRows - 1) / kPanelRows);  // >= 1: the diag
         for (int rb = 0; rb < nrb; ++rb) T.pn_tasks.push_back({s, rb, di, 0});
         const int nt = (mt + kUpdTile - 1) / kUpdTile;
+        // the next panel's columns (lookahead strip) apart from the rest
+        const bool more = p1 < k;
         for (int ti = 0; ti < nt; ++ti)
           for (int tj = 0; tj <= ti; ++tj)
-            T.tiles.push_back({s, p1 + ti * kUpdTile, p1 + tj * kUpdTile, p});
+            (more && tj == 0 ? T.tiles_s : T.tiles).push_back({s, p1 + ti * kUpdTile, p1 + tj * kUpdTile, p});
         T.wide_update_flops += 2LL * (p1 - p * kWidePanel) * mt * (mt + 1) / 2;
       }
       T.pn_ptr.push_back(static_cast<int>(T.pn_tasks.size()));
       T.tl_ptr.push_back(static_cast<int>(T.tiles.size()));
+      T.ts_ptr.push_back(static_cast<int>(T.tiles_s.size()));
       T.dg_ptr.push_back(static_cast<int>(T.dg_nodes.size()));
       T.max_dg = std::max(T.max_dg, T.dg_ptr.back() - T.dg_ptr[T.dg_ptr.size() - 2]);
     }

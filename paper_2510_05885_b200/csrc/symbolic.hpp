@@ -95,7 +95,10 @@ struct Supernodal {
   std::vector<std::array<int, 4>> asm_task;  // {front, col0, 0, 0}
   std::vector<std::array<int, 4>> pn_tasks;
   std::vector<int> dg_nodes;
-  std::vector<int> asm_task_ptr, lp_ptr, pn_ptr, tl_ptr, dg_ptr;
+  // lookahead strip tiles (the next panel's column block) of panel g are
+  // tiles_s[ts_ptr[g]..], the rest tiles[tl_ptr[g]..]
+  std::vector<std::array<int, 4>> tiles_s;
+  std::vector<int> asm_task_ptr, lp_ptr, pn_ptr, tl_ptr, ts_ptr, dg_ptr;
   int max_dg = 0;  // most fronts in one huge panel launch
   std::vector<std::array<int, 4>> tiles;
   long long wide_update_flops = 0;
@@ -110,7 +113,7 @@ constexpr int kWarpFront = 32;
 constexpr int kWidePanel = 32;  // pivots per panel of a wide front
 constexpr int kAsmCols = 8;     // front columns per assembly task (warp each)
 constexpr int kUpdTile = 32;    // trailing-update tile edge (one warp)
-constexpr int kPanelRows = 128; // rows below a panel solved per CTA (huge path)
+constexpr int kPanelRows = 96;  // rows below a panel solved per CTA (huge path; 3 lockstep warps)
 constexpr int kHugeFront = 1536;  // levels with a larger front use the
                                   // three-kernel (whole-GPU) path
 

@@ -48,7 +48,7 @@ constexpr int kGroups = kWarps / 4;   // 4-warp tile groups
 constexpr int kSL = 40;               // smem column stride of a staged 32-row block
 constexpr int kTrsRows = 96;          // rows per TRSM round (warps 1..3)
 constexpr int kSLT = kTrsRows + 2;    // smem column stride of the TRSM stage
-constexpr int kHugeRows = 128;        // TRSM rows per CTA, huge path
+constexpr int kHugeRows = kPanelRows + 32;  // threads per huge-path panel CTA: diag warp + 96 TRSM
 constexpr unsigned kFull = 0xffffffffu;
 
 // Us[p][j] = unscaled u = F(p0+p+1+j, p0+p) after the first p pivots (zero
@@ -561,7 +561,7 @@ k_wide_panel(SnDev sd, FactorDev fd, const int4* __restrict__ tasks, int panel, 
   const size_t ld = wide_ld(f);
   const int p0 = panel * kWidePanel, p1 = min(p0 + kWidePanel, k), nb = p1 - p0;
   double* F = fd.lval + sd.l_off[s];
-  const int lo = p1 + rb * kHugeRows, hi = min(f, lo + kHugeRows);
+  const int lo = p1 + rb * kPanelRows, hi = min(f, lo + kPanelRows);
   if (threadIdx.x == 0) sm.prog = 0;
   __syncthreads();
   if (threadIdx.x < 32) {
