@@ -483,7 +483,11 @@ bool level_is_huge(int fmax, int nfronts) {
     const char* e = std::getenv("NCL_HUGE_MIN_F");
     return e ? std::atoi(e) : kHugeMinF;
   }();
-  return fmax > kHugeFront || (fmax >= huge_min_f && nfronts <= 4);
+  static const int huge_max_n = [] {
+    const char* e = std::getenv("NCL_HUGE_MAX_N");
+    return e ? std::atoi(e) : kHugeMaxN;
+  }();
+  return fmax > kHugeFront || (fmax >= huge_min_f && nfronts <= huge_max_n);
 }
 
 Supernodal build_supernodal(const LowerCsc& A, const Symbolic& S, int schur_n0) {

@@ -123,10 +123,11 @@ constexpr int kHugeFront = 1536;  // levels with a larger front use the
 Supernodal build_supernodal(const LowerCsc& A, const Symbolic& S, int schur_n0 = 0);
 
 // wide levels factored by the multi-kernel path (one front over every SM):
-// a front above kHugeFront, or at most four fronts of kHugeMinF rows
+// a front above kHugeFront, or at most kHugeMaxN fronts of kHugeMinF rows
 // (NCL_HUGE_MIN_F overrides; measured on the 78,400-bus mesh: 7.02 ms per
 // Newton step with the cluster kernel on those levels, 6.47 ms with this path)
 constexpr int kHugeMinF = 256;
+constexpr int kHugeMaxN = 16;
 bool level_is_huge(int fmax, int nfronts);
 
 }  // namespace nclb
