@@ -40,18 +40,6 @@ __global__ void __launch_bounds__(512, 1) k_group(double* F, size_t ld, int f, d
   if (threadIdx.x == 0) *out = t1 - t0;
 }
 
-__global__ void __launch_bounds__(512, 1) k_rowtask(double* F, size_t ld, int f, double* d, long long* out, int ngroups, int cnt) {
-  extern __shared__ __align__(16) double dyn[];
-  RowSmem* R = reinterpret_cast<RowSmem*>(dyn);
-  const int grp = threadIdx.x >> 7, gt = threadIdx.x & 127;
-  __syncthreads();
-  long long t0 = clock64();
-  if (grp < ngroups) group_rowtask(F, ld, f, d, 0, 32, 32 + 32 * 40 * grp + 256, 64, cnt, R[grp], gt, 1 + grp);
-  __syncthreads();
-  long long t1 = clock64();
-  if (threadIdx.x == 0) *out = t1 - t0;
-}
-
 int main() {
   const int f = 3200;
   const size_t ld = wide_ld(f);
@@ -70,14 +58,6 @@ int main() {
       k_group<<<1, 512, 4 * sizeof(GroupSmem)>>>(F, ld, f, d, out, ng, nt);
       cudaMemcpy(ho, out, 8, cudaMemcpyDeviceToHost);
       printf("group_tile: %d groups x %d tiles: %lld cycles (%lld per tile per group)  %s\n", ng, nt, ho[0], ho[0] / nt,
-             cudaGetErrorString(cudaGetLastError()));
-    }
-  cudaFuncSetAttribute(k_rowtask, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * (int)sizeof(RowSmem));
-  for (int ng : {1, 3, 4})
-    for (int cnt : {1, 2, 8}) {
-      k_rowtask<<<1, 512, 4 * sizeof(RowSmem)>>>(F, ld, f, d, out, ng, cnt);
-      cudaMemcpy(ho, out, 8, cudaMemcpyDeviceToHost);
-      printf("rowtask: %d groups x %d tiles: %lld cycles (%lld per tile)  %s\n", ng, cnt, ho[0], ho[0] / cnt,
              cudaGetErrorString(cudaGetLastError()));
     }
   return 0;
