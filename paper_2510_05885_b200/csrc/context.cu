@@ -135,6 +135,12 @@ class LdlSystem {
     launches_ += npaths() > 0 ? 1 : 0;
     const auto& T = sn_;
     for (int l = 0; l < nlevels(); ++l) {
+      if (lvl_fmax_[l] <= small_front_limit()) {  // a warp per front
+        launch_small_front(sd_, fd, kval, lvl_nodes_.p + T.lvl_ptr[l], T.lvl_ptr[l + 1] - T.lvl_ptr[l],
+                           eps, st_);
+        launches_ += 1;
+        continue;
+      }
       if (lvl_cluster_[l] > 0) {  // one launch, one cluster per front
         unsigned long long* tr = (l == trace_level_) ? trace_.p : nullptr;
         const int used = launch_wide_front(sd_, fd, kval, lvl_nodes_.p + T.lvl_ptr[l],
@@ -222,6 +228,11 @@ class LdlSystem {
       launch_fwd_warp(sd_, lval_.p, wp_.p, uvec_.p, flags_.p, 2, counter_.p, npaths(), grid_, st_);
     }
     for (int l = 0; l < nlevels(); ++l) {
+      if (lvl_fmax_[l] <= small_front_limit()) {
+        launch_fwd_small(sd_, lval_.p, wp_.p, uvec_.p, lvl_nodes_.p + sn_.lvl_ptr[l],
+                         sn_.lvl_ptr[l + 1] - sn_.lvl_ptr[l], st_);
+        continue;
+      }
       const int used = launch_fwd_front(sd_, lval_.p, wp_.p, uvec_.p, lvl_nodes_.p + sn_.lvl_ptr[l],
                                         sn_.lvl_ptr[l + 1] - sn_.lvl_ptr[l], solve_cluster_[l],
                                         lvl_fmax_[l], lvl_kmax_[l] >= solve_par_k(), st_);
@@ -233,6 +244,11 @@ class LdlSystem {
   }
   void bwd_seq(double* x) {
     for (int l = nlevels() - 1; l >= 0; --l) {
+      if (lvl_fmax_[l] <= small_front_limit()) {
+        launch_bwd_small(sd_, lval_.p, d_.p, wp_.p, xp_.p, lvl_nodes_.p + sn_.lvl_ptr[l],
+                         sn_.lvl_ptr[l + 1] - sn_.lvl_ptr[l], st_);
+        continue;
+      }
       const int used = launch_bwd_front(sd_, lval_.p, d_.p, wp_.p, xp_.p,
                                         lvl_nodes_.p + sn_.lvl_ptr[l],
                                         sn_.lvl_ptr[l + 1] - sn_.lvl_ptr[l], solve_cluster_[l],
