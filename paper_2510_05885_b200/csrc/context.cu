@@ -135,9 +135,9 @@ class LdlSystem {
     launches_ += npaths() > 0 ? 1 : 0;
     const auto& T = sn_;
     for (int l = 0; l < nlevels(); ++l) {
-      if (lvl_fmax_[l] <= small_front_limit()) {  // a warp per front
+      if (lvl_fmax_[l] <= small_factor_limit()) {  // a warp per front
         launch_small_front(sd_, fd, kval, lvl_nodes_.p + T.lvl_ptr[l], T.lvl_ptr[l + 1] - T.lvl_ptr[l],
-                           eps, st_);
+                           lvl_fmax_[l], eps, st_);
         launches_ += 1;
         continue;
       }
@@ -228,9 +228,9 @@ class LdlSystem {
       launch_fwd_warp(sd_, lval_.p, wp_.p, uvec_.p, flags_.p, 2, counter_.p, npaths(), grid_, st_);
     }
     for (int l = 0; l < nlevels(); ++l) {
-      if (lvl_fmax_[l] <= small_front_limit()) {
+      if (lvl_fmax_[l] <= small_solve_limit()) {
         launch_fwd_small(sd_, lval_.p, wp_.p, uvec_.p, lvl_nodes_.p + sn_.lvl_ptr[l],
-                         sn_.lvl_ptr[l + 1] - sn_.lvl_ptr[l], st_);
+                         sn_.lvl_ptr[l + 1] - sn_.lvl_ptr[l], lvl_fmax_[l], st_);
         continue;
       }
       const int used = launch_fwd_front(sd_, lval_.p, wp_.p, uvec_.p, lvl_nodes_.p + sn_.lvl_ptr[l],
@@ -244,9 +244,9 @@ class LdlSystem {
   }
   void bwd_seq(double* x) {
     for (int l = nlevels() - 1; l >= 0; --l) {
-      if (lvl_fmax_[l] <= small_front_limit()) {
+      if (lvl_fmax_[l] <= small_solve_limit()) {
         launch_bwd_small(sd_, lval_.p, d_.p, wp_.p, xp_.p, lvl_nodes_.p + sn_.lvl_ptr[l],
-                         sn_.lvl_ptr[l + 1] - sn_.lvl_ptr[l], st_);
+                         sn_.lvl_ptr[l + 1] - sn_.lvl_ptr[l], lvl_fmax_[l], st_);
         continue;
       }
       const int used = launch_bwd_front(sd_, lval_.p, d_.p, wp_.p, xp_.p,

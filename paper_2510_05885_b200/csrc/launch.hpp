@@ -42,15 +42,16 @@ void launch_bwd_warp(const SnDev& sd, const double* lval, const double* d,
                      const double* w, double* x, int* flags, int epoch,
                      const int8_t* wide, int* counter, int npaths, int grid,
                      cudaStream_t st);
-// small_front.cu: levels whose fronts all have <= small_front_limit() rows,
-// one warp per front (factorization, forward and backward solve)
-int small_front_limit();
+// small_front.cu: levels whose fronts all have <= small_*_limit() rows, one
+// warp per front (factorization; forward and backward solve)
+int small_factor_limit();
+int small_solve_limit();
 void launch_small_front(const SnDev& sd, const FactorDev& fd, const double* kval, const int* nodes,
-                        int count, double eps, cudaStream_t st);
+                        int count, int fmax, double eps, cudaStream_t st);
 void launch_fwd_small(const SnDev& sd, const double* lval, double* w, double* uvec,
-                      const int* nodes, int count, cudaStream_t st);
+                      const int* nodes, int count, int fmax, cudaStream_t st);
 void launch_bwd_small(const SnDev& sd, const double* lval, const double* d, const double* w,
-                      double* x, const int* nodes, int count, cudaStream_t st);
+                      double* x, const int* nodes, int count, int fmax, cudaStream_t st);
 // wide_solve.cu: one cluster per front of a level; return the cluster used
 int launch_fwd_front(const SnDev& sd, const double* lval, double* w, double* uvec,
                      const int* nodes, int count, int cluster, int max_f, bool par,

@@ -16,9 +16,12 @@
 
 namespace nclb {
 
-constexpr int kSmallF = 64;
-constexpr int kSmallLd = kSmallF + 1;  // conflict-free column-major shared front
-constexpr int kSmallWarps = 4;
+// instances: R rows per lane (fronts <= 32 R rows), W warps (fronts) per CTA.
+// Factorization: levels of fronts <= 64 rows (R = 2, W = 4; a one-warp
+// 128-row front was measured slower than the cluster kernel).  Solves: levels
+// of fronts <= 128 rows (R = 4, no shared front needed).
+constexpr int kSmallFactorF = 64;
+constexpr int kSmallSolveF = 128;
 constexpr unsigned kSFull = 0xffffffffu;
 
 // assembly of one column into the shared front (warp): zero, A entries, the
@@ -45,35 +48,40 @@ __device__ __forceinline__ void small_assemble_col(const SnDev& sd, const Factor
   }
 }
 
-__global__ void __launch_bounds__(kSmallWarps * 32)
+template <int R, int W>
+__global__ void __launch_bounds__(W * 32)
 k_small_front(SnDev sd, FactorDev fd, const double* __restrict__ kval,
               const int* __restrict__ nodes, int count, double eps) {
+  constexpr int FM = 32 * R, LDS = FM + 1;  // conflict-free column-major shared front
   extern __shared__ double small_smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int fi = blockIdx.x * kSmallWarps + warp;
+  const int fi = blockIdx.x * W + warp;
   if (fi >= count) return;  // warp-level work only below: no CTA barriers
-  double* S = small_smem + static_cast<size_t>(warp) * kSmallF * kSmallLd;
+  double* S = small_smem + static_cast<size_t>(warp) * FM * LDS;
   const int s = nodes[fi];
   const int c0 = sd.first[s], k = sd.first[s + 1] - c0, f = sd.f[s];
   const int kp = s == sd.schur ? 0 : k;
   const size_t ld = wide_ld(f);
   double* F = fd.lval + sd.l_off[s];
-  for (int J = 0; J < f; ++J) small_assemble_col(sd, fd, kval, s, c0, k, f, J, S + J * kSmallLd);
+  for (int J = 0; J < f; ++J) small_assemble_col(sd, fd, kval, s, c0, k, f, J, S + J * LDS);
   __syncwarp();
   int npos = 0, nneg = 0, pert = 0;
   bool bad = false;
-  const int i0 = lane, i1 = lane + 32;  // the two rows of this lane
   for (int p = 0; p < kp; ++p) {
-    const double* colp = S + p * kSmallLd;
+    const double* colp = S + p * LDS;
     double dp = colp[p];
     int pflag = 0;
     if (fabs(dp) < eps) {
       dp = (dp >= 0.0) ? eps : -eps;
       pflag = 1;
     }
-    const double l0 = (i0 > p && i0 < f) ? colp[i0] / dp : 0.0;
-    const double l1 = (i1 > p && i1 < f) ? colp[i1] / dp : 0.0;
-    bad |= !isfinite(l0) || !isfinite(l1);
+    double l[R];  // rows lane + 32 r
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int i = lane + 32 * r;
+      l[r] = (i > p && i < f) ? colp[i] / dp : 0.0;
+      bad |= !isfinite(l[r]);
+    }
     if (lane == 0) {
       fd.d[c0 + p] = dp;
       pert += pflag;
@@ -86,17 +94,23 @@ k_small_front(SnDev sd, FactorDev fd, const double* __restrict__ kval,
     // trailing update with the unscaled column p (untouched until below)
     for (int j = p + 1; j < f; ++j) {
       const double uj = colp[j];
-      double* cj = S + j * kSmallLd;
-      if (i0 >= j && i0 < f) cj[i0] -= l0 * uj;
-      if (i1 >= j && i1 < f) cj[i1] -= l1 * uj;
+      double* cj = S + j * LDS;
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int i = lane + 32 * r;
+        if (i >= j && i < f) cj[i] -= l[r] * uj;
+      }
     }
     __syncwarp();
-    if (i0 > p && i0 < f) S[p * kSmallLd + i0] = l0;
-    if (i1 > p && i1 < f) S[p * kSmallLd + i1] = l1;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int i = lane + 32 * r;
+      if (i > p && i < f) S[p * LDS + i] = l[r];
+    }
     __syncwarp();
   }
   for (int j = 0; j < f; ++j)
-    for (int i = j + lane; i < f; i += 32) F[i + j * ld] = S[j * kSmallLd + i];
+    for (int i = j + lane; i < f; i += 32) F[i + j * ld] = S[j * LDS + i];
   const bool fail = __any_sync(kSFull, bad);
   if (lane == 0) {
     if (npos) atomicAdd(fd.stats + 0, npos);
@@ -108,12 +122,13 @@ k_small_front(SnDev sd, FactorDev fd, const double* __restrict__ kval,
 
 // forward solve of a small front (warp): gather, k-step substitution with
 // the L column loaded per step (coalesced), update vector for the parent
-__global__ void __launch_bounds__(kSmallWarps * 32)
+template <int R, int W>
+__global__ void __launch_bounds__(W * 32)
 k_fwd_small(SnDev sd, const double* __restrict__ lval, double* w, double* uvec,
             const int* __restrict__ nodes, int count) {
-  __shared__ double Ts[kSmallWarps][kSmallF];
+  __shared__ double Ts[W][32 * R];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int fi = blockIdx.x * kSmallWarps + warp;
+  const int fi = blockIdx.x * W + warp;
   if (fi >= count) return;
   double* T = Ts[warp];
   const int s = nodes[fi];
@@ -129,28 +144,40 @@ k_fwd_small(SnDev sd, const double* __restrict__ lval, double* w, double* uvec,
     for (int i = lane; i < fu; i += 32) T[sd.rel[rp + i]] += __ldcg(uvec + rp + i);
     __syncwarp();
   }
-  const int i0 = lane, i1 = lane + 32;
-  double t0 = i0 < f ? T[i0] : 0.0, t1 = i1 < f ? T[i1] : 0.0;
+  double t[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) t[r] = lane + 32 * r < f ? T[lane + 32 * r] : 0.0;
   for (int p = 0; p < kp; ++p) {
     const double* Lp = L + p * ld;
-    const double a0 = (i0 > p && i0 < f) ? __ldg(Lp + i0) : 0.0;
-    const double a1 = (i1 > p && i1 < f) ? __ldg(Lp + i1) : 0.0;
-    const double xp = __shfl_sync(kSFull, p < 32 ? t0 : t1, p & 31);
-    t0 -= a0 * xp;
-    t1 -= a1 * xp;
+    double a[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int i = lane + 32 * r;
+      a[r] = (i > p && i < f) ? __ldg(Lp + i) : 0.0;
+    }
+    double src = t[0];
+#pragma unroll
+    for (int r = 1; r < R; ++r) src = (p >> 5) == r ? t[r] : src;
+    const double xp = __shfl_sync(kSFull, src, p & 31);
+#pragma unroll
+    for (int r = 0; r < R; ++r) t[r] -= a[r] * xp;
   }
   double* u = uvec + sd.rel_ptr[s];
-  if (i0 < f) (i0 < k ? w[c0 + i0] : u[i0 - k]) = t0;
-  if (i1 < f) (i1 < k ? w[c0 + i1] : u[i1 - k]) = t1;
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int i = lane + 32 * r;
+    if (i < f) (i < k ? w[c0 + i] : u[i - k]) = t[r];
+  }
 }
 
 // backward solve of a small front (warp): L^T x = D^-1 w with the parent's
 // rows already solved; warp reductions per pivot, last pivot first
-__global__ void __launch_bounds__(kSmallWarps * 32)
+template <int R, int W>
+__global__ void __launch_bounds__(W * 32)
 k_bwd_small(SnDev sd, const double* __restrict__ lval, const double* __restrict__ d,
             const double* __restrict__ w, double* x, const int* __restrict__ nodes, int count) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int fi = blockIdx.x * kSmallWarps + warp;
+  const int fi = blockIdx.x * W + warp;
   if (fi >= count) return;
   const int s = nodes[fi];
   if (s == sd.schur) return;
@@ -158,55 +185,75 @@ k_bwd_small(SnDev sd, const double* __restrict__ lval, const double* __restrict_
   const size_t ld = wide_ld(f);
   const double* L = lval + sd.l_off[s];
   const int* rows = sd.rows + sd.rows_ptr[s];
-  const int i0 = lane, i1 = lane + 32;
-  double x0 = 0.0, x1 = 0.0;  // solved values of this lane's rows
-  if (i0 >= k && i0 < f) x0 = __ldcg(x + rows[i0]);
-  if (i1 >= k && i1 < f) x1 = __ldcg(x + rows[i1]);
+  double xv[R];  // solved values of this lane's rows
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int i = lane + 32 * r;
+    xv[r] = (i >= k && i < f) ? __ldcg(x + rows[i]) : 0.0;
+  }
   for (int p = k - 1; p >= 0; --p) {
     const double* Lp = L + p * ld;
     double part = 0.0;
-    if (i0 > p && i0 < f) part += __ldg(Lp + i0) * x0;
-    if (i1 > p && i1 < f) part += __ldg(Lp + i1) * x1;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int i = lane + 32 * r;
+      if (i > p && i < f) part += __ldg(Lp + i) * xv[r];
+    }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(kSFull, part, o);
     const double xp = __ldcg(w + c0 + p) / __ldcg(d + c0 + p) - part;
-    if (i0 == p) x0 = xp;
-    if (i1 == p) x1 = xp;
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+      if (lane + 32 * r == p) xv[r] = xp;
   }
-  if (i0 < k) x[c0 + i0] = x0;
-  if (i1 < k) x[c0 + i1] = x1;
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int i = lane + 32 * r;
+    if (i < k) x[c0 + i] = xv[r];
+  }
 }
 
 // ---------------------------------------------------------------------------
-static size_t small_front_smem() { return sizeof(double) * kSmallWarps * kSmallF * kSmallLd; }
+template <int R, int W>
+static size_t small_front_smem() { return sizeof(double) * W * (32 * R) * (32 * R + 1); }
 
-int small_front_limit() { return kSmallF; }
+int small_factor_limit() { return kSmallFactorF; }
+int small_solve_limit() { return kSmallSolveF; }
 
-void launch_small_front(const SnDev& sd, const FactorDev& fd, const double* kval, const int* nodes,
-                        int count, double eps, cudaStream_t st) {
+template <int R, int W>
+static void small_launch(const SnDev& sd, const FactorDev& fd, const double* kval, const int* nodes,
+                         int count, double eps, cudaStream_t st) {
   static bool init = false;
   if (!init) {
-    cudaFuncSetAttribute(k_small_front, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(small_front_smem()));
+    cudaFuncSetAttribute(k_small_front<R, W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(small_front_smem<R, W>()));
     init = true;
   }
-  if (count)
-    k_small_front<<<(count + kSmallWarps - 1) / kSmallWarps, kSmallWarps * 32, small_front_smem(), st>>>(
-        sd, fd, kval, nodes, count, eps);
+  k_small_front<R, W><<<(count + W - 1) / W, W * 32, small_front_smem<R, W>(), st>>>(sd, fd, kval, nodes,
+                                                                                     count, eps);
+}
+
+void launch_small_front(const SnDev& sd, const FactorDev& fd, const double* kval, const int* nodes,
+                        int count, int fmax, double eps, cudaStream_t st) {
+  if (count && fmax <= kSmallFactorF) small_launch<2, 4>(sd, fd, kval, nodes, count, eps, st);
 }
 
 void launch_fwd_small(const SnDev& sd, const double* lval, double* w, double* uvec,
-                      const int* nodes, int count, cudaStream_t st) {
-  if (count)
-    k_fwd_small<<<(count + kSmallWarps - 1) / kSmallWarps, kSmallWarps * 32, 0, st>>>(sd, lval, w, uvec,
-                                                                                      nodes, count);
+                      const int* nodes, int count, int fmax, cudaStream_t st) {
+  if (!count) return;
+  if (fmax <= 64)
+    k_fwd_small<2, 4><<<(count + 3) / 4, 128, 0, st>>>(sd, lval, w, uvec, nodes, count);
+  else
+    k_fwd_small<4, 4><<<(count + 3) / 4, 128, 0, st>>>(sd, lval, w, uvec, nodes, count);
 }
 
 void launch_bwd_small(const SnDev& sd, const double* lval, const double* d, const double* w,
-                      double* x, const int* nodes, int count, cudaStream_t st) {
-  if (count)
-    k_bwd_small<<<(count + kSmallWarps - 1) / kSmallWarps, kSmallWarps * 32, 0, st>>>(sd, lval, d, w, x,
-                                                                                      nodes, count);
+                      double* x, const int* nodes, int count, int fmax, cudaStream_t st) {
+  if (!count) return;
+  if (fmax <= 64)
+    k_bwd_small<2, 4><<<(count + 3) / 4, 128, 0, st>>>(sd, lval, d, w, x, nodes, count);
+  else
+    k_bwd_small<4, 4><<<(count + 3) / 4, 128, 0, st>>>(sd, lval, d, w, x, nodes, count);
 }
 
 }  // namespace nclb
