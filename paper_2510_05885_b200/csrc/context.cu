@@ -59,9 +59,14 @@ struct FactorInfo {
 // ---------------------------------------------------------------------------
 class LdlSystem {
  public:
+  // S: the reference's symbolic analysis (exposed, and the layout factors()
+  // returns).  The numeric work uses the same elimination tree re-postordered
+  // with the tallest child last (S2_): identical factor entries, but chains
+  // occupy consecutive columns and collapse into relaxed supernodes.
   LdlSystem(const LowerCsc& K, const Symbolic& S, cudaStream_t st, int schur_n0 = 0)
       : K_(K), S_(S), st_(st) {
-    sn_ = build_supernodal(K_, S_, schur_n0);
+    S2_ = analyze_with_permutation(K_, tallest_child_last(K_, S_.perm));
+    sn_ = build_supernodal(K_, S2_, schur_n0);
     N_ = K_.n;
     upload();
   }
@@ -378,19 +383,29 @@ class LdlSystem {
     if (!lv.empty())
       CK(cudaMemcpy(lv.data(), lval_.p, lv.size() * sizeof(double), cudaMemcpyDeviceToHost));
     if (N_) CK(cudaMemcpy(dv.data(), d_.p, dv.size() * sizeof(double), cudaMemcpyDeviceToHost));
+    // reference column j <-> internal column S2_.iperm[S_.perm[j]]
+    std::vector<int> in(static_cast<size_t>(N_));
+    for (int j = 0; j < N_; ++j) in[j] = S2_.iperm[S_.perm[j]];
     if (lcol_ptr) std::copy(S_.lcol_ptr.begin(), S_.lcol_ptr.end(), lcol_ptr);
-    if (d) std::copy(dv.begin(), dv.end(), d);
+    if (d)
+      for (int j = 0; j < N_; ++j) d[j] = dv[in[j]];
     if (!lrow_ind && !lval) return;
-    // column j of L: rows below j in the front of its supernode, ascending
-    for (int s = 0; s < nsn; ++s) {
-      const int c0 = sn_.first[s], k = sn_.first[s + 1] - c0, f = sn_.f[s];
+    // the reference's L pattern; each value from its position in the internal
+    // front (relaxed supernodes hold explicit zeros, columns are reordered)
+    const std::vector<int> lri = l_row_pattern(K_, S_);
+    std::vector<int> col2sn(static_cast<size_t>(N_));
+    for (int s = 0; s < nsn; ++s)
+      for (int c = sn_.first[s]; c < sn_.first[s + 1]; ++c) col2sn[c] = s;
+    for (int j = 0; j < N_; ++j) {
+      const int jj = in[j], s = col2sn[jj];
+      const int c0 = sn_.first[s], f = sn_.f[s], p = jj - c0;
       const long long ld = sn_.wide[s] ? wide_ld(f) : f;
-      const int* rows = sn_.rows.data() + sn_.rows_ptr[s];
-      for (int p = 0; p < k; ++p) {
-        int q = S_.lcol_ptr[c0 + p];
-        for (int r = p + 1; r < f; ++r, ++q) {
-          if (lrow_ind) lrow_ind[q] = rows[r];
-          if (lval) lval[q] = lv[static_cast<size_t>(sn_.l_off[s] + r + p * ld)];
+      const int* rows = sn_.rows.data() + sn_.rows_ptr[s];  // ascending internal rows
+      for (int q = S_.lcol_ptr[j]; q < S_.lcol_ptr[j + 1]; ++q) {
+        if (lrow_ind) lrow_ind[q] = lri[q];
+        if (lval) {
+          const int r = static_cast<int>(std::lower_bound(rows, rows + f, in[lri[q]]) - rows);
+          lval[q] = lv[static_cast<size_t>(sn_.l_off[s] + r + p * ld)];
         }
       }
     }
@@ -509,7 +524,7 @@ class LdlSystem {
       trace_.alloc(128 * static_cast<size_t>(std::max(1, T.lvl_ptr.empty() ? 1 : T.nsn)));
       trace_.zero(st_);
     }
-    perm_.upload(S_.perm);
+    perm_.upload(S2_.perm);
     lval_.alloc(static_cast<size_t>(T.l_off[T.nsn]) + kLvalPad);
     lval_.zero(st_);
     d_.alloc(static_cast<size_t>(N_));
@@ -594,7 +609,7 @@ class LdlSystem {
   }
 
   LowerCsc K_;
-  Symbolic S_;
+  Symbolic S_, S2_;
   Supernodal sn_;
   cudaStream_t st_;
   int N_ = 0;

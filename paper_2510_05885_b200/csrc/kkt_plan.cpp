@@ -188,43 +188,8 @@ KktPlan make_kkt_plan(int nt, const int* hp_ptr, const int* hp_idx, int m,
     std::vector<int> perm = amd_order(B);
     for (int& v : perm) v += schur_n0;
     for (int j = 0; j < schur_n0; ++j) perm.push_back(j);
-    // re-postorder the elimination tree with every node's tallest child last
-    // (same tree, same fill): chains then occupy consecutive columns and the
-    // relaxed supernodes of build_supernodal can follow them
-    {
-      const Symbolic S0 = analyze_with_permutation(K, perm);
-      const int n = N;
-      std::vector<int> height(static_cast<size_t>(n), 0), head(static_cast<size_t>(n), -1),
-          next(static_cast<size_t>(n), -1), order;
-      for (int j = 0; j < n; ++j)
-        if (S0.parent[j] >= 0) height[S0.parent[j]] = std::max(height[S0.parent[j]], height[j] + 1);
-      // children lists sorted by height descending -> pushed so the tallest is visited last
-      std::vector<std::vector<int>> kids(static_cast<size_t>(n));
-      std::vector<int> roots;
-      for (int j = 0; j < n; ++j) (S0.parent[j] >= 0 ? kids[S0.parent[j]] : roots).push_back(j);
-      for (auto& v : kids)
-        std::stable_sort(v.begin(), v.end(), [&](int a, int b) { return height[a] < height[b]; });
-      // iterative postorder; the coupling columns stay last (their subtree is the top)
-      std::vector<std::pair<int, int>> stack;
-      for (int r : roots) {
-        stack.push_back({r, 0});
-        while (!stack.empty()) {
-          auto& [v, i] = stack.back();
-          if (i < static_cast<int>(kids[v].size())) {
-            const int c = kids[v][i++];
-            stack.push_back({c, 0});
-          } else {
-            order.push_back(v);
-            stack.pop_back();
-          }
-        }
-      }
-      std::vector<int> np(static_cast<size_t>(n));
-      for (int k = 0; k < n; ++k) np[k] = perm[order[k]];
-      perm.swap(np);
-      (void)head;
-      (void)next;
-    }
+    // the coupling columns stay last: they are the top of the tree
+    perm = tallest_child_last(K, perm);
     P.sym = analyze_with_permutation(K, perm);
     P.sn = build_supernodal(K, P.sym, schur_n0);
   } else {

@@ -139,49 +139,74 @@ k_factor_warp(SnDev sd, FactorDev fd, const double* __restrict__ kval,
 
 // ---------------------------------------------------------------------------
 // forward solve L w = b (in place on the permuted vector w); update vectors of
-// the multifrontal solve live at uvec + rel_ptr[s] (f - k entries)
+// the multifrontal solve live at uvec + rel_ptr[s] (f - k entries).  The L
+// block's column entries of a lane's row are all loaded before the
+// substitution chain, and the heavy child's update vector is kept in shared
+// memory along the path (path tops still write theirs for other readers).
 __global__ void __launch_bounds__(kWarpsPerCta * 32)
 k_fwd_warp(SnDev sd, const double* __restrict__ lval, double* w, double* uvec,
            int* flags, int epoch, int* counter, int npaths) {
   __shared__ double Ts[kWarpsPerCta][kWF];
+  __shared__ double Hs[kWarpsPerCta][kWF];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   double* T = Ts[wid];
+  double* Hv = Hs[wid];
   for (;;) {
     const int pi = next_path(counter, lane);
     if (pi >= npaths) break;
-    for (int q = sd.path_ptr[pi]; q < sd.path_ptr[pi + 1]; ++q) {
+    const int pb = sd.path_ptr[pi], pe = sd.path_ptr[pi + 1];
+    int heavy = -1;
+    for (int q = pb; q < pe; ++q) {
       const int s = sd.path_nodes[q];
       const int c0 = sd.first[s], k = sd.first[s + 1] - c0, f = sd.f[s];
       const int chb = sd.ch_ptr[s], che = sd.ch_ptr[s + 1];
-      for (int c = chb + lane; c < che; c += 32)
-        while (ld_acquire(flags + sd.ch[c]) != epoch) {
-        }
+      const double* Lb = lval + sd.l_off[s];
+      double lv[kWF];  // L(lane, p), p < lane
+#pragma unroll
+      for (int p = 0; p < kWF; ++p)
+        lv[p] = (p < k && lane > p && lane < f) ? __ldg(Lb + lane + static_cast<size_t>(p) * f) : 0.0;
+      const double wv = (lane < k) ? __ldcg(w + c0 + lane) : 0.0;
+      for (int c = chb + lane; c < che; c += 32) {
+        const int ch = sd.ch[c];
+        if (ch != heavy)
+          while (ld_acquire(flags + ch) != epoch) {
+          }
+      }
       __syncwarp();
-      T[lane] = (lane < k) ? __ldcg(w + c0 + lane) : 0.0;
+      T[lane] = wv;
       __syncwarp();
       for (int cc = chb; cc < che; ++cc) {
         const int c = sd.ch[cc];
         const int fu = f_minus_k(sd, c);
-        if (lane < fu) T[sd.rel[sd.rel_ptr[c] + lane]] += __ldcg(uvec + sd.rel_ptr[c] + lane);
+        if (lane < fu)
+          T[sd.rel[sd.rel_ptr[c] + lane]] += (c == heavy) ? Hv[lane] : __ldcg(uvec + sd.rel_ptr[c] + lane);
         __syncwarp();
       }
       double t = (lane < f) ? T[lane] : 0.0;
-      const double* Lb = lval + sd.l_off[s];
-      for (int p = 0; p < k; ++p) {
-        const double lv = (lane > p && lane < f) ? Lb[lane + static_cast<size_t>(p) * f] : 0.0;
-        const double wp = __shfl_sync(0xffffffffu, t, p);
-        t -= lv * wp;
+#pragma unroll
+      for (int p = 0; p < kWF; ++p) {
+        if (p < k) {
+          const double wp = __shfl_sync(0xffffffffu, t, p);
+          t -= lv[p] * wp;
+        }
       }
+      __syncwarp();
+      if (lane >= k && lane < f) Hv[lane - k] = t;
       if (lane < k)
         w[c0 + lane] = t;
-      else if (lane < f)
+      else if (lane < f && q == pe - 1)
         uvec[sd.rel_ptr[s] + lane - k] = t;
-      publish(flags + s, epoch, lane);
+      if (q == pe - 1) publish(flags + s, epoch, lane);
+      heavy = s;
+      __syncwarp();
     }
   }
 }
 
-// backward solve L^T x = D^-1 w, paths taken in reverse order, top-down
+// backward solve L^T x = D^-1 w, paths taken in reverse order, top-down.
+// Lane q owns pivot q and its L column (loaded up front); the rows below the
+// block enter through one shuffle-broadcast dot product per lane, then the
+// pivots resolve last-first with one shuffle + FMA each.
 __global__ void __launch_bounds__(kWarpsPerCta * 32)
 k_bwd_warp(SnDev sd, const double* __restrict__ lval, const double* __restrict__ d,
            const double* __restrict__ w, double* x, int* flags, int epoch,
@@ -203,17 +228,28 @@ k_bwd_warp(SnDev sd, const double* __restrict__ lval, const double* __restrict__
     for (int q = pe - 1; q >= pb; --q) {
       const int s = sd.path_nodes[q];
       const int c0 = sd.first[s], k = sd.first[s + 1] - c0, f = sd.f[s];
-      double xr = 0.0;
-      if (lane >= k && lane < f) xr = __ldcg(x + sd.rows[sd.rows_ptr[s] + lane]);
-      const double zr = (lane < k) ? w[c0 + lane] / d[c0 + lane] : 0.0;
       const double* Lb = lval + sd.l_off[s];
-      for (int p = k - 1; p >= 0; --p) {
-        const double part = (lane > p && lane < f) ? Lb[lane + static_cast<size_t>(p) * f] * xr : 0.0;
-        const double sum = warp_sum(part);
-        const double xp = __shfl_sync(0xffffffffu, zr, p) - sum;
-        if (lane == p) xr = xp;
+      double lc[kWF];  // L(r, lane), r > lane
+#pragma unroll
+      for (int r = 0; r < kWF; ++r)
+        lc[r] = (lane < k && r > lane && r < f) ? __ldg(Lb + r + static_cast<size_t>(lane) * f) : 0.0;
+      const double xr = (lane >= k && lane < f) ? __ldcg(x + sd.rows[sd.rows_ptr[s] + lane]) : 0.0;
+      double z = (lane < k) ? w[c0 + lane] / d[c0 + lane] : 0.0;
+#pragma unroll
+      for (int r = 0; r < kWF; ++r) {
+        if (r >= k && r < f) {
+          const double xv = __shfl_sync(0xffffffffu, xr, r);
+          z -= lc[r] * xv;
+        }
       }
-      if (lane < k) x[c0 + lane] = xr;
+#pragma unroll
+      for (int p = kWF - 1; p >= 0; --p) {
+        if (p < k) {
+          const double xp = __shfl_sync(0xffffffffu, z, p);
+          if (lane < p) z -= lc[p] * xp;
+        }
+      }
+      if (lane < k) x[c0 + lane] = z;
       publish(flags + s, epoch, lane);
     }
   }

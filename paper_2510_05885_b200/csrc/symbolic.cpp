@@ -478,6 +478,70 @@ Symbolic analyze_with_permutation(const LowerCsc& A,
 
 // ---------------------------------------------------------------------------
 // Fundamental supernodes, front structures, maps and schedules.
+std::vector<int> l_row_pattern(const LowerCsc& A, const Symbolic& S) {
+  const int n = S.n;
+  // permuted lower pattern by row: columns j < i of row i
+  std::vector<int> rp(static_cast<size_t>(n) + 1, 0);
+  for (int c = 0; c < n; ++c)
+    for (int p = A.col_ptr[c]; p < A.col_ptr[c + 1]; ++p) {
+      const int i = S.iperm[A.row_ind[p]], j = S.iperm[c];
+      if (i != j) rp[std::max(i, j) + 1]++;
+    }
+  for (int i = 0; i < n; ++i) rp[i + 1] += rp[i];
+  std::vector<int> rc(static_cast<size_t>(rp[n]));
+  {
+    std::vector<int> nx(rp.begin(), rp.end() - 1);
+    for (int c = 0; c < n; ++c)
+      for (int p = A.col_ptr[c]; p < A.col_ptr[c + 1]; ++p) {
+        const int i = S.iperm[A.row_ind[p]], j = S.iperm[c];
+        if (i != j) rc[nx[std::max(i, j)]++] = std::min(i, j);
+      }
+  }
+  // row k's columns = its reach in the elimination tree (sparse.cpp:157-175)
+  std::vector<int> out(static_cast<size_t>(S.lcol_ptr[n]));
+  std::vector<int> fill(S.lcol_ptr.begin(), S.lcol_ptr.end() - 1), mark(static_cast<size_t>(n), -1);
+  for (int k = 0; k < n; ++k) {
+    mark[k] = k;
+    for (int p = rp[k]; p < rp[k + 1]; ++p)
+      for (int j = rc[p]; j >= 0 && mark[j] != k; j = S.parent[j]) {
+        mark[j] = k;
+        out[fill[j]++] = k;
+      }
+  }
+  return out;
+}
+
+std::vector<int> tallest_child_last(const LowerCsc& A, const std::vector<int>& perm) {
+  const Symbolic S0 = analyze_with_permutation(A, perm);
+  const int n = S0.n;
+  std::vector<int> height(static_cast<size_t>(n), 0);
+  for (int j = 0; j < n; ++j)
+    if (S0.parent[j] >= 0) height[S0.parent[j]] = std::max(height[S0.parent[j]], height[j] + 1);
+  std::vector<std::vector<int>> kids(static_cast<size_t>(n));
+  std::vector<int> roots, order;
+  order.reserve(static_cast<size_t>(n));
+  for (int j = 0; j < n; ++j) (S0.parent[j] >= 0 ? kids[S0.parent[j]] : roots).push_back(j);
+  for (auto& v : kids)
+    std::stable_sort(v.begin(), v.end(), [&](int a, int b) { return height[a] < height[b]; });
+  std::vector<std::pair<int, int>> stack;
+  for (int r : roots) {
+    stack.push_back({r, 0});
+    while (!stack.empty()) {
+      auto& [v, i] = stack.back();
+      if (i < static_cast<int>(kids[v].size())) {
+        const int c = kids[v][i++];
+        stack.push_back({c, 0});
+      } else {
+        order.push_back(v);
+        stack.pop_back();
+      }
+    }
+  }
+  std::vector<int> np(static_cast<size_t>(n));
+  for (int k = 0; k < n; ++k) np[k] = perm[order[k]];
+  return np;
+}
+
 bool level_is_huge(int fmax, int nfronts) {
   static const int huge_min_f = [] {
     const char* e = std::getenv("NCL_HUGE_MIN_F");
@@ -511,18 +575,22 @@ Supernodal build_supernodal(const LowerCsc& A, const Symbolic& S, int schur_n0) 
   // coupling rows through every block front, and chains of 4-pivot fronts
   // collapse into a few wide ones.  (Not in the default mode: the reference's
   // L pattern is read back from the fronts there.)
-  const bool relax = schur_n0 > 0;
+  // Relaxed supernodes: in Schur mode (see above); otherwise only while the
+  // merged front still fits the warp tier (<= 32 rows) -- chains of tiny
+  // fronts (ring power grids: 30k+ supernodes on one path) collapse into
+  // fewer, larger warp-tier fronts at the price of explicit zeros.
+  const bool schur_relax = schur_n0 > 0;
   long long sn_true = n > 0 ? cnt[0] + 1 : 0;  // true nonzeros of the open supernode
   for (int j = 1; j < n; ++j) {
     const int k = j - T.first.back();
     // exact nesting (no explicit zeros); other children of j may hang off the
     // supernode's interior columns -- their updates land in its front rows
     bool cont = S.parent[j - 1] == j && cnt[j - 1] == cnt[j] + 1 && k < 65535;
-    if (!cont && relax && S.parent[j - 1] == j && k < 96) {
+    if (!cont && S.parent[j - 1] == j && k < 96) {
       const long long f = k + 1 + cnt[j];                    // front with j joined
       const long long dense = (2 * f - k) * (k + 1) / 2;     // sum_{i<=k} (f - i)
       const long long truenz = sn_true + cnt[j] + 1;
-      cont = dense - truenz <= truenz;
+      cont = dense - truenz <= truenz && (schur_relax || f <= kWarpFront);
     }
     if (cont) {
       sn_true += cnt[j] + 1;

@@ -122,6 +122,15 @@ constexpr int kHugeFront = 1536;  // levels with a larger front use the
 // not factored; its front is the local Schur complement.
 Supernodal build_supernodal(const LowerCsc& A, const Symbolic& S, int schur_n0 = 0);
 
+// the same elimination tree re-postordered with every node's tallest child
+// last (same fill, same factor entries): chains become consecutive columns
+// that (relaxed) supernodes can follow.  perm[k] = variable eliminated k-th.
+std::vector<int> tallest_child_last(const LowerCsc& A, const std::vector<int>& perm);
+
+// the reference's row indices of L (sparse.cpp:157-175 / factorize's
+// ascending order per column): lrow_ind for lcol_ptr
+std::vector<int> l_row_pattern(const LowerCsc& A, const Symbolic& S);
+
 // wide levels factored by the multi-kernel path (one front over every SM):
 // a front above kHugeFront, or at most kHugeMaxN fronts of kHugeMinF rows
 // (NCL_HUGE_MIN_F overrides; measured on the 78,400-bus mesh: 7.02 ms per
