@@ -444,6 +444,10 @@ class LdlSystem {
     rel_.upload(T.rel);
     path_ptr_.upload(T.path_ptr);
     path_nodes_.upload(T.path_nodes);
+    lt_ptr_.upload(T.lt_ptr);
+    lt_ent_.upload(T.lt_ent);
+    ls_ptr_.upload(T.ls_ptr);
+    ls_ent_.upload(T.ls_ent);
     lvl_nodes_.upload(T.lvl_nodes);
     std::vector<int8_t> wide(T.wide.begin(), T.wide.end());
     wide_.upload(wide);
@@ -505,7 +509,26 @@ class LdlSystem {
       while (c > 1 && nf * c > 2 * sms) c >>= 1;
       lvl_cluster_[l] = c;
     }
-    if (std::getenv("NCL_LEVEL_STATS")) {  // diagnostic: wide-tier level profile
+    if (std::getenv("NCL_LEVEL_STATS")) {  // diagnostic: warp-tier paths, wide-tier levels
+      int longest = 0, lp = -1;
+      for (int p = 0; p + 1 < static_cast<int>(T.path_ptr.size()); ++p)
+        if (T.path_ptr[p + 1] - T.path_ptr[p] > longest) longest = T.path_ptr[p + 1] - T.path_ptr[p], lp = p;
+      if (lp >= 0) {
+        double sk = 0, sf = 0, sch = 0, slt = 0, sasm = 0;
+        for (int q = T.path_ptr[lp]; q < T.path_ptr[lp + 1]; ++q) {
+          const int s = T.path_nodes[q];
+          sk += T.first[s + 1] - T.first[s];
+          sf += T.f[s];
+          sch += T.ch_ptr[s + 1] - T.ch_ptr[s];
+          slt += T.lt_ptr[s + 1] - T.lt_ptr[s];
+          sasm += T.asm_ptr[s + 1] - T.asm_ptr[s];
+        }
+        std::fprintf(stderr,
+                     "[ncl paths] %d paths, sn_height %d, longest %d: mean k %.1f f %.1f children %.1f "
+                     "light entries %.1f A entries %.1f\n",
+                     static_cast<int>(T.path_ptr.size()) - 1, T.sn_height, longest, sk / longest, sf / longest,
+                     sch / longest, slt / longest, sasm / longest);
+      }
       for (int l = 0; l < nlevels(); ++l) {
         int fmax = 0, kmax = 0;
         double fl = 0;
@@ -602,6 +625,10 @@ class LdlSystem {
     sd_.rel = rel_.p;
     sd_.path_ptr = path_ptr_.p;
     sd_.path_nodes = path_nodes_.p;
+    sd_.lt_ptr = lt_ptr_.p;
+    sd_.lt_ent = lt_ent_.p;
+    sd_.ls_ptr = ls_ptr_.p;
+    sd_.ls_ent = ls_ent_.p;
     sd_.wide = wide_.p;
     sd_.schur = T.schur;
     grid_ = warp_tier_grid();
@@ -633,8 +660,8 @@ class LdlSystem {
   DBuf<int> first_, f_, sparent_, rows_ptr_, rows_, u_ld_, asm_ptr_, asm_pos_, asm_slot_,
       ch_ptr_, ch_, rel_ptr_, rel_, path_ptr_, path_nodes_, lvl_nodes_, perm_, flags_,
       counter_, fr_ptr_, fr_col_, fr_slot_, dg_nodes_, asm_cp_, cc_off_, cc_ptr_, cc_rbase_,
-      cc_cnt_;
-  DBuf<long long> cc_ubase_;
+      cc_cnt_, lt_ptr_, ls_ptr_;
+  DBuf<long long> cc_ubase_, lt_ent_, ls_ent_;
   DBuf<double> dscr_;
   DBuf<int8_t> wide_;
   DBuf<int4> asm_task_;

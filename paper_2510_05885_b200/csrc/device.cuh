@@ -32,6 +32,10 @@ struct SnDev {
   const int* rel;
   const int* path_ptr;
   const int* path_nodes;
+  const int* lt_ptr;         // nsn+1: light-child factor extend-add chunks
+  const long long* lt_ent;   //   src | dst << 48 (symbolic.hpp)
+  const int* ls_ptr;         // nsn+1: light-child solve chunks
+  const long long* ls_ent;
   const int8_t* wide;        // 1: wide-tier front (stored f x f in lval)
   int schur;                 // Schur-mode coupling supernode (assembled only), or -1
 };
@@ -57,6 +61,16 @@ __device__ __forceinline__ int ld_acquire(const int* p) {
 
 __device__ __forceinline__ void st_release(int* p, int v) {
   asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// 1/d: MUFU approximation + two Newton steps (|d| >= the pivot eps)
+__device__ __forceinline__ double rcp_nr(double d) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
+  double e = fma(-d, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-d, r, 1.0);
+  return fma(r, e, r);
 }
 
 // max of non-negative doubles (NaN skipped, like std::max(acc, nan) == acc)

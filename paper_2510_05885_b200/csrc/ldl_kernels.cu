@@ -17,6 +17,7 @@
 //    wide_kernels.cu (factorization) and wide_solve.cu (solves).
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <cstdio>
 
 #include "device.cuh"
 #include "launch.hpp"
@@ -47,86 +48,217 @@ __device__ __forceinline__ void publish(int* flag, int epoch, int lane) {
 }
 
 // ---------------------------------------------------------------------------
-// warp-tier numeric factorization
+// warp-tier numeric factorization.  A warp walks its path bottom-up.  Each
+// front is assembled in shared memory (lane = front row) and then factored
+// in registers: lane i holds row i of the front, pivot p broadcasts column p
+// by shuffles and every lane applies its rank-1 row update -- no shared
+// memory round trip per update.  The update block is then scattered straight
+// into the (zeroed) shared front of the next node on the path, the parent;
+// only a path top writes its update block and flag to global memory, since
+// every other node's parent is the same warp.  The assembly loads that do
+// not depend on other warps -- the A entries (kLtA chunks in registers), the
+// light children's extend-add chunks (symbolic.hpp lt_ent: destinations
+// distinct within a chunk, so a chunk is one parallel step) -- are issued
+// before the light children's flags are awaited.  Order of the sums: heavy
+// child, A entries, light children in child order.
+#ifdef NCL_WTRACE
+__device__ unsigned long long g_wtrace[6];
+#endif
+constexpr int kLtR = 6;   // light-child chunks held in registers
+constexpr int kLtA = 2;   // A-entry chunks held in registers
+constexpr long long kSrcMask = (1LL << 48) - 1;
+constexpr int kCB = kWF + 2;  // pivot-column broadcast buffer (x2 per warp)
+constexpr size_t kWarpFactorDoubles = 2 * kWF * kFLD + 2 * kCB;
+constexpr size_t kWarpFactorBytes = sizeof(double) * kWarpFactorDoubles;
+
 __global__ void __launch_bounds__(kWarpsPerCta * 32)
 k_factor_warp(SnDev sd, FactorDev fd, const double* __restrict__ kval,
               int* flags, int epoch, int* counter, int npaths, double eps) {
-  __shared__ double smem[kWarpsPerCta][kWF * kFLD];
+  extern __shared__ double wsm[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  double* F = smem[wid];
   int npos = 0, nneg = 0, pert = 0, fail = 0;
   for (;;) {
     const int pi = next_path(counter, lane);
     if (pi >= npaths) break;
     const int pb = sd.path_ptr[pi], pe = sd.path_ptr[pi + 1];
+    double* F = wsm + static_cast<size_t>(wid) * kWarpFactorDoubles;
+    double* N = F + kWF * kFLD;
+    double* cb = N + kWF * kFLD;
+    int s = sd.path_nodes[pb];
+    {
+      const int f0 = sd.f[s];
+      for (int c = 0; c < f0; ++c) F[c * kFLD + lane] = 0.0;
+    }
+    int heavy = -1;
+#ifdef NCL_WTRACE
+    const bool trc = pi == npaths - 1;
+    unsigned long long tph[6] = {0, 0, 0, 0, 0, 0};
+    long long tq = clock64();
+#define WT(i)                           \
+  if (trc) {                            \
+    const long long tn = clock64();     \
+    tph[i] += tn - tq;                  \
+    tq = tn;                            \
+  }
+#else
+#define WT(i)
+#endif
     for (int q = pb; q < pe; ++q) {
-      const int s = sd.path_nodes[q];
       const int c0 = sd.first[s], k = sd.first[s + 1] - c0, f = sd.f[s];
       const int chb = sd.ch_ptr[s], che = sd.ch_ptr[s + 1];
-      for (int c = chb + lane; c < che; c += 32)
-        while (ld_acquire(flags + sd.ch[c]) != epoch) {
-        }
+      // loads that depend on no other warp
+      const int lb = sd.lt_ptr[s], le = sd.lt_ptr[s + 1];
+      long long ent[kLtR];
+#pragma unroll
+      for (int t = 0; t < kLtR; ++t)
+        ent[t] = (lb + t * 32 < le) ? __ldg(sd.lt_ent + lb + t * 32 + lane) : -1;
+      const int ab = sd.asm_ptr[s], ae = sd.asm_ptr[s + 1];
+      double av[kLtA];
+      int ap[kLtA];
+#pragma unroll
+      for (int t = 0; t < kLtA; ++t) {
+        const int a = ab + t * 32 + lane;
+        ap[t] = a < ae ? __ldg(sd.asm_pos + a) : -1;
+        av[t] = a < ae ? __ldg(kval + __ldg(sd.asm_slot + a)) : 0.0;
+      }
+      const bool top = q == pe - 1;
+      const int sn = top ? -1 : sd.path_nodes[q + 1];
+      const int fn = top ? 0 : sd.f[sn];
+      const int myrel = (!top && lane >= k && lane < f) ? __ldg(sd.rel + sd.rel_ptr[s] + lane - k) : 0;
+      WT(0);
+      for (int c = chb + lane; c < che; c += 32) {
+        const int ch = sd.ch[c];
+        if (ch != heavy)
+          while (ld_acquire(flags + ch) != epoch) {
+          }
+      }
       __syncwarp();
-      for (int c = 0; c < f; ++c) F[c * kFLD + lane] = 0.0;
-      __syncwarp();
-      for (int a = sd.asm_ptr[s] + lane; a < sd.asm_ptr[s + 1]; a += 32) {
+      WT(1);
+      double lv[kLtR];
+#pragma unroll
+      for (int t = 0; t < kLtR; ++t) lv[t] = ent[t] >= 0 ? __ldcg(fd.upd + (ent[t] & kSrcMask)) : 0.0;
+#pragma unroll
+      for (int t = 0; t < kLtA; ++t)
+        if (ap[t] >= 0) F[(ap[t] >> 16) * kFLD + (ap[t] & 0xffff)] += av[t];
+      for (int a = ab + kLtA * 32 + lane; a < ae; a += 32) {
         const int pos = sd.asm_pos[a];
         F[(pos >> 16) * kFLD + (pos & 0xffff)] += __ldg(kval + sd.asm_slot[a]);
       }
       __syncwarp();
-      for (int cc = chb; cc < che; ++cc) {
-        const int c = sd.ch[cc];
-        const int fu = sd.u_ld[c];
-        const int* rel = sd.rel + sd.rel_ptr[c];
-        const double* U = fd.upd + sd.u_off[c];
-        if (lane < fu) {
-          const int ri = rel[lane];
-          for (int j = 0; j <= lane; ++j)
-            F[rel[j] * kFLD + ri] += __ldcg(U + lane + static_cast<size_t>(j) * fu);
+      WT(2);
+#pragma unroll
+      for (int t = 0; t < kLtR; ++t) {
+        if (lb + t * 32 < le) {
+          if (ent[t] >= 0) {
+            const int dst = static_cast<int>(ent[t] >> 48);
+            F[(dst >> 5) * kFLD + (dst & 31)] += lv[t];
+          }
+          __syncwarp();
+        }
+      }
+      for (int e = lb + kLtR * 32; e < le; e += 32) {
+        const long long x = __ldg(sd.lt_ent + e + lane);
+        if (x >= 0) {
+          const int dst = static_cast<int>(x >> 48);
+          F[(dst >> 5) * kFLD + (dst & 31)] += __ldcg(fd.upd + (x & kSrcMask));
         }
         __syncwarp();
       }
-      double* Lb = fd.lval + sd.l_off[s];
+      // fr[j]: front row `lane`, column p + j while pivot p is processed
+      // (the row shifts down one column per pivot, so the pivot column is
+      // always fr[0] and every register index is static).  Pivot p's column
+      // is broadcast through shared memory (cb, two alternating buffers, one
+      // warp barrier per pivot), the next pivot is shuffled out as soon as
+      // its column is updated, and l = u * (1/d) with the wide tier's
+      // reciprocal.  l goes to the front's column p in shared memory, d to
+      // lane p; both reach global memory in bulk after the loop.
+      WT(3);
+      double fr[kWF + 1];
+#pragma unroll
+      for (int j = 0; j < kWF; ++j) fr[j] = (j < f && lane < f) ? F[j * kFLD + lane] : 0.0;
+      fr[kWF] = 0.0;
+      double myd = 0.0;
+      bool mypf = false;
+      double dnext = __shfl_sync(0xffffffffu, fr[0], 0);
       for (int p = 0; p < k; ++p) {
-        const double u = (lane < f) ? F[p * kFLD + lane] : 0.0;
-        double dp = __shfl_sync(0xffffffffu, u, p);
-        int pflag = 0;
-        if (fabs(dp) < eps) {
-          dp = (dp >= 0.0) ? eps : -eps;
-          pflag = 1;
+        double dp = dnext;
+        const bool pf = fabs(dp) < eps;
+        if (pf) dp = (dp >= 0.0) ? eps : -eps;
+        if (lane == p) {
+          myd = dp;
+          mypf = pf;
         }
-        const bool bad = !isfinite(dp) || dp == 0.0;
         const bool mine = lane > p && lane < f;
-        const double l = mine ? u / dp : 0.0;
-#pragma unroll 4
-        for (int j = p + 1; j < f; ++j) {
-          const double uj = F[p * kFLD + j];
-          if (lane >= j && lane < f) F[j * kFLD + lane] -= l * uj;
+        const double u = fr[0];
+        double* cbp = cb + (p & 1) * kCB;
+        if (lane >= p) cbp[lane - p] = u;
+        const double l = mine ? u * rcp_nr(dp) : 0.0;
+        if (mine) F[p * kFLD + lane] = l;
+        fail |= !isfinite(l);
+        __syncwarp();
+        fr[0] = fr[1] - l * cbp[1];
+        dnext = __shfl_sync(0xffffffffu, fr[0], (p + 1) & 31);
+        const int fmp = f - p;  // live columns p .. f-1
+#pragma unroll
+        for (int b8 = 0; b8 < kWF; b8 += 8) {
+          if (b8 < fmp) {
+#pragma unroll
+            for (int j = (b8 == 0 ? 2 : b8); j < b8 + 8; j += 2) {
+              const double2 v = *reinterpret_cast<const double2*>(cbp + j);
+              fr[j - 1] = fr[j] - l * v.x;
+              fr[j] = fr[j + 1] - l * v.y;
+            }
+          }
         }
-        if (mine) {
-          Lb[lane + static_cast<size_t>(p) * f] = l;
-          if (!isfinite(l)) fail = 1;
+      }
+      __syncwarp();
+      {
+        double* Lb = fd.lval + sd.l_off[s];
+        for (int p = 0; p < k; ++p)
+          if (lane > p && lane < f) Lb[lane + static_cast<size_t>(p) * f] = F[p * kFLD + lane];
+        const bool piv = lane < k;
+        if (piv) fd.d[c0 + lane] = myd;
+        fail |= piv && (!isfinite(myd) || myd == 0.0);
+        const unsigned pos = __ballot_sync(0xffffffffu, piv && myd > 0.0);
+        const unsigned neg = __ballot_sync(0xffffffffu, piv && !(myd > 0.0));
+        const unsigned prt = __ballot_sync(0xffffffffu, piv && mypf);
+        npos += __popc(pos);
+        nneg += __popc(neg);
+        pert += __popc(prt);
+      }
+      WT(4);
+      if (top) {
+        const int fu = f - k;
+        double* Us = fd.upd + sd.u_off[s];
+        if (lane >= k && lane < f) {
+#pragma unroll
+          for (int j = 0; j < kWF; ++j)
+            if (j < fu && j <= lane - k) Us[(lane - k) + static_cast<size_t>(j) * fu] = fr[j];
         }
-        if (lane == 0) {
-          fd.d[c0 + p] = dp;
-          pert += pflag;
-          if (bad) fail = 1;
-          if (dp > 0.0)
-            npos++;
-          else
-            nneg++;
+        publish(flags + s, epoch, lane);
+      } else {
+        for (int c = 0; c < fn; ++c) N[c * kFLD + lane] = 0.0;
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < kWF; ++j) {
+          if (j < f - k) {
+            const int cj = __shfl_sync(0xffffffffu, myrel, (j + k) & 31);
+            if (lane >= j + k && lane < f) N[cj * kFLD + myrel] = fr[j];
+          }
         }
         __syncwarp();
+        double* t = F;
+        F = N;
+        N = t;
+        heavy = s;
+        s = sn;
       }
-      const int fu = f - k;
-      double* Us = fd.upd + sd.u_off[s];
-      if (lane >= k && lane < f) {
-        const int i = lane - k;
-        for (int j = 0; j <= i; ++j)
-          Us[i + static_cast<size_t>(j) * fu] = F[(k + j) * kFLD + lane];
-      }
-      publish(flags + s, epoch, lane);
+      WT(5);
     }
+#ifdef NCL_WTRACE
+    if (trc && lane == 0)
+      for (int i = 0; i < 6; ++i) g_wtrace[i] = tph[i];
+#endif
   }
   fail = __any_sync(0xffffffffu, fail);
   if (lane == 0) {
@@ -141,8 +273,12 @@ k_factor_warp(SnDev sd, FactorDev fd, const double* __restrict__ kval,
 // forward solve L w = b (in place on the permuted vector w); update vectors of
 // the multifrontal solve live at uvec + rel_ptr[s] (f - k entries).  The L
 // block's column entries of a lane's row are all loaded before the
-// substitution chain, and the heavy child's update vector is kept in shared
-// memory along the path (path tops still write theirs for other readers).
+// substitution chain; the heavy child's update vector stays in shared memory
+// along the path (path tops write theirs for other readers) and the light
+// children's entries arrive as chunks with distinct destinations (ls_ent),
+// their index words loaded before the children's flags are awaited.
+constexpr int kLsR = 4;  // light-child solve chunks held in registers
+
 __global__ void __launch_bounds__(kWarpsPerCta * 32)
 k_fwd_warp(SnDev sd, const double* __restrict__ lval, double* w, double* uvec,
            int* flags, int epoch, int* counter, int npaths) {
@@ -155,12 +291,18 @@ k_fwd_warp(SnDev sd, const double* __restrict__ lval, double* w, double* uvec,
     const int pi = next_path(counter, lane);
     if (pi >= npaths) break;
     const int pb = sd.path_ptr[pi], pe = sd.path_ptr[pi + 1];
-    int heavy = -1;
+    int heavy = -1, hfu = 0;
     for (int q = pb; q < pe; ++q) {
       const int s = sd.path_nodes[q];
       const int c0 = sd.first[s], k = sd.first[s + 1] - c0, f = sd.f[s];
       const int chb = sd.ch_ptr[s], che = sd.ch_ptr[s + 1];
       const double* Lb = lval + sd.l_off[s];
+      const int lb = sd.ls_ptr[s], le = sd.ls_ptr[s + 1];
+      long long ent[kLsR];
+#pragma unroll
+      for (int t = 0; t < kLsR; ++t)
+        ent[t] = (lb + t * 32 < le) ? __ldg(sd.ls_ent + lb + t * 32 + lane) : -1;
+      const int hri = (heavy >= 0 && lane < hfu) ? __ldg(sd.rel + sd.rel_ptr[heavy] + lane) : 0;
       double lv[kWF];  // L(lane, p), p < lane
 #pragma unroll
       for (int p = 0; p < kWF; ++p)
@@ -173,13 +315,23 @@ k_fwd_warp(SnDev sd, const double* __restrict__ lval, double* w, double* uvec,
           }
       }
       __syncwarp();
+      double uv[kLsR];
+#pragma unroll
+      for (int t = 0; t < kLsR; ++t) uv[t] = ent[t] >= 0 ? __ldcg(uvec + (ent[t] & kSrcMask)) : 0.0;
       T[lane] = wv;
       __syncwarp();
-      for (int cc = chb; cc < che; ++cc) {
-        const int c = sd.ch[cc];
-        const int fu = f_minus_k(sd, c);
-        if (lane < fu)
-          T[sd.rel[sd.rel_ptr[c] + lane]] += (c == heavy) ? Hv[lane] : __ldcg(uvec + sd.rel_ptr[c] + lane);
+      if (lane < hfu) T[hri] += Hv[lane];
+      __syncwarp();
+#pragma unroll
+      for (int t = 0; t < kLsR; ++t) {
+        if (lb + t * 32 < le) {
+          if (ent[t] >= 0) T[ent[t] >> 48] += uv[t];
+          __syncwarp();
+        }
+      }
+      for (int e = lb + kLsR * 32; e < le; e += 32) {
+        const long long x = __ldg(sd.ls_ent + e + lane);
+        if (x >= 0) T[x >> 48] += __ldcg(uvec + (x & kSrcMask));
         __syncwarp();
       }
       double t = (lane < f) ? T[lane] : 0.0;
@@ -198,6 +350,7 @@ k_fwd_warp(SnDev sd, const double* __restrict__ lval, double* w, double* uvec,
         uvec[sd.rel_ptr[s] + lane - k] = t;
       if (q == pe - 1) publish(flags + s, epoch, lane);
       heavy = s;
+      hfu = f - k;
       __syncwarp();
     }
   }
@@ -206,7 +359,11 @@ k_fwd_warp(SnDev sd, const double* __restrict__ lval, double* w, double* uvec,
 // backward solve L^T x = D^-1 w, paths taken in reverse order, top-down.
 // Lane q owns pivot q and its L column (loaded up front); the rows below the
 // block enter through one shuffle-broadcast dot product per lane, then the
-// pivots resolve last-first with one shuffle + FMA each.
+// pivots resolve last-first with one shuffle + FMA each.  Along a path the
+// parent's front values (its pivots' x and the rows below it) stay in
+// registers, lane i holding front row i, and the child reads its rows below
+// through rel with a shuffle; only a path's top node reads x from memory, and
+// only nodes with light children (other paths' tops) publish a flag.
 __global__ void __launch_bounds__(kWarpsPerCta * 32)
 k_bwd_warp(SnDev sd, const double* __restrict__ lval, const double* __restrict__ d,
            const double* __restrict__ w, double* x, int* flags, int epoch,
@@ -225,6 +382,7 @@ k_bwd_warp(SnDev sd, const double* __restrict__ lval, const double* __restrict__
         }
       __syncwarp();
     }
+    double pv = 0.0;  // parent front row `lane` (previous node on the path)
     for (int q = pe - 1; q >= pb; --q) {
       const int s = sd.path_nodes[q];
       const int c0 = sd.first[s], k = sd.first[s + 1] - c0, f = sd.f[s];
@@ -233,8 +391,15 @@ k_bwd_warp(SnDev sd, const double* __restrict__ lval, const double* __restrict__
 #pragma unroll
       for (int r = 0; r < kWF; ++r)
         lc[r] = (lane < k && r > lane && r < f) ? __ldg(Lb + r + static_cast<size_t>(lane) * f) : 0.0;
-      const double xr = (lane >= k && lane < f) ? __ldcg(x + sd.rows[sd.rows_ptr[s] + lane]) : 0.0;
-      double z = (lane < k) ? w[c0 + lane] / d[c0 + lane] : 0.0;
+      double xr;
+      if (q == pe - 1) {
+        xr = (lane >= k && lane < f) ? __ldcg(x + sd.rows[sd.rows_ptr[s] + lane]) : 0.0;
+      } else {
+        const int ri = (lane >= k && lane < f) ? __ldg(sd.rel + sd.rel_ptr[s] + lane - k) : 0;
+        xr = __shfl_sync(0xffffffffu, pv, ri);
+        if (!(lane >= k && lane < f)) xr = 0.0;
+      }
+      double z = (lane < k) ? __ldcg(w + c0 + lane) / __ldg(d + c0 + lane) : 0.0;
 #pragma unroll
       for (int r = 0; r < kWF; ++r) {
         if (r >= k && r < f) {
@@ -250,7 +415,8 @@ k_bwd_warp(SnDev sd, const double* __restrict__ lval, const double* __restrict__
         }
       }
       if (lane < k) x[c0 + lane] = z;
-      publish(flags + s, epoch, lane);
+      pv = lane < k ? z : xr;
+      if (sd.ls_ptr[s + 1] > sd.ls_ptr[s]) publish(flags + s, epoch, lane);  // light children wait
     }
   }
 }
@@ -273,8 +439,23 @@ void launch_factor_warp(const SnDev& sd, const FactorDev& fd, const double* kval
                         int* flags, int epoch, int* counter, int npaths,
                         double eps, int grid, cudaStream_t st) {
   if (npaths == 0) return;
-  k_factor_warp<<<grid, kWarpsPerCta * 32, 0, st>>>(sd, fd, kval, flags, epoch,
-                                                   counter, npaths, eps);
+  static bool init = false;
+  if (!init) {
+    cudaFuncSetAttribute(k_factor_warp, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(kWarpsPerCta * kWarpFactorBytes));
+    init = true;
+  }
+  k_factor_warp<<<grid, kWarpsPerCta * 32, kWarpsPerCta * kWarpFactorBytes, st>>>(
+      sd, fd, kval, flags, epoch, counter, npaths, eps);
+#ifdef NCL_WTRACE  // diagnostic build: phase cycles of the last path's warp (NCL_NO_GRAPH=1)
+  {
+    unsigned long long t[6];
+    cudaStreamSynchronize(st);
+    cudaMemcpyFromSymbol(t, g_wtrace, sizeof(t));
+    std::fprintf(stderr, "[ncl wtrace] static %llu flags %llu A %llu light %llu factor %llu next %llu\n",
+                 t[0], t[1], t[2], t[3], t[4], t[5]);
+  }
+#endif
 }
 
 void launch_fwd_warp(const SnDev& sd, const double* lval, double* w, double* uvec,
@@ -310,8 +491,10 @@ int warp_tier_grid() {
   int dev = 0, sms = 0, per_sm = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_factor_warp,
-                                                kWarpsPerCta * 32, 0);
+  cudaFuncSetAttribute(k_factor_warp, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       static_cast<int>(kWarpsPerCta * kWarpFactorBytes));
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_factor_warp, kWarpsPerCta * 32,
+                                                kWarpsPerCta * kWarpFactorBytes);
   int a = 0, b = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, k_fwd_warp, kWarpsPerCta * 32, 0);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_bwd_warp, kWarpsPerCta * 32, 0);

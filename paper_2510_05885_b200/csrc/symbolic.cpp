@@ -554,6 +554,40 @@ bool level_is_huge(int fmax, int nfronts) {
   return fmax > kHugeFront || (fmax >= huge_min_f && nfronts <= huge_max_n);
 }
 
+// Orders extend-add entries (dst, src) into chunks of 32 with pairwise
+// distinct destinations, entries of one destination kept in their given
+// order (so the sums are deterministic); a chunk with fewer than 32
+// destinations left is padded with -1.  Destinations with the most entries
+// left go first, which keeps the chunk count at max(total / 32, deepest).
+static void chunk_entries(const std::vector<std::pair<int, long long>>& ent, std::vector<long long>& out) {
+  if (ent.empty()) return;
+  std::vector<int> dsts;
+  for (const auto& e : ent) dsts.push_back(e.first);
+  std::sort(dsts.begin(), dsts.end());
+  dsts.erase(std::unique(dsts.begin(), dsts.end()), dsts.end());
+  std::vector<std::vector<long long>> q(dsts.size());
+  for (const auto& e : ent)
+    q[std::lower_bound(dsts.begin(), dsts.end(), e.first) - dsts.begin()].push_back(e.second);
+  std::vector<size_t> head(dsts.size(), 0);
+  std::vector<int> order(dsts.size());
+  size_t left = ent.size();
+  while (left > 0) {
+    order.clear();
+    for (size_t d = 0; d < dsts.size(); ++d)
+      if (head[d] < q[d].size()) order.push_back(static_cast<int>(d));
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
+      return q[a].size() - head[a] > q[b].size() - head[b];
+    });
+    const size_t take = std::min<size_t>(order.size(), 32);
+    for (size_t t = 0; t < take; ++t) {
+      const int d = order[t];
+      out.push_back(q[d][head[d]++] | (static_cast<long long>(dsts[d]) << 48));
+      --left;
+    }
+    for (size_t t = take; t < 32; ++t) out.push_back(-1);
+  }
+}
+
 Supernodal build_supernodal(const LowerCsc& A, const Symbolic& S, int schur_n0) {
   const int n = S.n;
   Supernodal T;
@@ -791,6 +825,36 @@ Supernodal build_supernodal(const LowerCsc& A, const Symbolic& S, int schur_n0) 
     std::reverse(tmp.begin(), tmp.end());  // bottom -> top
     T.path_nodes.insert(T.path_nodes.end(), tmp.begin(), tmp.end());
     T.path_ptr.push_back(static_cast<int>(T.path_nodes.size()));
+  }
+  // light-child extend-add lists of the warp tier (ldl_kernels.cu)
+  {
+    std::vector<int> pred(static_cast<size_t>(nsn), -1);
+    for (size_t pi = 0; pi + 1 < T.path_ptr.size(); ++pi)
+      for (int q = T.path_ptr[pi] + 1; q < T.path_ptr[pi + 1]; ++q)
+        pred[T.path_nodes[q]] = T.path_nodes[q - 1];
+    T.lt_ptr.assign(static_cast<size_t>(nsn) + 1, 0);
+    T.ls_ptr.assign(static_cast<size_t>(nsn) + 1, 0);
+    std::vector<std::pair<int, long long>> et, es;
+    for (int s = 0; s < nsn; ++s) {
+      et.clear();
+      es.clear();
+      if (!T.wide[s]) {
+        for (int q = T.ch_ptr[s]; q < T.ch_ptr[s + 1]; ++q) {
+          const int c = T.ch[q];
+          if (c == pred[s]) continue;
+          const int fu = T.f[c] - (T.first[c + 1] - T.first[c]);
+          const int* rl = T.rel.data() + T.rel_ptr[c];
+          for (int j = 0; j < fu; ++j)
+            for (int i = j; i < fu; ++i)
+              et.emplace_back(rl[i] | (rl[j] << 5), T.u_off[c] + i + static_cast<long long>(j) * fu);
+          for (int i = 0; i < fu; ++i) es.emplace_back(rl[i], T.rel_ptr[c] + i);
+        }
+      }
+      chunk_entries(et, T.lt_ent);
+      chunk_entries(es, T.ls_ent);
+      T.lt_ptr[s + 1] = static_cast<int>(T.lt_ent.size());
+      T.ls_ptr[s + 1] = static_cast<int>(T.ls_ent.size());
+    }
   }
   // wide-tier levels by wide-height (children first)
   std::vector<int> wl(static_cast<size_t>(nsn), -1);

@@ -84,6 +84,13 @@ struct Supernodal {
   // warp tier: heavy paths (bottom -> top), ordered so that every light
   // child's path precedes the path it hangs from
   std::vector<int> path_ptr, path_nodes;
+  // warp tier: extend-add entries of the children that are not the node's
+  // path predecessor ("light" children), in chunks of 32 with distinct
+  // destinations: src | dst << 48, -1 = padding.  Factorization: src = upd
+  // offset, dst = row | col << 5 of the front; solves: src = update-vector
+  // offset, dst = front row.
+  std::vector<int> lt_ptr, ls_ptr;
+  std::vector<long long> lt_ent, ls_ent;
   // wide tier: level lists (level 0 = deepest wide fronts)
   std::vector<int> lvl_ptr, lvl_nodes;
   // huge-front (three-kernel) schedule: assembly tasks {front, first

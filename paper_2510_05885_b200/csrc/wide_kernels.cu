@@ -177,14 +177,6 @@ __device__ __noinline__ void assemble_col(const SnDev& sd, const FactorDev& fd,
 // into basic blocks the scheduler cannot interleave across): MUFU.RCP64H
 // seed + two Newton steps, within 1 ulp for the pivot magnitudes static
 // pivoting admits (|d| >= eps; NaN/Inf propagate and are flagged).
-__device__ __forceinline__ double rcp_nr(double d) {
-  double r;
-  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
-  double e = fma(-d, r, 1.0);
-  r = fma(r, e, r);
-  e = fma(-d, r, 1.0);
-  return fma(r, e, r);
-}
 
 // ---------------------------------------------------------------------------
 // Pivots [pb, pe) of the diagonal block with a rotation width of W registers:
