@@ -71,6 +71,48 @@ constexpr int kCB = kWF + 2;  // pivot-column broadcast buffer (x2 per warp)
 constexpr size_t kWarpFactorDoubles = 2 * kWF * kFLD + 2 * kCB;
 constexpr size_t kWarpFactorBytes = sizeof(double) * kWarpFactorDoubles;
 
+// The k pivots of a warp-tier front held as register rows (fr[j] = row
+// `lane`, column p + j while pivot p is processed: the row shifts down one
+// column per pivot, so every register index is static).  NC = register
+// columns kept live (>= f).  Pivot p's column is broadcast through shared
+// memory (cb, two alternating buffers, one warp barrier per pivot), the next
+// pivot is shuffled out as soon as its column is updated, and l = u * (1/d)
+// with the wide tier's reciprocal.  l is written to column p of the shared
+// front F, d stays in lane p (myd, perturbed flag mypf).
+template <int NC>
+__device__ __forceinline__ void warp_pivots(double (&fr)[kWF + 1], double* F, double* cb, int k, int f,
+                                            double eps, int lane, double& myd, bool& mypf, int& fail) {
+  double dnext = __shfl_sync(0xffffffffu, fr[0], 0);
+  for (int p = 0; p < k; ++p) {
+    double dp = dnext;
+    const bool pf = fabs(dp) < eps;
+    if (pf) dp = (dp >= 0.0) ? eps : -eps;
+    myd = lane == p ? dp : myd;
+    mypf = lane == p ? pf : mypf;
+    const bool mine = lane > p && lane < f;
+    const double u = fr[0];
+    double* cbp = cb + (p & 1) * kCB;
+    if (lane >= p) cbp[lane - p] = u;
+    const double r = rcp_nr(dp);
+    const double l = mine ? u * r : 0.0;
+    if (mine) F[p * kFLD + lane] = l;
+    fail |= !isfinite(l);
+    __syncwarp();
+    double2 v[NC / 2];
+    v[0].y = cbp[1];
+#pragma unroll
+    for (int j = 2; j < NC; j += 2) v[j / 2] = *reinterpret_cast<const double2*>(cbp + j);
+    fr[0] = fr[1] - l * v[0].y;
+    dnext = __shfl_sync(0xffffffffu, fr[0], (p + 1) & 31);
+#pragma unroll
+    for (int j = 2; j < NC; j += 2) {
+      fr[j - 1] = fr[j] - l * v[j / 2].x;
+      fr[j] = fr[j + 1] - l * v[j / 2].y;
+    }
+    fr[NC - 1] = 0.0;
+  }
+}
+
 __global__ void __launch_bounds__(kWarpsPerCta * 32)
 k_factor_warp(SnDev sd, FactorDev fd, const double* __restrict__ kval,
               int* flags, int epoch, int* counter, int npaths, double eps) {
@@ -84,6 +126,9 @@ k_factor_warp(SnDev sd, FactorDev fd, const double* __restrict__ kval,
     double* F = wsm + static_cast<size_t>(wid) * kWarpFactorDoubles;
     double* N = F + kWF * kFLD;
     double* cb = N + kWF * kFLD;
+    cb[lane] = 0.0;
+    cb[kCB + lane] = 0.0;
+    if (lane < 2) cb[32 + lane] = cb[kCB + 32 + lane] = 0.0;
     int s = sd.path_nodes[pb];
     {
       const int f0 = sd.f[s];
@@ -179,38 +224,12 @@ k_factor_warp(SnDev sd, FactorDev fd, const double* __restrict__ kval,
       fr[kWF] = 0.0;
       double myd = 0.0;
       bool mypf = false;
-      double dnext = __shfl_sync(0xffffffffu, fr[0], 0);
-      for (int p = 0; p < k; ++p) {
-        double dp = dnext;
-        const bool pf = fabs(dp) < eps;
-        if (pf) dp = (dp >= 0.0) ? eps : -eps;
-        if (lane == p) {
-          myd = dp;
-          mypf = pf;
-        }
-        const bool mine = lane > p && lane < f;
-        const double u = fr[0];
-        double* cbp = cb + (p & 1) * kCB;
-        if (lane >= p) cbp[lane - p] = u;
-        const double l = mine ? u * rcp_nr(dp) : 0.0;
-        if (mine) F[p * kFLD + lane] = l;
-        fail |= !isfinite(l);
-        __syncwarp();
-        fr[0] = fr[1] - l * cbp[1];
-        dnext = __shfl_sync(0xffffffffu, fr[0], (p + 1) & 31);
-        const int fmp = f - p;  // live columns p .. f-1
-#pragma unroll
-        for (int b8 = 0; b8 < kWF; b8 += 8) {
-          if (b8 < fmp) {
-#pragma unroll
-            for (int j = (b8 == 0 ? 2 : b8); j < b8 + 8; j += 2) {
-              const double2 v = *reinterpret_cast<const double2*>(cbp + j);
-              fr[j - 1] = fr[j] - l * v.x;
-              fr[j] = fr[j + 1] - l * v.y;
-            }
-          }
-        }
-      }
+      if (f <= 8)
+        warp_pivots<8>(fr, F, cb, k, f, eps, lane, myd, mypf, fail);
+      else if (f <= 16)
+        warp_pivots<16>(fr, F, cb, k, f, eps, lane, myd, mypf, fail);
+      else
+        warp_pivots<kWF>(fr, F, cb, k, f, eps, lane, myd, mypf, fail);
       __syncwarp();
       {
         double* Lb = fd.lval + sd.l_off[s];
