@@ -448,6 +448,18 @@ class LdlSystem {
     lt_ent_.upload(T.lt_ent);
     ls_ptr_.upload(T.ls_ptr);
     ls_ent_.upload(T.ls_ent);
+    {
+      std::vector<int4> pr(T.prec.size() / 4);
+      for (size_t i = 0; i < pr.size(); ++i)
+        pr[i] = make_int4(T.prec[4 * i], T.prec[4 * i + 1], T.prec[4 * i + 2], T.prec[4 * i + 3]);
+      prec_.upload(pr);
+      std::vector<longlong2> po(T.poff.size() / 2);
+      for (size_t i = 0; i < po.size(); ++i) {
+        po[i].x = T.poff[2 * i];
+        po[i].y = T.poff[2 * i + 1];
+      }
+      poff_.upload(po);
+    }
     lvl_nodes_.upload(T.lvl_nodes);
     std::vector<int8_t> wide(T.wide.begin(), T.wide.end());
     wide_.upload(wide);
@@ -629,6 +641,8 @@ class LdlSystem {
     sd_.lt_ent = lt_ent_.p;
     sd_.ls_ptr = ls_ptr_.p;
     sd_.ls_ent = ls_ent_.p;
+    sd_.prec = prec_.p;
+    sd_.poff = poff_.p;
     sd_.wide = wide_.p;
     sd_.schur = T.schur;
     grid_ = warp_tier_grid();
@@ -664,7 +678,8 @@ class LdlSystem {
   DBuf<long long> cc_ubase_, lt_ent_, ls_ent_;
   DBuf<double> dscr_;
   DBuf<int8_t> wide_;
-  DBuf<int4> asm_task_;
+  DBuf<int4> asm_task_, prec_;
+  DBuf<longlong2> poff_;
   DBuf<int4> pn_tasks_;
   DBuf<int4> tiles_, tiles_s_;
   cudaStream_t st2_ = nullptr;        // huge-level lookahead stream

@@ -36,6 +36,8 @@ struct SnDev {
   const long long* lt_ent;   //   src | dst << 48 (symbolic.hpp)
   const int* ls_ptr;         // nsn+1: light-child solve chunks
   const long long* ls_ent;
+  const int4* prec;          // 4 per path position (symbolic.hpp)
+  const longlong2* poff;     // 1 per path position: {l_off, u_off}
   const int8_t* wide;        // 1: wide-tier front (stored f x f in lval)
   int schur;                 // Schur-mode coupling supernode (assembled only), or -1
 };
@@ -57,6 +59,25 @@ __device__ __forceinline__ int ld_acquire(const int* p) {
   int v;
   asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
+}
+
+// Flag polling of the warp tier.  A relaxed load (no L1 invalidation, which
+// ld.acquire.gpu costs: CCTL.IVALL after every poll, and with it the L1 hits
+// of all static index data).  Ordering: the producer stores its data, fences
+// (__threadfence) and releases the flag; the consumer branches on the polled
+// value and only then issues its loads of the produced data, all of which
+// are L2 loads (ld.global.cg): L2 is the point of coherence and a load cannot
+// issue before the branch it follows has resolved.  flag_wait_done() keeps
+// the compiler from hoisting those loads above the poll.
+__device__ __forceinline__ int ld_relaxed(const int* p) {
+  int v;
+  asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void flag_wait_done() {
+  __syncwarp();
+  asm volatile("" ::: "memory");
 }
 
 __device__ __forceinline__ void st_release(int* p, int v) {

@@ -62,7 +62,7 @@ __device__ __forceinline__ void publish(int* flag, int epoch, int lane) {
 // before the light children's flags are awaited.  Order of the sums: heavy
 // child, A entries, light children in child order.
 #ifdef NCL_WTRACE
-__device__ unsigned long long g_wtrace[6];
+__device__ unsigned long long g_wtrace[9];
 #endif
 constexpr int kLtR = 6;   // light-child chunks held in registers
 constexpr int kLtA = 2;   // A-entry chunks held in registers
@@ -113,31 +113,67 @@ __device__ __forceinline__ void warp_pivots(double (&fr)[kWF + 1], double* F, do
   }
 }
 
+// static description of the node at one path position (symbolic.hpp prec)
+struct WRec {
+  int s, c0, k, f, chb, che, lb, le, ab, ae, relp, rowsp, lsb, lse, spar;
+  long long loff, uoff;
+};
+
+__device__ __forceinline__ WRec load_rec(const SnDev& sd, int q) {
+  const int4 a = __ldg(sd.prec + 4 * q), b = __ldg(sd.prec + 4 * q + 1);
+  const int4 c = __ldg(sd.prec + 4 * q + 2), d = __ldg(sd.prec + 4 * q + 3);
+  const longlong2 o = __ldg(sd.poff + q);
+  return WRec{a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w, c.x, c.y, c.z, c.w, d.x, d.y, d.z, o.x, o.y};
+}
+
+// the factorization's index loads for one node (no values)
+struct FIdx {
+  long long ent[kLtR];  // light-child chunks
+  int ap[kLtA], as[kLtA];  // A entries: front position, value slot
+  int chid;             // this lane's child (first 32)
+  int myrel;            // parent position of front row `lane` (rows below)
+};
+
+__device__ __forceinline__ void load_fidx(const SnDev& sd, const WRec& R, int lane, FIdx& X) {
+#pragma unroll
+  for (int t = 0; t < kLtR; ++t) X.ent[t] = (R.lb + t * 32 < R.le) ? __ldg(sd.lt_ent + R.lb + t * 32 + lane) : -1;
+#pragma unroll
+  for (int t = 0; t < kLtA; ++t) {
+    const int a = R.ab + t * 32 + lane;
+    X.ap[t] = a < R.ae ? __ldg(sd.asm_pos + a) : -1;
+    X.as[t] = a < R.ae ? __ldg(sd.asm_slot + a) : 0;
+  }
+  X.chid = R.chb + lane < R.che ? __ldg(sd.ch + R.chb + lane) : -1;
+  X.myrel = (lane >= R.k && lane < R.f) ? __ldg(sd.rel + R.relp + lane - R.k) : 0;
+}
+
 __global__ void __launch_bounds__(kWarpsPerCta * 32)
 k_factor_warp(SnDev sd, FactorDev fd, const double* __restrict__ kval,
               int* flags, int epoch, int* counter, int npaths, double eps) {
   extern __shared__ double wsm[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   int npos = 0, nneg = 0, pert = 0, fail = 0;
+  double* F = wsm + static_cast<size_t>(wid) * kWarpFactorDoubles;
+  double* N = F + kWF * kFLD;
+  double* cb = N + kWF * kFLD;
+  cb[lane] = 0.0;
+  cb[kCB + lane] = 0.0;
+  if (lane < 2) cb[32 + lane] = cb[kCB + 32 + lane] = 0.0;
   for (;;) {
     const int pi = next_path(counter, lane);
     if (pi >= npaths) break;
     const int pb = sd.path_ptr[pi], pe = sd.path_ptr[pi + 1];
-    double* F = wsm + static_cast<size_t>(wid) * kWarpFactorDoubles;
-    double* N = F + kWF * kFLD;
-    double* cb = N + kWF * kFLD;
-    cb[lane] = 0.0;
-    cb[kCB + lane] = 0.0;
-    if (lane < 2) cb[32 + lane] = cb[kCB + 32 + lane] = 0.0;
-    int s = sd.path_nodes[pb];
-    {
-      const int f0 = sd.f[s];
-      for (int c = 0; c < f0; ++c) F[c * kFLD + lane] = 0.0;
-    }
+    // software pipeline along the path: node q+1's record, index loads and
+    // light-child flags are issued while node q is factored
+    WRec R = load_rec(sd, pb);
+    FIdx X;
+    load_fidx(sd, R, lane, X);
+    int fl = X.chid >= 0 ? ld_relaxed(flags + X.chid) : epoch;
+    for (int c = 0; c < R.f; ++c) F[c * kFLD + lane] = 0.0;
     int heavy = -1;
 #ifdef NCL_WTRACE
     const bool trc = pi == npaths - 1;
-    unsigned long long tph[6] = {0, 0, 0, 0, 0, 0};
+    unsigned long long tph[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
     long long tq = clock64();
 #define WT(i)                           \
   if (trc) {                            \
@@ -149,43 +185,32 @@ k_factor_warp(SnDev sd, FactorDev fd, const double* __restrict__ kval,
 #define WT(i)
 #endif
     for (int q = pb; q < pe; ++q) {
-      const int c0 = sd.first[s], k = sd.first[s + 1] - c0, f = sd.f[s];
-      const int chb = sd.ch_ptr[s], che = sd.ch_ptr[s + 1];
-      // loads that depend on no other warp
-      const int lb = sd.lt_ptr[s], le = sd.lt_ptr[s + 1];
-      long long ent[kLtR];
-#pragma unroll
-      for (int t = 0; t < kLtR; ++t)
-        ent[t] = (lb + t * 32 < le) ? __ldg(sd.lt_ent + lb + t * 32 + lane) : -1;
-      const int ab = sd.asm_ptr[s], ae = sd.asm_ptr[s + 1];
-      double av[kLtA];
-      int ap[kLtA];
-#pragma unroll
-      for (int t = 0; t < kLtA; ++t) {
-        const int a = ab + t * 32 + lane;
-        ap[t] = a < ae ? __ldg(sd.asm_pos + a) : -1;
-        av[t] = a < ae ? __ldg(kval + __ldg(sd.asm_slot + a)) : 0.0;
-      }
       const bool top = q == pe - 1;
-      const int sn = top ? -1 : sd.path_nodes[q + 1];
-      const int fn = top ? 0 : sd.f[sn];
-      const int myrel = (!top && lane >= k && lane < f) ? __ldg(sd.rel + sd.rel_ptr[s] + lane - k) : 0;
+      const int k = R.k, f = R.f;
+      WRec Rn = R;
+      if (!top) Rn = load_rec(sd, q + 1);
+      double av[kLtA];
+#pragma unroll
+      for (int t = 0; t < kLtA; ++t) av[t] = X.ap[t] >= 0 ? __ldg(kval + X.as[t]) : 0.0;
       WT(0);
-      for (int c = chb + lane; c < che; c += 32) {
+      if (X.chid >= 0 && X.chid != heavy && fl != epoch)
+        while (ld_relaxed(flags + X.chid) != epoch) {
+        }
+      for (int c = R.chb + 32 + lane; c < R.che; c += 32) {
         const int ch = sd.ch[c];
         if (ch != heavy)
-          while (ld_acquire(flags + ch) != epoch) {
+          while (ld_relaxed(flags + ch) != epoch) {
           }
       }
-      __syncwarp();
+      flag_wait_done();
       WT(1);
       double lv[kLtR];
 #pragma unroll
-      for (int t = 0; t < kLtR; ++t) lv[t] = ent[t] >= 0 ? __ldcg(fd.upd + (ent[t] & kSrcMask)) : 0.0;
+      for (int t = 0; t < kLtR; ++t) lv[t] = X.ent[t] >= 0 ? __ldcg(fd.upd + (X.ent[t] & kSrcMask)) : 0.0;
 #pragma unroll
       for (int t = 0; t < kLtA; ++t)
-        if (ap[t] >= 0) F[(ap[t] >> 16) * kFLD + (ap[t] & 0xffff)] += av[t];
-      for (int a = ab + kLtA * 32 + lane; a < ae; a += 32) {
+        if (X.ap[t] >= 0) F[(X.ap[t] >> 16) * kFLD + (X.ap[t] & 0xffff)] += av[t];
+      for (int a = R.ab + kLtA * 32 + lane; a < R.ae; a += 32) {
         const int pos = sd.asm_pos[a];
         F[(pos >> 16) * kFLD + (pos & 0xffff)] += __ldg(kval + sd.asm_slot[a]);
       }
@@ -193,15 +218,15 @@ k_factor_warp(SnDev sd, FactorDev fd, const double* __restrict__ kval,
       WT(2);
 #pragma unroll
       for (int t = 0; t < kLtR; ++t) {
-        if (lb + t * 32 < le) {
-          if (ent[t] >= 0) {
-            const int dst = static_cast<int>(ent[t] >> 48);
+        if (R.lb + t * 32 < R.le) {
+          if (X.ent[t] >= 0) {
+            const int dst = static_cast<int>(X.ent[t] >> 48);
             F[(dst >> 5) * kFLD + (dst & 31)] += lv[t];
           }
           __syncwarp();
         }
       }
-      for (int e = lb + kLtR * 32; e < le; e += 32) {
+      for (int e = R.lb + kLtR * 32; e < R.le; e += 32) {
         const long long x = __ldg(sd.lt_ent + e + lane);
         if (x >= 0) {
           const int dst = static_cast<int>(x >> 48);
@@ -209,19 +234,16 @@ k_factor_warp(SnDev sd, FactorDev fd, const double* __restrict__ kval,
         }
         __syncwarp();
       }
-      // fr[j]: front row `lane`, column p + j while pivot p is processed
-      // (the row shifts down one column per pivot, so the pivot column is
-      // always fr[0] and every register index is static).  Pivot p's column
-      // is broadcast through shared memory (cb, two alternating buffers, one
-      // warp barrier per pivot), the next pivot is shuffled out as soon as
-      // its column is updated, and l = u * (1/d) with the wide tier's
-      // reciprocal.  l goes to the front's column p in shared memory, d to
-      // lane p; both reach global memory in bulk after the loop.
       WT(3);
       double fr[kWF + 1];
 #pragma unroll
       for (int j = 0; j < kWF; ++j) fr[j] = (j < f && lane < f) ? F[j * kFLD + lane] : 0.0;
       fr[kWF] = 0.0;
+      const int myrel = X.myrel;
+      // node q+1's index loads, in flight during the pivots
+      WT(6);
+      if (!top) load_fidx(sd, Rn, lane, X);
+      WT(7);
       double myd = 0.0;
       bool mypf = false;
       if (f <= 8)
@@ -230,13 +252,16 @@ k_factor_warp(SnDev sd, FactorDev fd, const double* __restrict__ kval,
         warp_pivots<16>(fr, F, cb, k, f, eps, lane, myd, mypf, fail);
       else
         warp_pivots<kWF>(fr, F, cb, k, f, eps, lane, myd, mypf, fail);
+      WT(8);
+      // node q+1's light-child flags (its heavy child is this node)
+      if (!top) fl = (X.chid >= 0 && X.chid != R.s) ? ld_relaxed(flags + X.chid) : epoch;
       __syncwarp();
       {
-        double* Lb = fd.lval + sd.l_off[s];
+        double* Lb = fd.lval + R.loff;
         for (int p = 0; p < k; ++p)
           if (lane > p && lane < f) Lb[lane + static_cast<size_t>(p) * f] = F[p * kFLD + lane];
         const bool piv = lane < k;
-        if (piv) fd.d[c0 + lane] = myd;
+        if (piv) fd.d[R.c0 + lane] = myd;
         fail |= piv && (!isfinite(myd) || myd == 0.0);
         const unsigned pos = __ballot_sync(0xffffffffu, piv && myd > 0.0);
         const unsigned neg = __ballot_sync(0xffffffffu, piv && !(myd > 0.0));
@@ -248,35 +273,36 @@ k_factor_warp(SnDev sd, FactorDev fd, const double* __restrict__ kval,
       WT(4);
       if (top) {
         const int fu = f - k;
-        double* Us = fd.upd + sd.u_off[s];
+        double* Us = fd.upd + R.uoff;
         if (lane >= k && lane < f) {
 #pragma unroll
           for (int j = 0; j < kWF; ++j)
             if (j < fu && j <= lane - k) Us[(lane - k) + static_cast<size_t>(j) * fu] = fr[j];
         }
-        publish(flags + s, epoch, lane);
+        publish(flags + R.s, epoch, lane);
       } else {
-        for (int c = 0; c < fn; ++c) N[c * kFLD + lane] = 0.0;
-        __syncwarp();
+        // update block -> the parent's (zeroed) shared front
+        int cj[kWF];
 #pragma unroll
-        for (int j = 0; j < kWF; ++j) {
-          if (j < f - k) {
-            const int cj = __shfl_sync(0xffffffffu, myrel, (j + k) & 31);
-            if (lane >= j + k && lane < f) N[cj * kFLD + myrel] = fr[j];
-          }
-        }
+        for (int j = 0; j < kWF; ++j) cj[j] = __shfl_sync(0xffffffffu, myrel, (j + k) & 31);
+        for (int c = 0; c < Rn.f; ++c) N[c * kFLD + lane] = 0.0;
+        __syncwarp();
+        const int fu = f - k;
+#pragma unroll
+        for (int j = 0; j < kWF; ++j)
+          if (j < fu && lane >= j + k && lane < f) N[cj[j] * kFLD + myrel] = fr[j];
         __syncwarp();
         double* t = F;
         F = N;
         N = t;
-        heavy = s;
-        s = sn;
+        heavy = R.s;
+        R = Rn;
       }
       WT(5);
     }
 #ifdef NCL_WTRACE
     if (trc && lane == 0)
-      for (int i = 0; i < 6; ++i) g_wtrace[i] = tph[i];
+      for (int i = 0; i < 9; ++i) g_wtrace[i] = tph[i];
 #endif
   }
   fail = __any_sync(0xffffffffu, fail);
@@ -310,30 +336,41 @@ k_fwd_warp(SnDev sd, const double* __restrict__ lval, double* w, double* uvec,
     const int pi = next_path(counter, lane);
     if (pi >= npaths) break;
     const int pb = sd.path_ptr[pi], pe = sd.path_ptr[pi + 1];
-    int heavy = -1, hfu = 0;
-    for (int q = pb; q < pe; ++q) {
-      const int s = sd.path_nodes[q];
-      const int c0 = sd.first[s], k = sd.first[s + 1] - c0, f = sd.f[s];
-      const int chb = sd.ch_ptr[s], che = sd.ch_ptr[s + 1];
-      const double* Lb = lval + sd.l_off[s];
-      const int lb = sd.ls_ptr[s], le = sd.ls_ptr[s + 1];
-      long long ent[kLsR];
-#pragma unroll
-      for (int t = 0; t < kLsR; ++t)
-        ent[t] = (lb + t * 32 < le) ? __ldg(sd.ls_ent + lb + t * 32 + lane) : -1;
-      const int hri = (heavy >= 0 && lane < hfu) ? __ldg(sd.rel + sd.rel_ptr[heavy] + lane) : 0;
-      double lv[kWF];  // L(lane, p), p < lane
+    // software pipeline: node q+1's record, L block, rhs and index words are
+    // loaded while node q is substituted
+    WRec R = load_rec(sd, pb);
+    double lv[kWF];  // L(lane, p), p < lane
+    double wv;
+    long long ent[kLsR];
+    int chid;
+    auto load_node = [&](const WRec& Q) {
+      const double* Lb = lval + Q.loff;
 #pragma unroll
       for (int p = 0; p < kWF; ++p)
-        lv[p] = (p < k && lane > p && lane < f) ? __ldg(Lb + lane + static_cast<size_t>(p) * f) : 0.0;
-      const double wv = (lane < k) ? __ldcg(w + c0 + lane) : 0.0;
-      for (int c = chb + lane; c < che; c += 32) {
+        lv[p] = (p < Q.k && lane > p && lane < Q.f) ? __ldg(Lb + lane + static_cast<size_t>(p) * Q.f) : 0.0;
+      wv = (lane < Q.k) ? __ldcg(w + Q.c0 + lane) : 0.0;
+#pragma unroll
+      for (int t = 0; t < kLsR; ++t)
+        ent[t] = (Q.lsb + t * 32 < Q.lse) ? __ldg(sd.ls_ent + Q.lsb + t * 32 + lane) : -1;
+      chid = Q.chb + lane < Q.che ? __ldg(sd.ch + Q.chb + lane) : -1;
+    };
+    load_node(R);
+    int heavy = -1, hfu = 0, hri = 0;
+    for (int q = pb; q < pe; ++q) {
+      const bool top = q == pe - 1;
+      const int k = R.k, f = R.f;
+      WRec Rn = R;
+      if (!top) Rn = load_rec(sd, q + 1);
+      if (chid >= 0 && chid != heavy)
+        while (ld_relaxed(flags + chid) != epoch) {
+        }
+      for (int c = R.chb + 32 + lane; c < R.che; c += 32) {
         const int ch = sd.ch[c];
         if (ch != heavy)
-          while (ld_acquire(flags + ch) != epoch) {
+          while (ld_relaxed(flags + ch) != epoch) {
           }
       }
-      __syncwarp();
+      flag_wait_done();
       double uv[kLsR];
 #pragma unroll
       for (int t = 0; t < kLsR; ++t) uv[t] = ent[t] >= 0 ? __ldcg(uvec + (ent[t] & kSrcMask)) : 0.0;
@@ -343,12 +380,12 @@ k_fwd_warp(SnDev sd, const double* __restrict__ lval, double* w, double* uvec,
       __syncwarp();
 #pragma unroll
       for (int t = 0; t < kLsR; ++t) {
-        if (lb + t * 32 < le) {
+        if (R.lsb + t * 32 < R.lse) {
           if (ent[t] >= 0) T[ent[t] >> 48] += uv[t];
           __syncwarp();
         }
       }
-      for (int e = lb + kLsR * 32; e < le; e += 32) {
+      for (int e = R.lsb + kLsR * 32; e < R.lse; e += 32) {
         const long long x = __ldg(sd.ls_ent + e + lane);
         if (x >= 0) T[x >> 48] += __ldcg(uvec + (x & kSrcMask));
         __syncwarp();
@@ -361,28 +398,33 @@ k_fwd_warp(SnDev sd, const double* __restrict__ lval, double* w, double* uvec,
           t -= lv[p] * wp;
         }
       }
+      const int hri_n = (!top && lane < f - k) ? __ldg(sd.rel + R.relp + lane) : 0;
+      if (!top) load_node(Rn);
       __syncwarp();
       if (lane >= k && lane < f) Hv[lane - k] = t;
       if (lane < k)
-        w[c0 + lane] = t;
-      else if (lane < f && q == pe - 1)
-        uvec[sd.rel_ptr[s] + lane - k] = t;
-      if (q == pe - 1) publish(flags + s, epoch, lane);
-      heavy = s;
+        w[R.c0 + lane] = t;
+      else if (lane < f && top)
+        uvec[R.relp + lane - k] = t;
+      if (top) publish(flags + R.s, epoch, lane);
+      heavy = R.s;
       hfu = f - k;
+      hri = hri_n;
+      R = Rn;
       __syncwarp();
     }
   }
 }
 
 // backward solve L^T x = D^-1 w, paths taken in reverse order, top-down.
-// Lane q owns pivot q and its L column (loaded up front); the rows below the
-// block enter through one shuffle-broadcast dot product per lane, then the
-// pivots resolve last-first with one shuffle + FMA each.  Along a path the
-// parent's front values (its pivots' x and the rows below it) stay in
-// registers, lane i holding front row i, and the child reads its rows below
-// through rel with a shuffle; only a path's top node reads x from memory, and
-// only nodes with light children (other paths' tops) publish a flag.
+// Lane q owns pivot q and its L column; the rows below the block enter
+// through one shuffle-broadcast dot product per lane, then the pivots
+// resolve last-first with one shuffle + FMA each.  Along a path the parent's
+// front values (its pivots' x and the rows below it) stay in registers, lane
+// i holding front row i, and the child reads its rows below through rel with
+// a shuffle; only a path's top node reads x from memory, and only nodes with
+// light children (other paths' tops) publish a flag.  Node q-1's record, L
+// columns, w, d and rel are loaded while node q is solved.
 __global__ void __launch_bounds__(kWarpsPerCta * 32)
 k_bwd_warp(SnDev sd, const double* __restrict__ lval, const double* __restrict__ d,
            const double* __restrict__ w, double* x, int* flags, int epoch,
@@ -393,32 +435,32 @@ k_bwd_warp(SnDev sd, const double* __restrict__ lval, const double* __restrict__
     if (pj >= npaths) break;
     const int pi = npaths - 1 - pj;
     const int pb = sd.path_ptr[pi], pe = sd.path_ptr[pi + 1];
-    {
-      const int top = sd.path_nodes[pe - 1];
-      const int par = sd.sparent[top];
-      if (par >= 0 && !wide[par] && lane == 0)
-        while (ld_acquire(flags + par) != epoch) {
-        }
-      __syncwarp();
-    }
-    double pv = 0.0;  // parent front row `lane` (previous node on the path)
-    for (int q = pe - 1; q >= pb; --q) {
-      const int s = sd.path_nodes[q];
-      const int c0 = sd.first[s], k = sd.first[s + 1] - c0, f = sd.f[s];
-      const double* Lb = lval + sd.l_off[s];
-      double lc[kWF];  // L(r, lane), r > lane
+    WRec R = load_rec(sd, pe - 1);
+    double lc[kWF];  // L(r, lane), r > lane
+    double wd;       // w / d of pivot `lane`
+    auto load_node = [&](const WRec& Q) {
+      const double* Lb = lval + Q.loff;
 #pragma unroll
       for (int r = 0; r < kWF; ++r)
-        lc[r] = (lane < k && r > lane && r < f) ? __ldg(Lb + r + static_cast<size_t>(lane) * f) : 0.0;
-      double xr;
-      if (q == pe - 1) {
-        xr = (lane >= k && lane < f) ? __ldcg(x + sd.rows[sd.rows_ptr[s] + lane]) : 0.0;
-      } else {
-        const int ri = (lane >= k && lane < f) ? __ldg(sd.rel + sd.rel_ptr[s] + lane - k) : 0;
-        xr = __shfl_sync(0xffffffffu, pv, ri);
-        if (!(lane >= k && lane < f)) xr = 0.0;
-      }
-      double z = (lane < k) ? __ldcg(w + c0 + lane) / __ldg(d + c0 + lane) : 0.0;
+        lc[r] = (lane < Q.k && r > lane && r < Q.f) ? __ldg(Lb + r + static_cast<size_t>(lane) * Q.f) : 0.0;
+      wd = (lane < Q.k) ? __ldcg(w + Q.c0 + lane) / __ldg(d + Q.c0 + lane) : 0.0;
+    };
+    load_node(R);
+    double xr;
+    {
+      const int par = R.spar;
+      const int row = (lane >= R.k && lane < R.f) ? __ldg(sd.rows + R.rowsp + lane) : 0;
+      if (par >= 0 && !wide[par] && lane == 0)
+        while (ld_relaxed(flags + par) != epoch) {
+        }
+      flag_wait_done();
+      xr = (lane >= R.k && lane < R.f) ? __ldcg(x + row) : 0.0;
+    }
+    for (int q = pe - 1; q >= pb; --q) {
+      const int k = R.k, f = R.f;
+      WRec Rn = R;
+      if (q > pb) Rn = load_rec(sd, q - 1);
+      double z = wd;
 #pragma unroll
       for (int r = 0; r < kWF; ++r) {
         if (r >= k && r < f) {
@@ -426,6 +468,8 @@ k_bwd_warp(SnDev sd, const double* __restrict__ lval, const double* __restrict__
           z -= lc[r] * xv;
         }
       }
+      // the next (child) node's rows below as positions in this front
+      const int myrel = (q > pb && lane >= Rn.k && lane < Rn.f) ? __ldg(sd.rel + Rn.relp + lane - Rn.k) : 0;
 #pragma unroll
       for (int p = kWF - 1; p >= 0; --p) {
         if (p < k) {
@@ -433,9 +477,15 @@ k_bwd_warp(SnDev sd, const double* __restrict__ lval, const double* __restrict__
           if (lane < p) z -= lc[p] * xp;
         }
       }
-      if (lane < k) x[c0 + lane] = z;
-      pv = lane < k ? z : xr;
-      if (sd.ls_ptr[s + 1] > sd.ls_ptr[s]) publish(flags + s, epoch, lane);  // light children wait
+      if (lane < k) x[R.c0 + lane] = z;
+      const double pv = lane < k ? z : xr;  // this front's row `lane`
+      if (R.lse > R.lsb) publish(flags + R.s, epoch, lane);  // light children wait
+      if (q > pb) {
+        load_node(Rn);
+        xr = __shfl_sync(0xffffffffu, pv, myrel);
+        if (!(lane >= Rn.k && lane < Rn.f)) xr = 0.0;
+      }
+      R = Rn;
     }
   }
 }
@@ -468,11 +518,13 @@ void launch_factor_warp(const SnDev& sd, const FactorDev& fd, const double* kval
       sd, fd, kval, flags, epoch, counter, npaths, eps);
 #ifdef NCL_WTRACE  // diagnostic build: phase cycles of the last path's warp (NCL_NO_GRAPH=1)
   {
-    unsigned long long t[6];
+    unsigned long long t[9];
     cudaStreamSynchronize(st);
     cudaMemcpyFromSymbol(t, g_wtrace, sizeof(t));
-    std::fprintf(stderr, "[ncl wtrace] static %llu flags %llu A %llu light %llu factor %llu next %llu\n",
-                 t[0], t[1], t[2], t[3], t[4], t[5]);
+    std::fprintf(stderr,
+                 "[ncl wtrace] static %llu flags %llu A %llu light %llu fr %llu fidx %llu pivots %llu "
+                 "flags+stores %llu next %llu\n",
+                 t[0], t[1], t[2], t[3], t[6], t[7], t[8], t[4], t[5]);
   }
 #endif
 }

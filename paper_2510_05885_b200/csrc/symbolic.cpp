@@ -856,6 +856,19 @@ Supernodal build_supernodal(const LowerCsc& A, const Symbolic& S, int schur_n0) 
       T.ls_ptr[s + 1] = static_cast<int>(T.ls_ent.size());
     }
   }
+  // per-path-position records of the warp tier
+  T.prec.assign(T.path_nodes.size() * 16, 0);
+  T.poff.assign(T.path_nodes.size() * 2, 0);
+  for (size_t q = 0; q < T.path_nodes.size(); ++q) {
+    const int s = T.path_nodes[q];
+    const int r[16] = {s, T.first[s], T.first[s + 1] - T.first[s], T.f[s],
+                       T.ch_ptr[s], T.ch_ptr[s + 1], T.lt_ptr[s], T.lt_ptr[s + 1],
+                       T.asm_ptr[s], T.asm_ptr[s + 1], T.rel_ptr[s], T.rows_ptr[s],
+                       T.ls_ptr[s], T.ls_ptr[s + 1], T.sparent[s], 0};
+    std::copy(r, r + 16, T.prec.begin() + 16 * q);
+    T.poff[2 * q] = T.l_off[s];
+    T.poff[2 * q + 1] = T.u_off[s];
+  }
   // wide-tier levels by wide-height (children first)
   std::vector<int> wl(static_cast<size_t>(nsn), -1);
   int nlev = 0;

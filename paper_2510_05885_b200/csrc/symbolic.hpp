@@ -91,6 +91,13 @@ struct Supernodal {
   // offset, dst = front row.
   std::vector<int> lt_ptr, ls_ptr;
   std::vector<long long> lt_ent, ls_ent;
+  // warp tier: one record per path position q (path_nodes order) so a warp
+  // reaches everything static about its next node with one dependent load:
+  // prec[4q..4q+3] = {s, first, k, f}, {ch_b, ch_e, lt_b, lt_e},
+  // {asm_b, asm_e, rel_ptr, rows_ptr}, {ls_b, ls_e, sparent, 0};
+  // poff[2q..2q+1] = {l_off, u_off}
+  std::vector<int> prec;
+  std::vector<long long> poff;
   // wide tier: level lists (level 0 = deepest wide fronts)
   std::vector<int> lvl_ptr, lvl_nodes;
   // huge-front (three-kernel) schedule: assembly tasks {front, first
