@@ -230,7 +230,7 @@ class LdlSystem {
     if (npaths()) {
       CK(cudaMemsetAsync(counter_.p, 0, sizeof(int), st_));
       CK(cudaMemsetAsync(flags_.p, 0, sizeof(int) * flags_.n, st_));
-      launch_fwd_warp(sd_, lval_.p, wp_.p, uvec_.p, flags_.p, 2, counter_.p, npaths(), grid_, st_);
+      launch_fwd_warp(sd_, lval_.p, wp_.p, uvec_.p, flags_.p, 2, counter_.p, npaths(), sgrid_, st_);
     }
     for (int l = 0; l < nlevels(); ++l) {
       if (lvl_fmax_[l] <= small_solve_limit()) {
@@ -264,7 +264,7 @@ class LdlSystem {
     if (npaths()) {
       CK(cudaMemsetAsync(counter_.p, 0, sizeof(int), st_));
       launch_bwd_warp(sd_, lval_.p, d_.p, wp_.p, xp_.p, flags_.p, 3, wide_.p, counter_.p,
-                      npaths(), grid_, st_);
+                      npaths(), sgrid_, st_);
     }
     launch_permute_out(N_, perm_.p, xp_.p, x, st_);
     launches_ += 1 + (npaths() > 0 ? 1 : 0) + nlevels();
@@ -645,7 +645,8 @@ class LdlSystem {
     sd_.poff = poff_.p;
     sd_.wide = wide_.p;
     sd_.schur = T.schur;
-    grid_ = warp_tier_grid();
+    grid_ = warp_tier_grid(false);
+    sgrid_ = warp_tier_grid(true);
     CK(cudaStreamSynchronize(st_));
   }
 
@@ -654,7 +655,7 @@ class LdlSystem {
   Supernodal sn_;
   cudaStream_t st_;
   int N_ = 0;
-  int grid_ = 1;
+  int grid_ = 1, sgrid_ = 1;  // warp-tier factor / solve grids (resident CTAs)
   int epoch_ = 1;  // the factorization uses epoch 1, solves 2, 3, ...
   bool use_graph_ = std::getenv("NCL_NO_GRAPH") == nullptr;
   int nfact_ = 0;

@@ -65,7 +65,7 @@ void launch_permute_in(int n, const int* perm, const double* b, double* w,
                        cudaStream_t st);
 void launch_permute_out(int n, const int* perm, const double* xp, double* x,
                         cudaStream_t st);
-int warp_tier_grid();
+int warp_tier_grid(bool solves);  // resident CTAs of the factor / solve kernels
 
 // kkt_kernels.cu
 void launch_assemble(const AsmDev& a, int form, int m, int m_eq, int nt,

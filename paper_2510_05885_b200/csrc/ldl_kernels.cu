@@ -558,19 +558,21 @@ void launch_permute_out(int n, const int* perm, const double* xp, double* x,
   k_permute_out<<<(n + 255) / 256, 256, 0, st>>>(n, perm, xp, x);
 }
 
-int warp_tier_grid() {
+int warp_tier_grid(bool solves) {
   int dev = 0, sms = 0, per_sm = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaFuncSetAttribute(k_factor_warp, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       static_cast<int>(kWarpsPerCta * kWarpFactorBytes));
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_factor_warp, kWarpsPerCta * 32,
-                                                kWarpsPerCta * kWarpFactorBytes);
-  int a = 0, b = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, k_fwd_warp, kWarpsPerCta * 32, 0);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_bwd_warp, kWarpsPerCta * 32, 0);
-  per_sm = per_sm < a ? per_sm : a;
-  per_sm = per_sm < b ? per_sm : b;
+  if (solves) {
+    int a = 0, b = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, k_fwd_warp, kWarpsPerCta * 32, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_bwd_warp, kWarpsPerCta * 32, 0);
+    per_sm = a < b ? a : b;
+  } else {
+    cudaFuncSetAttribute(k_factor_warp, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(kWarpsPerCta * kWarpFactorBytes));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_factor_warp, kWarpsPerCta * 32,
+                                                  kWarpsPerCta * kWarpFactorBytes);
+  }
   if (per_sm < 1) per_sm = 1;
   return sms * per_sm;
 }
