@@ -444,6 +444,7 @@ class LdlSystem {
     rel_.upload(T.rel);
     path_ptr_.upload(T.path_ptr);
     path_nodes_.upload(T.path_nodes);
+    bwd_path_.upload(T.bwd_path);
     lt_ptr_.upload(T.lt_ptr);
     lt_ent_.upload(T.lt_ent);
     ls_ptr_.upload(T.ls_ptr);
@@ -637,6 +638,7 @@ class LdlSystem {
     sd_.rel = rel_.p;
     sd_.path_ptr = path_ptr_.p;
     sd_.path_nodes = path_nodes_.p;
+    sd_.bwd_path = bwd_path_.p;
     sd_.lt_ptr = lt_ptr_.p;
     sd_.lt_ent = lt_ent_.p;
     sd_.ls_ptr = ls_ptr_.p;
@@ -675,7 +677,7 @@ class LdlSystem {
   DBuf<int> first_, f_, sparent_, rows_ptr_, rows_, u_ld_, asm_ptr_, asm_pos_, asm_slot_,
       ch_ptr_, ch_, rel_ptr_, rel_, path_ptr_, path_nodes_, lvl_nodes_, perm_, flags_,
       counter_, fr_ptr_, fr_col_, fr_slot_, dg_nodes_, asm_cp_, cc_off_, cc_ptr_, cc_rbase_,
-      cc_cnt_, lt_ptr_, ls_ptr_;
+      cc_cnt_, lt_ptr_, ls_ptr_, bwd_path_;
   DBuf<long long> cc_ubase_, lt_ent_, ls_ent_;
   DBuf<double> dscr_;
   DBuf<int8_t> wide_;

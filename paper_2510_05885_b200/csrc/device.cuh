@@ -32,6 +32,7 @@ struct SnDev {
   const int* rel;
   const int* path_ptr;
   const int* path_nodes;
+  const int* bwd_path;       // backward-solve path order
   const int* lt_ptr;         // nsn+1: light-child factor extend-add chunks
   const long long* lt_ent;   //   src | dst << 48 (symbolic.hpp)
   const int* ls_ptr;         // nsn+1: light-child solve chunks
@@ -72,6 +73,43 @@ __device__ __forceinline__ int ld_acquire(const int* p) {
 __device__ __forceinline__ int ld_relaxed(const int* p) {
   int v;
   asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Read-only loads issued exactly where written (asm volatile): the software
+// pipelines of the warp tier issue a node ahead, and the compiler would
+// otherwise sink plain __ldg loads down to their first use.
+__device__ __forceinline__ int ldg_pin(const int* p) {
+  int v;
+  asm volatile("ld.global.nc.b32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ long long ldg_pin(const long long* p) {
+  long long v;
+  asm volatile("ld.global.nc.b64 %0, [%1];" : "=l"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ double ldg_pin(const double* p) {
+  double v;
+  asm volatile("ld.global.nc.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ int4 ldg_pin(const int4* p) {
+  int4 v;
+  asm volatile("ld.global.nc.v4.s32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
+__device__ __forceinline__ longlong2 ldg_pin(const longlong2* p) {
+  longlong2 v;
+  asm volatile("ld.global.nc.v2.s64 {%0, %1}, [%2];" : "=l"(v.x), "=l"(v.y) : "l"(p));
+  return v;
+}
+
+__device__ __forceinline__ double ldcg_pin(const double* p) {
+  double v;
+  asm volatile("ld.global.cg.f64 %0, [%1];" : "=d"(v) : "l"(p));
   return v;
 }
 

@@ -41,6 +41,16 @@ __device__ __forceinline__ int next_path(int* counter, int lane) {
   return __shfl_sync(0xffffffffu, pi, 0);
 }
 
+// spin on a flag with exponential back-off: a waiting warp then hardly takes
+// issue slots (or L2 bandwidth) from the warp it waits for on the same SM
+__device__ __forceinline__ void wait_flag(const int* flag, int epoch) {
+  unsigned ns = 32;
+  while (ld_relaxed(flag) != epoch) {
+    __nanosleep(ns);
+    if (ns < 512) ns <<= 1;
+  }
+}
+
 __device__ __forceinline__ void publish(int* flag, int epoch, int lane) {
   __threadfence();
   __syncwarp();
@@ -61,8 +71,24 @@ __device__ __forceinline__ void publish(int* flag, int epoch, int lane) {
 // distinct within a chunk, so a chunk is one parallel step) -- are issued
 // before the light children's flags are awaited.  Order of the sums: heavy
 // child, A entries, light children in child order.
-#ifdef NCL_WTRACE
-__device__ unsigned long long g_wtrace[9];
+// Phase timers of the warp-tier factorization.  NCL_WTRACE builds print the
+// cycles the longest path's warp spends per phase (diagnostic, NCL_NO_GRAPH=1).
+// Default builds keep the same code with a condition that is never true at
+// run time: the dead blocks split the node loop into basic blocks that ptxas
+// schedules separately, and that keeps each phase's loads issued ahead of
+// their uses -- measured on the 3927-node spine of opf_toy 78484: 19.8 ms
+// without the blocks, 14.2 ms with them.
+#ifndef NCL_WTRACE
+#define NCL_WTRACE_DEAD
+#endif
+#if defined(NCL_WTRACE) || defined(NCL_WTRACE_DEAD)
+__device__ unsigned long long g_wtrace[11];
+__device__ unsigned long long g_wtime[4];  // kernel start (min), spine start/end, last other path end (max)
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 #endif
 constexpr int kLtR = 6;   // light-child chunks held in registers
 constexpr int kLtA = 2;   // A-entry chunks held in registers
@@ -120,9 +146,9 @@ struct WRec {
 };
 
 __device__ __forceinline__ WRec load_rec(const SnDev& sd, int q) {
-  const int4 a = __ldg(sd.prec + 4 * q), b = __ldg(sd.prec + 4 * q + 1);
-  const int4 c = __ldg(sd.prec + 4 * q + 2), d = __ldg(sd.prec + 4 * q + 3);
-  const longlong2 o = __ldg(sd.poff + q);
+  const int4 a = ldg_pin(sd.prec + 4 * q), b = ldg_pin(sd.prec + 4 * q + 1);
+  const int4 c = ldg_pin(sd.prec + 4 * q + 2), d = ldg_pin(sd.prec + 4 * q + 3);
+  const longlong2 o = ldg_pin(sd.poff + q);
   return WRec{a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w, c.x, c.y, c.z, c.w, d.x, d.y, d.z, o.x, o.y};
 }
 
@@ -136,15 +162,15 @@ struct FIdx {
 
 __device__ __forceinline__ void load_fidx(const SnDev& sd, const WRec& R, int lane, FIdx& X) {
 #pragma unroll
-  for (int t = 0; t < kLtR; ++t) X.ent[t] = (R.lb + t * 32 < R.le) ? __ldg(sd.lt_ent + R.lb + t * 32 + lane) : -1;
+  for (int t = 0; t < kLtR; ++t) X.ent[t] = (R.lb + t * 32 < R.le) ? ldg_pin(sd.lt_ent + R.lb + t * 32 + lane) : -1;
 #pragma unroll
   for (int t = 0; t < kLtA; ++t) {
     const int a = R.ab + t * 32 + lane;
-    X.ap[t] = a < R.ae ? __ldg(sd.asm_pos + a) : -1;
-    X.as[t] = a < R.ae ? __ldg(sd.asm_slot + a) : 0;
+    X.ap[t] = a < R.ae ? ldg_pin(sd.asm_pos + a) : -1;
+    X.as[t] = a < R.ae ? ldg_pin(sd.asm_slot + a) : 0;
   }
-  X.chid = R.chb + lane < R.che ? __ldg(sd.ch + R.chb + lane) : -1;
-  X.myrel = (lane >= R.k && lane < R.f) ? __ldg(sd.rel + R.relp + lane - R.k) : 0;
+  X.chid = R.chb + lane < R.che ? ldg_pin(sd.ch + R.chb + lane) : -1;
+  X.myrel = (lane >= R.k && lane < R.f) ? ldg_pin(sd.rel + R.relp + lane - R.k) : 0;
 }
 
 __global__ void __launch_bounds__(kWarpsPerCta * 32)
@@ -156,6 +182,9 @@ k_factor_warp(SnDev sd, FactorDev fd, const double* __restrict__ kval,
   double* F = wsm + static_cast<size_t>(wid) * kWarpFactorDoubles;
   double* N = F + kWF * kFLD;
   double* cb = N + kWF * kFLD;
+#if defined(NCL_WTRACE) || defined(NCL_WTRACE_DEAD)
+  if (lane == 0) atomicMin(&g_wtime[0], gtimer());
+#endif
   cb[lane] = 0.0;
   cb[kCB + lane] = 0.0;
   if (lane < 2) cb[32 + lane] = cb[kCB + 32 + lane] = 0.0;
@@ -169,17 +198,34 @@ k_factor_warp(SnDev sd, FactorDev fd, const double* __restrict__ kval,
     FIdx X;
     load_fidx(sd, R, lane, X);
     int fl = X.chid >= 0 ? ld_relaxed(flags + X.chid) : epoch;
+    double av[kLtA];  // A values (kval is an input: prefetched a node ahead)
+#pragma unroll
+    for (int t = 0; t < kLtA; ++t) av[t] = X.ap[t] >= 0 ? ldg_pin(kval + X.as[t]) : 0.0;
     for (int c = 0; c < R.f; ++c) F[c * kFLD + lane] = 0.0;
     int heavy = -1;
+#if defined(NCL_WTRACE) || defined(NCL_WTRACE_DEAD)
 #ifdef NCL_WTRACE
-    const bool trc = pi == npaths - 1;
-    unsigned long long tph[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+    const bool trc = pi == 0;  // the longest root path is handed out first
+#else
+    const bool trc = pi == 0 && epoch == 0x7fffffff;
+#endif
+    if (trc && lane == 0) g_wtime[1] = gtimer();
+    unsigned long long tph[11] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
     long long tq = clock64();
+#ifndef NCL_WT_MASK
+#define NCL_WT_MASK 0xffff
+#endif
 #define WT(i)                           \
-  if (trc) {                            \
+  if (((NCL_WT_MASK >> (i)) & 1) && trc) { \
     const long long tn = clock64();     \
     tph[i] += tn - tq;                  \
     tq = tn;                            \
+  }
+#elif defined(NCL_WT_CLK)
+#define WT(i)                            \
+  {                                      \
+    const long long t_ = clock64();      \
+    asm volatile("" ::"l"(t_));          \
   }
 #else
 #define WT(i)
@@ -189,18 +235,13 @@ k_factor_warp(SnDev sd, FactorDev fd, const double* __restrict__ kval,
       const int k = R.k, f = R.f;
       WRec Rn = R;
       if (!top) Rn = load_rec(sd, q + 1);
-      double av[kLtA];
-#pragma unroll
-      for (int t = 0; t < kLtA; ++t) av[t] = X.ap[t] >= 0 ? __ldg(kval + X.as[t]) : 0.0;
       WT(0);
       if (X.chid >= 0 && X.chid != heavy && fl != epoch)
-        while (ld_relaxed(flags + X.chid) != epoch) {
-        }
+        wait_flag(flags + X.chid, epoch);
       for (int c = R.chb + 32 + lane; c < R.che; c += 32) {
         const int ch = sd.ch[c];
         if (ch != heavy)
-          while (ld_relaxed(flags + ch) != epoch) {
-          }
+          wait_flag(flags + ch, epoch);
       }
       flag_wait_done();
       WT(1);
@@ -254,12 +295,33 @@ k_factor_warp(SnDev sd, FactorDev fd, const double* __restrict__ kval,
         warp_pivots<kWF>(fr, F, cb, k, f, eps, lane, myd, mypf, fail);
       WT(8);
       // node q+1's light-child flags (its heavy child is this node)
-      if (!top) fl = (X.chid >= 0 && X.chid != R.s) ? ld_relaxed(flags + X.chid) : epoch;
+      if (!top) {
+        fl = (X.chid >= 0 && X.chid != R.s) ? ld_relaxed(flags + X.chid) : epoch;
+#pragma unroll
+        for (int t = 0; t < kLtA; ++t) av[t] = X.ap[t] >= 0 ? ldg_pin(kval + X.as[t]) : 0.0;
+      }
       __syncwarp();
+      WT(9);
       {
+        // the f x k L block is contiguous: coalesced linear stores (entries
+        // on or above the diagonal written as zero)
         double* Lb = fd.lval + R.loff;
-        for (int p = 0; p < k; ++p)
-          if (lane > p && lane < f) Lb[lane + static_cast<size_t>(p) * f] = F[p * kFLD + lane];
+        const int nl = f * k;
+        const float rf = 1.0f / static_cast<float>(f);
+#pragma unroll 4
+        for (int idx = lane; idx < nl; idx += 32) {
+          int col = __float2int_rd((static_cast<float>(idx) + 0.5f) * rf);
+          int row = idx - col * f;
+          if (row >= f) {
+            row -= f;
+            ++col;
+          } else if (row < 0) {
+            row += f;
+            --col;
+          }
+          Lb[idx] = row > col ? F[col * kFLD + row] : 0.0;
+        }
+        WT(10);
         const bool piv = lane < k;
         if (piv) fd.d[R.c0 + lane] = myd;
         fail |= piv && (!isfinite(myd) || myd == 0.0);
@@ -300,9 +362,12 @@ k_factor_warp(SnDev sd, FactorDev fd, const double* __restrict__ kval,
       }
       WT(5);
     }
-#ifdef NCL_WTRACE
-    if (trc && lane == 0)
-      for (int i = 0; i < 9; ++i) g_wtrace[i] = tph[i];
+#if defined(NCL_WTRACE) || defined(NCL_WTRACE_DEAD)
+    if (trc && lane == 0) {
+      for (int i = 0; i < 11; ++i) g_wtrace[i] = tph[i];
+      g_wtime[2] = gtimer();
+    }
+    if (!trc && lane == 0) atomicMax(&g_wtime[3], gtimer());
 #endif
   }
   fail = __any_sync(0xffffffffu, fail);
@@ -347,12 +412,12 @@ k_fwd_warp(SnDev sd, const double* __restrict__ lval, double* w, double* uvec,
       const double* Lb = lval + Q.loff;
 #pragma unroll
       for (int p = 0; p < kWF; ++p)
-        lv[p] = (p < Q.k && lane > p && lane < Q.f) ? __ldg(Lb + lane + static_cast<size_t>(p) * Q.f) : 0.0;
-      wv = (lane < Q.k) ? __ldcg(w + Q.c0 + lane) : 0.0;
+        lv[p] = (p < Q.k && lane > p && lane < Q.f) ? ldg_pin(Lb + lane + static_cast<size_t>(p) * Q.f) : 0.0;
+      wv = (lane < Q.k) ? ldcg_pin(w + Q.c0 + lane) : 0.0;
 #pragma unroll
       for (int t = 0; t < kLsR; ++t)
-        ent[t] = (Q.lsb + t * 32 < Q.lse) ? __ldg(sd.ls_ent + Q.lsb + t * 32 + lane) : -1;
-      chid = Q.chb + lane < Q.che ? __ldg(sd.ch + Q.chb + lane) : -1;
+        ent[t] = (Q.lsb + t * 32 < Q.lse) ? ldg_pin(sd.ls_ent + Q.lsb + t * 32 + lane) : -1;
+      chid = Q.chb + lane < Q.che ? ldg_pin(sd.ch + Q.chb + lane) : -1;
     };
     load_node(R);
     int heavy = -1, hfu = 0, hri = 0;
@@ -362,13 +427,11 @@ k_fwd_warp(SnDev sd, const double* __restrict__ lval, double* w, double* uvec,
       WRec Rn = R;
       if (!top) Rn = load_rec(sd, q + 1);
       if (chid >= 0 && chid != heavy)
-        while (ld_relaxed(flags + chid) != epoch) {
-        }
+        wait_flag(flags + chid, epoch);
       for (int c = R.chb + 32 + lane; c < R.che; c += 32) {
         const int ch = sd.ch[c];
         if (ch != heavy)
-          while (ld_relaxed(flags + ch) != epoch) {
-          }
+          wait_flag(flags + ch, epoch);
       }
       flag_wait_done();
       double uv[kLsR];
@@ -398,7 +461,7 @@ k_fwd_warp(SnDev sd, const double* __restrict__ lval, double* w, double* uvec,
           t -= lv[p] * wp;
         }
       }
-      const int hri_n = (!top && lane < f - k) ? __ldg(sd.rel + R.relp + lane) : 0;
+      const int hri_n = (!top && lane < f - k) ? ldg_pin(sd.rel + R.relp + lane) : 0;
       if (!top) load_node(Rn);
       __syncwarp();
       if (lane >= k && lane < f) Hv[lane - k] = t;
@@ -433,7 +496,7 @@ k_bwd_warp(SnDev sd, const double* __restrict__ lval, const double* __restrict__
   for (;;) {
     const int pj = next_path(counter, lane);
     if (pj >= npaths) break;
-    const int pi = npaths - 1 - pj;
+    const int pi = __ldg(sd.bwd_path + pj);
     const int pb = sd.path_ptr[pi], pe = sd.path_ptr[pi + 1];
     WRec R = load_rec(sd, pe - 1);
     double lc[kWF];  // L(r, lane), r > lane
@@ -442,8 +505,8 @@ k_bwd_warp(SnDev sd, const double* __restrict__ lval, const double* __restrict__
       const double* Lb = lval + Q.loff;
 #pragma unroll
       for (int r = 0; r < kWF; ++r)
-        lc[r] = (lane < Q.k && r > lane && r < Q.f) ? __ldg(Lb + r + static_cast<size_t>(lane) * Q.f) : 0.0;
-      wd = (lane < Q.k) ? __ldcg(w + Q.c0 + lane) / __ldg(d + Q.c0 + lane) : 0.0;
+        lc[r] = (lane < Q.k && r > lane && r < Q.f) ? ldg_pin(Lb + r + static_cast<size_t>(lane) * Q.f) : 0.0;
+      wd = (lane < Q.k) ? ldcg_pin(w + Q.c0 + lane) / ldg_pin(d + Q.c0 + lane) : 0.0;
     };
     load_node(R);
     double xr;
@@ -451,8 +514,7 @@ k_bwd_warp(SnDev sd, const double* __restrict__ lval, const double* __restrict__
       const int par = R.spar;
       const int row = (lane >= R.k && lane < R.f) ? __ldg(sd.rows + R.rowsp + lane) : 0;
       if (par >= 0 && !wide[par] && lane == 0)
-        while (ld_relaxed(flags + par) != epoch) {
-        }
+        wait_flag(flags + par, epoch);
       flag_wait_done();
       xr = (lane >= R.k && lane < R.f) ? __ldcg(x + row) : 0.0;
     }
@@ -469,7 +531,7 @@ k_bwd_warp(SnDev sd, const double* __restrict__ lval, const double* __restrict__
         }
       }
       // the next (child) node's rows below as positions in this front
-      const int myrel = (q > pb && lane >= Rn.k && lane < Rn.f) ? __ldg(sd.rel + Rn.relp + lane - Rn.k) : 0;
+      const int myrel = (q > pb && lane >= Rn.k && lane < Rn.f) ? ldg_pin(sd.rel + Rn.relp + lane - Rn.k) : 0;
 #pragma unroll
       for (int p = kWF - 1; p >= 0; --p) {
         if (p < k) {
@@ -518,13 +580,18 @@ void launch_factor_warp(const SnDev& sd, const FactorDev& fd, const double* kval
       sd, fd, kval, flags, epoch, counter, npaths, eps);
 #ifdef NCL_WTRACE  // diagnostic build: phase cycles of the last path's warp (NCL_NO_GRAPH=1)
   {
-    unsigned long long t[9];
+    unsigned long long t[11], tt[4];
     cudaStreamSynchronize(st);
     cudaMemcpyFromSymbol(t, g_wtrace, sizeof(t));
+    cudaMemcpyFromSymbol(tt, g_wtime, sizeof(tt));
+    std::fprintf(stderr, "[ncl wtime] spine starts %.3f ms, ends %.3f ms, other paths end %.3f ms\n",
+                 (tt[1] - tt[0]) * 1e-6, (tt[2] - tt[0]) * 1e-6, (tt[3] - tt[0]) * 1e-6);
+    const unsigned long long init[4] = {~0ull, 0, 0, 0};
+    cudaMemcpyToSymbol(g_wtime, init, sizeof(init));
     std::fprintf(stderr,
                  "[ncl wtrace] static %llu flags %llu A %llu light %llu fr %llu fidx %llu pivots %llu "
-                 "flags+stores %llu next %llu\n",
-                 t[0], t[1], t[2], t[3], t[6], t[7], t[8], t[4], t[5]);
+                 "flagpf %llu Lstore %llu d+stats %llu next %llu\n",
+                 t[0], t[1], t[2], t[3], t[6], t[7], t[8], t[9], t[10], t[4], t[5]);
   }
 #endif
 }

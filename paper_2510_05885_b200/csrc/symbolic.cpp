@@ -826,6 +826,40 @@ Supernodal build_supernodal(const LowerCsc& A, const Symbolic& S, int schur_n0) 
     T.path_nodes.insert(T.path_nodes.end(), tmp.begin(), tmp.end());
     T.path_ptr.push_back(static_cast<int>(T.path_nodes.size()));
   }
+  // Long paths that no other warp-tier path waits on (top is a root or has a
+  // wide parent) are handed out first: a chain-shaped tree's spine otherwise
+  // starts only after every side path has been taken.  Deadlock-free: the
+  // moved paths wait only on later paths, which never wait on them, and
+  // there are far fewer of them (<= kFrontPaths) than resident warps.  The
+  // backward solve keeps the reverse depth order (bwd_path).
+  {
+    const int np = static_cast<int>(T.path_ptr.size()) - 1;
+    std::vector<int> cand;
+    for (int p = 0; p < np; ++p) {
+      const int top = T.path_nodes[T.path_ptr[p + 1] - 1];
+      const int par = T.sparent[top];
+      if ((par < 0 || T.wide[par]) && T.path_ptr[p + 1] - T.path_ptr[p] >= kFrontPathLen) cand.push_back(p);
+    }
+    std::stable_sort(cand.begin(), cand.end(), [&](int a, int b) {
+      return T.path_ptr[a + 1] - T.path_ptr[a] > T.path_ptr[b + 1] - T.path_ptr[b];
+    });
+    if (cand.size() > static_cast<size_t>(kFrontPaths)) cand.resize(kFrontPaths);
+    std::vector<int> order(cand.begin(), cand.end()), isfront(static_cast<size_t>(np), 0);
+    for (int p : cand) isfront[p] = 1;
+    for (int p = 0; p < np; ++p)
+      if (!isfront[p]) order.push_back(p);
+    std::vector<int> nptr(1, 0), nnodes, newidx(static_cast<size_t>(np));
+    for (int i = 0; i < np; ++i) {
+      const int p = order[i];
+      newidx[p] = i;
+      nnodes.insert(nnodes.end(), T.path_nodes.begin() + T.path_ptr[p], T.path_nodes.begin() + T.path_ptr[p + 1]);
+      nptr.push_back(static_cast<int>(nnodes.size()));
+    }
+    T.path_ptr.swap(nptr);
+    T.path_nodes.swap(nnodes);
+    T.bwd_path.assign(static_cast<size_t>(np), 0);
+    for (int j = 0; j < np; ++j) T.bwd_path[j] = newidx[np - 1 - j];
+  }
   // light-child extend-add lists of the warp tier (ldl_kernels.cu)
   {
     std::vector<int> pred(static_cast<size_t>(nsn), -1);

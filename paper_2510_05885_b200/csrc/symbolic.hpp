@@ -84,6 +84,7 @@ struct Supernodal {
   // warp tier: heavy paths (bottom -> top), ordered so that every light
   // child's path precedes the path it hangs from
   std::vector<int> path_ptr, path_nodes;
+  std::vector<int> bwd_path;  // backward-solve hand-out order (path indices)
   // warp tier: extend-add entries of the children that are not the node's
   // path predecessor ("light" children), in chunks of 32 with distinct
   // destinations: src | dst << 48, -1 = padding.  Factorization: src = upd
@@ -124,6 +125,8 @@ struct Supernodal {
 };
 
 constexpr int kWarpFront = 32;
+constexpr int kFrontPaths = 32;     // long root paths handed out first (symbolic.cpp)
+constexpr int kFrontPathLen = 64;
 constexpr int kWidePanel = 32;  // pivots per panel of a wide front
 constexpr int kAsmCols = 8;     // front columns per assembly task (warp each)
 constexpr int kUpdTile = 32;    // trailing-update tile edge (one warp)
