@@ -83,6 +83,7 @@ __device__ __forceinline__ void publish(int* flag, int epoch, int lane) {
 #endif
 #if defined(NCL_WTRACE) || defined(NCL_WTRACE_DEAD)
 __device__ unsigned long long g_wtrace[11];
+__device__ unsigned long long g_ftrace[5];  // forward solve: flags, gather, substitute, prefetch, store
 __device__ unsigned long long g_wtime[4];  // kernel start (min), spine start/end, last other path end (max)
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
@@ -414,26 +415,39 @@ k_fwd_warp(SnDev sd, const double* __restrict__ lval, double* w, double* uvec,
       for (int p = 0; p < kWF; ++p)
         lv[p] = (p < Q.k && lane > p && lane < Q.f) ? ldg_pin(Lb + lane + static_cast<size_t>(p) * Q.f) : 0.0;
       wv = (lane < Q.k) ? ldcg_pin(w + Q.c0 + lane) : 0.0;
+    };
+    auto load_idx = [&](const WRec& Q) {
 #pragma unroll
       for (int t = 0; t < kLsR; ++t)
         ent[t] = (Q.lsb + t * 32 < Q.lse) ? ldg_pin(sd.ls_ent + Q.lsb + t * 32 + lane) : -1;
       chid = Q.chb + lane < Q.che ? ldg_pin(sd.ch + Q.chb + lane) : -1;
     };
     load_node(R);
+    load_idx(R);
+    int fl = chid >= 0 ? ld_relaxed(flags + chid) : epoch;  // polled a node ahead
     int heavy = -1, hfu = 0, hri = 0;
+#if defined(NCL_WTRACE) || defined(NCL_WTRACE_DEAD)
+#ifdef NCL_WTRACE
+    const bool trc = pi == 0;
+#else
+    const bool trc = pi == 0 && epoch == 0x7fffffff;
+#endif
+    unsigned long long tph[6] = {0, 0, 0, 0, 0, 0};
+    long long tq = clock64();
+#endif
     for (int q = pb; q < pe; ++q) {
       const bool top = q == pe - 1;
       const int k = R.k, f = R.f;
       WRec Rn = R;
       if (!top) Rn = load_rec(sd, q + 1);
-      if (chid >= 0 && chid != heavy)
-        wait_flag(flags + chid, epoch);
+      if (chid >= 0 && chid != heavy && fl != epoch) wait_flag(flags + chid, epoch);
       for (int c = R.chb + 32 + lane; c < R.che; c += 32) {
         const int ch = sd.ch[c];
         if (ch != heavy)
           wait_flag(flags + ch, epoch);
       }
       flag_wait_done();
+      WT(0);
       double uv[kLsR];
 #pragma unroll
       for (int t = 0; t < kLsR; ++t) uv[t] = ent[t] >= 0 ? __ldcg(uvec + (ent[t] & kSrcMask)) : 0.0;
@@ -453,6 +467,8 @@ k_fwd_warp(SnDev sd, const double* __restrict__ lval, double* w, double* uvec,
         if (x >= 0) T[x >> 48] += __ldcg(uvec + (x & kSrcMask));
         __syncwarp();
       }
+      WT(1);
+      if (!top) load_idx(Rn);  // node q+1's index words, in flight during the substitution
       double t = (lane < f) ? T[lane] : 0.0;
 #pragma unroll
       for (int p = 0; p < kWF; ++p) {
@@ -461,8 +477,13 @@ k_fwd_warp(SnDev sd, const double* __restrict__ lval, double* w, double* uvec,
           t -= lv[p] * wp;
         }
       }
+      WT(2);
       const int hri_n = (!top && lane < f - k) ? ldg_pin(sd.rel + R.relp + lane) : 0;
-      if (!top) load_node(Rn);
+      if (!top) {
+        load_node(Rn);
+        fl = (chid >= 0 && chid != R.s) ? ld_relaxed(flags + chid) : epoch;
+      }
+      WT(3);
       __syncwarp();
       if (lane >= k && lane < f) Hv[lane - k] = t;
       if (lane < k)
@@ -475,7 +496,12 @@ k_fwd_warp(SnDev sd, const double* __restrict__ lval, double* w, double* uvec,
       hri = hri_n;
       R = Rn;
       __syncwarp();
+      WT(4);
     }
+#if defined(NCL_WTRACE) || defined(NCL_WTRACE_DEAD)
+    if (trc && lane == 0)
+      for (int i = 0; i < 5; ++i) g_ftrace[i] = tph[i];
+#endif
   }
 }
 
@@ -602,6 +628,15 @@ void launch_fwd_warp(const SnDev& sd, const double* lval, double* w, double* uve
   if (npaths == 0) return;
   k_fwd_warp<<<grid, kWarpsPerCta * 32, 0, st>>>(sd, lval, w, uvec, flags, epoch,
                                                 counter, npaths);
+#ifdef NCL_WTRACE
+  {
+    unsigned long long t[5];
+    cudaStreamSynchronize(st);
+    cudaMemcpyFromSymbol(t, g_ftrace, sizeof(t));
+    std::fprintf(stderr, "[ncl ftrace] flags %llu gather %llu substitute %llu prefetch %llu store %llu\n", t[0],
+                 t[1], t[2], t[3], t[4]);
+  }
+#endif
 }
 
 void launch_bwd_warp(const SnDev& sd, const double* lval, const double* d,
