@@ -139,6 +139,12 @@ int ncl_plan_info(const ncl_plan* plan, ncl_kkt_info* info);
 int ncl_plan_symbolic(const ncl_plan* plan, int* perm, int* parent,
                       int* lcol_ptr);
 int ncl_plan_pattern(const ncl_plan* plan, int* col_ptr, int* row_ind);
+/* Checks the invariants of the warp-tier schedule built from the plan (paths,
+ * hand-out orders of the persistent kernels, light-child extend-add chunks,
+ * path-position records); internal = 1: the re-postordered structure the
+ * device factorization uses.  NCL_ELOGIC + ncl_last_error() on a violation.
+ * Test hook, no reference counterpart. */
+int ncl_plan_check_schedule(const ncl_plan* plan, int internal);
 /* Eigen AMDOrdering<int> restated (the ordering the reference calls at
  * sparse.cpp:81-100) on a full symmetric CSC pattern with sorted rows:
  * perm[k] = node eliminated k-th.  Lets a reference build without Eigen use

@@ -73,6 +73,7 @@ SIGS = {
     "ncl_plan_info": ([_p, C.POINTER(KktInfo)], _i),
     "ncl_plan_symbolic": ([_p, _ip, _ip, _ip], _i),
     "ncl_plan_pattern": ([_p, _ip, _ip], _i),
+    "ncl_plan_check_schedule": ([_p, _i], _i),
     "ncl_amd_full_pattern": ([_i, _ip, _ip, _ip], _i),
     "ncl_analyze_host": ([_i, _i, _ip, _ip, _ip, _ip, _ip, _ip], _i),
     "ncl_sparse_create": ([_i, _i, _ip, _ip, _dp, _ip, C.POINTER(_p)], _i),

@@ -1500,6 +1500,22 @@ int ncl_plan_pattern(const ncl_plan* plan, int* col_ptr, int* row_ind) {
   return NCL_OK;
 }
 
+int ncl_plan_check_schedule(const ncl_plan* plan, int internal) {
+  if (!plan) return NCL_EINVAL;
+  return guard([&] {
+    const auto& P = plan->plan;
+    const int n0 = P.sn.schur >= 0 ? P.N - P.sn.first[P.sn.schur] : 0;
+    std::string err;
+    if (internal) {  // the structure LdlSystem factors (context.cu: LdlSystem::LdlSystem)
+      const nclb::Symbolic S2 = nclb::analyze_with_permutation(P.K, nclb::tallest_child_last(P.K, P.sym.perm));
+      err = nclb::check_warp_schedule(nclb::build_supernodal(P.K, S2, n0));
+    } else {
+      err = nclb::check_warp_schedule(P.sn);
+    }
+    if (!err.empty()) throw std::logic_error("warp schedule: " + err);
+  });
+}
+
 int ncl_amd_full_pattern(int n, const int* Ap, const int* Ai, int* perm) {
   if (n < 0 || !Ap || !perm) return NCL_EINVAL;
   return guard([&] {

@@ -1006,3 +1006,118 @@ Supernodal build_supernodal(const LowerCsc& A, const Symbolic& S, int schur_n0) 
 }
 
 }  // namespace nclb
+
+namespace nclb {
+
+// Invariants of the warp-tier schedule (tests/test_warp_schedule.py).
+std::string check_warp_schedule(const Supernodal& T) {
+  const int nsn = T.nsn;
+  const int np = static_cast<int>(T.path_ptr.size()) - 1;
+  std::vector<int> path_of(static_cast<size_t>(nsn), -1), pos_of(static_cast<size_t>(nsn), -1);
+  for (int p = 0; p < np; ++p)
+    for (int q = T.path_ptr[p]; q < T.path_ptr[p + 1]; ++q) {
+      const int s = T.path_nodes[q];
+      if (s < 0 || s >= nsn || T.wide[s]) return "path holds a wide or invalid node";
+      if (path_of[s] >= 0) return "node on two paths";
+      path_of[s] = p;
+      pos_of[s] = q;
+      if (q > T.path_ptr[p] && T.sparent[T.path_nodes[q - 1]] != s) return "path step is not child -> parent";
+    }
+  for (int s = 0; s < nsn; ++s)
+    if (!T.wide[s] && path_of[s] < 0) return "warp node on no path";
+  // hand-out order: front paths first (tops without a warp-tier parent), the
+  // others after every path they wait on
+  int nfront = 0;
+  while (nfront < np) {
+    const int top = T.path_nodes[T.path_ptr[nfront + 1] - 1];
+    const int par = T.sparent[top];
+    if (T.path_ptr[nfront + 1] - T.path_ptr[nfront] < kFrontPathLen || !(par < 0 || T.wide[par])) break;
+    ++nfront;
+  }
+  if (nfront > kFrontPaths) return "too many front paths";
+  for (int p = 0; p < np; ++p)
+    for (int q = T.path_ptr[p]; q < T.path_ptr[p + 1]; ++q) {
+      const int s = T.path_nodes[q];
+      const int pred = q > T.path_ptr[p] ? T.path_nodes[q - 1] : -1;
+      for (int e = T.ch_ptr[s]; e < T.ch_ptr[s + 1]; ++e) {
+        const int c = T.ch[e];
+        if (c == pred) continue;
+        const int pc = path_of[c];
+        if (pc < 0 || T.path_nodes[T.path_ptr[pc + 1] - 1] != c) return "light child is not a path top";
+        if (pc < nfront) return "a front path is some node's light child";
+        if (p >= nfront && pc > p) return "path handed out before a light child's path";
+      }
+    }
+  // backward order: a permutation, each path after the path of its top's parent
+  if (static_cast<int>(T.bwd_path.size()) != np) return "bwd_path size";
+  std::vector<int> bpos(static_cast<size_t>(np), -1);
+  for (int j = 0; j < np; ++j) {
+    const int p = T.bwd_path[j];
+    if (p < 0 || p >= np || bpos[p] >= 0) return "bwd_path is not a permutation";
+    bpos[p] = j;
+  }
+  for (int p = 0; p < np; ++p) {
+    const int par = T.sparent[T.path_nodes[T.path_ptr[p + 1] - 1]];
+    if (par >= 0 && !T.wide[par] && bpos[path_of[par]] > bpos[p]) return "bwd: child path before its parent's";
+  }
+  // light-child chunks: distinct destinations per chunk, per destination in
+  // child order, exactly the light children's entries
+  for (int s = 0; s < nsn; ++s) {
+    for (int which = 0; which < 2; ++which) {
+      const std::vector<int>& ptr = which ? T.ls_ptr : T.lt_ptr;
+      const std::vector<long long>& ent = which ? T.ls_ent : T.lt_ent;
+      const int b = ptr[s], e = ptr[s + 1];
+      if ((e - b) % 32) return "chunk list not padded to 32";
+      std::vector<std::pair<int, long long>> want;
+      if (!T.wide[s]) {
+        const int q = pos_of[s];
+        const int pred = q > T.path_ptr[path_of[s]] ? T.path_nodes[q - 1] : -1;
+        for (int k = T.ch_ptr[s]; k < T.ch_ptr[s + 1]; ++k) {
+          const int c = T.ch[k];
+          if (c == pred) continue;
+          const int fu = T.f[c] - (T.first[c + 1] - T.first[c]);
+          const int* rl = T.rel.data() + T.rel_ptr[c];
+          if (which) {
+            for (int i = 0; i < fu; ++i) want.emplace_back(rl[i], T.rel_ptr[c] + i);
+          } else {
+            for (int j = 0; j < fu; ++j)
+              for (int i = j; i < fu; ++i)
+                want.emplace_back(rl[i] | (rl[j] << 5), T.u_off[c] + i + static_cast<long long>(j) * fu);
+          }
+        }
+      }
+      std::vector<std::pair<int, long long>> got;
+      for (int c0 = b; c0 < e; c0 += 32) {
+        std::vector<int> seen;
+        for (int t = c0; t < c0 + 32; ++t) {
+          if (ent[t] < 0) continue;
+          const int dst = static_cast<int>(ent[t] >> 48);
+          if (std::find(seen.begin(), seen.end(), dst) != seen.end()) return "destination twice in a chunk";
+          seen.push_back(dst);
+          got.emplace_back(dst, ent[t] & ((1LL << 48) - 1));
+        }
+      }
+      // per destination, the sources in the order the children contribute them
+      auto by_dst = [](std::vector<std::pair<int, long long>> v) {
+        std::stable_sort(v.begin(), v.end(), [](const auto& x, const auto& y) { return x.first < y.first; });
+        return v;
+      };
+      if (by_dst(got) != by_dst(want)) return "chunk entries differ from the light children's";
+    }
+  }
+  // path-position records
+  if (T.prec.size() != 16 * T.path_nodes.size() || T.poff.size() != 2 * T.path_nodes.size()) return "record sizes";
+  for (size_t q = 0; q < T.path_nodes.size(); ++q) {
+    const int s = T.path_nodes[q];
+    const int* r = T.prec.data() + 16 * q;
+    if (r[0] != s || r[1] != T.first[s] || r[2] != T.first[s + 1] - T.first[s] || r[3] != T.f[s] ||
+        r[4] != T.ch_ptr[s] || r[5] != T.ch_ptr[s + 1] || r[6] != T.lt_ptr[s] || r[7] != T.lt_ptr[s + 1] ||
+        r[8] != T.asm_ptr[s] || r[9] != T.asm_ptr[s + 1] || r[10] != T.rel_ptr[s] || r[11] != T.rows_ptr[s] ||
+        r[12] != T.ls_ptr[s] || r[13] != T.ls_ptr[s + 1] || r[14] != T.sparent[s] ||
+        T.poff[2 * q] != T.l_off[s] || T.poff[2 * q + 1] != T.u_off[s])
+      return "path record mismatch";
+  }
+  return "";
+}
+
+}  // namespace nclb

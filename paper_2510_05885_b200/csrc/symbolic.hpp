@@ -15,6 +15,7 @@
 
 #include <array>
 #include <cstdint>
+#include <string>
 #include <vector>
 
 namespace nclb {
@@ -147,6 +148,10 @@ std::vector<int> tallest_child_last(const LowerCsc& A, const std::vector<int>& p
 // the reference's row indices of L (sparse.cpp:157-175 / factorize's
 // ascending order per column): lrow_ind for lcol_ptr
 std::vector<int> l_row_pattern(const LowerCsc& A, const Symbolic& S);
+
+// invariants of the warp-tier schedule (paths, hand-out orders, chunk lists,
+// records); "" when they hold, else the first violation
+std::string check_warp_schedule(const Supernodal& T);
 
 // wide levels factored by the multi-kernel path (one front over every SM):
 // a front above kHugeFront, or at most kHugeMaxN fronts of kHugeMinF rows
