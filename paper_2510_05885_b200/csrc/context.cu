@@ -140,6 +140,10 @@ class LdlSystem {
     launches_ += npaths() > 0 ? 1 : 0;
     const auto& T = sn_;
     for (int l = 0; l < nlevels(); ++l) {
+      for (int s : lvl_split_[l]) {  // fronts with very many children: group sums first
+        launch_cc_partial(sd_, fd, s, T.f[s], T.split_ng[s], st_);
+        launches_ += 1;
+      }
       if (lvl_fmax_[l] <= small_factor_limit()) {  // a warp per front
         launch_small_front(sd_, fd, kval, lvl_nodes_.p + T.lvl_ptr[l], T.lvl_ptr[l + 1] - T.lvl_ptr[l],
                            lvl_fmax_[l], eps, st_);
@@ -233,6 +237,10 @@ class LdlSystem {
       launch_fwd_warp(sd_, lval_.p, wp_.p, uvec_.p, flags_.p, 2, counter_.p, npaths(), sgrid_, st_);
     }
     for (int l = 0; l < nlevels(); ++l) {
+      for (int s : lvl_usplit_[l]) {
+        launch_uv_partial(sd_, uvec_.p, s, sn_.f[s], sn_.usplit_ng[s], st_);
+        launches_ += 1;
+      }
       if (lvl_fmax_[l] <= small_solve_limit()) {
         launch_fwd_small(sd_, lval_.p, wp_.p, uvec_.p, lvl_nodes_.p + sn_.lvl_ptr[l],
                          sn_.lvl_ptr[l + 1] - sn_.lvl_ptr[l], lvl_fmax_[l], st_);
@@ -422,6 +430,7 @@ class LdlSystem {
     fd.upd = upd_.p;
     fd.stats = ds_.p->stats;
     fd.dscr = dscr_.p;
+    fd.ccpart = ccpart_.p;
     return fd;
   }
 
@@ -474,6 +483,12 @@ class LdlSystem {
     pn_tasks_.upload(pt);
     dg_nodes_.upload(T.dg_nodes);
     dscr_.alloc(static_cast<size_t>(std::max(1, T.max_dg)) * (kWidePanel * kWidePanel));
+    split_ng_.upload(T.split_ng);
+    split_off_.upload(T.split_off);
+    usplit_ng_.upload(T.usplit_ng);
+    usplit_off_.upload(T.usplit_off);
+    ccpart_.alloc(static_cast<size_t>(std::max(1LL, T.split_total)));
+    uvpart_.alloc(static_cast<size_t>(std::max(1LL, T.usplit_total)));
     asm_cp_.upload(T.asm_cp);
     cc_off_.upload(T.cc_off);
     cc_ptr_.upload(T.cc_ptr);
@@ -502,6 +517,14 @@ class LdlSystem {
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     }
     lvl_cluster_.assign(static_cast<size_t>(nlevels()), 0);
+    lvl_split_.assign(static_cast<size_t>(nlevels()), {});
+    lvl_usplit_.assign(static_cast<size_t>(nlevels()), {});
+    for (int l = 0; l < nlevels(); ++l)
+      for (int q = T.lvl_ptr[l]; q < T.lvl_ptr[l + 1]; ++q) {
+        const int s = T.lvl_nodes[q];
+        if (T.split_ng[s]) lvl_split_[l].push_back(s);
+        if (T.usplit_ng[s]) lvl_usplit_[l].push_back(s);
+      }
     lvl_fmax_.assign(static_cast<size_t>(nlevels()), 0);
     lvl_kmax_.assign(static_cast<size_t>(nlevels()), 0);
     solve_cluster_.assign(static_cast<size_t>(nlevels()), 1);
@@ -644,6 +667,11 @@ class LdlSystem {
     sd_.ls_ptr = ls_ptr_.p;
     sd_.ls_ent = ls_ent_.p;
     sd_.prec = prec_.p;
+    sd_.split_ng = split_ng_.p;
+    sd_.split_off = split_off_.p;
+    sd_.usplit_ng = usplit_ng_.p;
+    sd_.usplit_off = usplit_off_.p;
+    sd_.uvpart = uvpart_.p;
     sd_.poff = poff_.p;
     sd_.wide = wide_.p;
     sd_.schur = T.schur;
@@ -671,15 +699,16 @@ class LdlSystem {
   DBuf<double> bin_, xout_;
   long long launches_ = 0;
   std::vector<int> lvl_cluster_, lvl_fmax_, lvl_kmax_, solve_cluster_;
+  std::vector<std::vector<int>> lvl_split_, lvl_usplit_;  // per level: fronts with split extend-adds
   int trace_level_ = -1;
   DBuf<unsigned long long> trace_;
   SnDev sd_{};
   DBuf<int> first_, f_, sparent_, rows_ptr_, rows_, u_ld_, asm_ptr_, asm_pos_, asm_slot_,
       ch_ptr_, ch_, rel_ptr_, rel_, path_ptr_, path_nodes_, lvl_nodes_, perm_, flags_,
       counter_, fr_ptr_, fr_col_, fr_slot_, dg_nodes_, asm_cp_, cc_off_, cc_ptr_, cc_rbase_,
-      cc_cnt_, lt_ptr_, ls_ptr_, bwd_path_;
-  DBuf<long long> cc_ubase_, lt_ent_, ls_ent_;
-  DBuf<double> dscr_;
+      cc_cnt_, lt_ptr_, ls_ptr_, bwd_path_, split_ng_, usplit_ng_;
+  DBuf<long long> cc_ubase_, lt_ent_, ls_ent_, split_off_, usplit_off_;
+  DBuf<double> dscr_, ccpart_, uvpart_;
   DBuf<int8_t> wide_;
   DBuf<int4> asm_task_, prec_;
   DBuf<longlong2> poff_;

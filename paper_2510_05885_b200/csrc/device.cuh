@@ -39,6 +39,11 @@ struct SnDev {
   const long long* ls_ent;
   const int4* prec;          // 4 per path position (symbolic.hpp)
   const longlong2* poff;     // 1 per path position: {l_off, u_off}
+  const int* split_ng;       // per front: factorization extend-add groups (0: unsplit)
+  const long long* split_off;
+  const int* usplit_ng;      // per front: forward-solve gather groups (0: unsplit)
+  const long long* usplit_off;
+  double* uvpart;            // forward-solve group sums (split.cu)
   const int8_t* wide;        // 1: wide-tier front (stored f x f in lval)
   int schur;                 // Schur-mode coupling supernode (assembled only), or -1
 };
@@ -54,6 +59,7 @@ struct FactorDev {
   double* upd;    // u_total: warp-tier update blocks
   int* stats;     // [0] n_pos [1] n_neg [2] perturbed [3] fail
   double* dscr;   // huge-front path: per diag task {Us[32][32], rinv[32]}
+  double* ccpart; // split extend-add group sums (split.cu)
 };
 
 __device__ __forceinline__ int ld_acquire(const int* p) {

@@ -65,7 +65,9 @@ void launch_permute_in(int n, const int* perm, const double* b, double* w,
                        cudaStream_t st);
 void launch_permute_out(int n, const int* perm, const double* xp, double* x,
                         cudaStream_t st);
-int warp_tier_grid(bool solves);  // resident CTAs of the factor / solve kernels
+int warp_tier_grid(bool solves);
+void launch_cc_partial(const SnDev& sd, const FactorDev& fd, int s, int f, int ng, cudaStream_t st);
+void launch_uv_partial(const SnDev& sd, const double* uvec, int s, int f, int ng, cudaStream_t st);  // resident CTAs of the factor / solve kernels
 
 // kkt_kernels.cu
 void launch_assemble(const AsmDev& a, int form, int m, int m_eq, int nt,

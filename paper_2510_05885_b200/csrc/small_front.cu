@@ -37,6 +37,18 @@ __device__ __forceinline__ void small_assemble_col(const SnDev& sd, const Factor
   __syncwarp();
   for (int q = a0 + lane; q < a1; q += 32) a[sd.asm_pos[q] & 0xffff] += __ldg(kval + sd.asm_slot[q]);
   __syncwarp();
+  const int ng = sd.split_ng[s];
+  if (ng) {  // group sums of the contributions (split.cu), in group order
+    const double* P = fd.ccpart + sd.split_off[s] + static_cast<size_t>(J) * ng * f;
+    for (int r = J + lane; r < f; r += 32) {
+      double v = a[r];
+#pragma unroll 8
+      for (int g = 0; g < ng; ++g) v += __ldcg(P + static_cast<size_t>(g) * f + r);
+      a[r] = v;
+    }
+    __syncwarp();
+    return;
+  }
   for (int e = e0; e < e1; ++e) {
     const long long ub = sd.cc_ubase[e];
     const int rb = sd.cc_rbase[e], cw = sd.cc_cnt[e];
@@ -138,11 +150,22 @@ k_fwd_small(SnDev sd, const double* __restrict__ lval, double* w, double* uvec,
   const double* L = lval + sd.l_off[s];
   for (int r = lane; r < f; r += 32) T[r] = r < k ? __ldcg(w + c0 + r) : 0.0;
   __syncwarp();
-  for (int cc = sd.ch_ptr[s]; cc < sd.ch_ptr[s + 1]; ++cc) {
-    const int c = sd.ch[cc];
-    const int fu = f_minus_k(sd, c), rp = sd.rel_ptr[c];
-    for (int i = lane; i < fu; i += 32) T[sd.rel[rp + i]] += __ldcg(uvec + rp + i);
+  if (const int ng = sd.usplit_ng[s]) {  // group sums (split.cu), in group order
+    const double* P = sd.uvpart + sd.usplit_off[s];
+    for (int r = lane; r < f; r += 32) {
+      double v = T[r];
+#pragma unroll 8
+      for (int g = 0; g < ng; ++g) v += __ldcg(P + static_cast<size_t>(g) * f + r);
+      T[r] = v;
+    }
     __syncwarp();
+  } else {
+    for (int cc = sd.ch_ptr[s]; cc < sd.ch_ptr[s + 1]; ++cc) {
+      const int c = sd.ch[cc];
+      const int fu = f_minus_k(sd, c), rp = sd.rel_ptr[c];
+      for (int i = lane; i < fu; i += 32) T[sd.rel[rp + i]] += __ldcg(uvec + rp + i);
+      __syncwarp();
+    }
   }
   double t[R];
 #pragma unroll

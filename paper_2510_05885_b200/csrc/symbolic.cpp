@@ -955,6 +955,34 @@ Supernodal build_supernodal(const LowerCsc& A, const Symbolic& S, int schur_n0) 
       }
     }
   }
+  // fronts with very many children (the Schur mode's coupling front: one
+  // contribution per contingency block and column): their extend-add is
+  // pre-summed over groups of contributions by a wide grid (ldl_kernels.cu
+  // k_cc_partial / k_uv_partial) before the front's own kernel adds the
+  // group sums in group order
+  T.split_ng.assign(static_cast<size_t>(nsn), 0);
+  T.split_off.assign(static_cast<size_t>(nsn), 0);
+  T.usplit_ng.assign(static_cast<size_t>(nsn), 0);
+  T.usplit_off.assign(static_cast<size_t>(nsn), 0);
+  for (int s = 0; s < nsn; ++s) {
+    if (!T.wide[s] || T.f[s] > kSplitMaxF) continue;
+    int maxc = 0;
+    for (int J = 0; J < T.f[s]; ++J)
+      maxc = std::max(maxc, T.cc_ptr[T.cc_off[s] + J + 1] - T.cc_ptr[T.cc_off[s] + J]);
+    if (maxc >= kSplitMin) {
+      const int ng = std::min(kSplitMaxG, (maxc + kSplitPerGroup - 1) / kSplitPerGroup);
+      T.split_ng[s] = ng;
+      T.split_off[s] = T.split_total;
+      T.split_total += static_cast<long long>(ng) * T.f[s] * T.f[s];
+    }
+    const int nch = T.ch_ptr[s + 1] - T.ch_ptr[s];
+    if (nch >= kSplitMin) {
+      const int ng = std::min(kSplitMaxG, (nch + kSplitPerGroup - 1) / kSplitPerGroup);
+      T.usplit_ng[s] = ng;
+      T.usplit_off[s] = T.usplit_total;
+      T.usplit_total += static_cast<long long>(ng) * T.f[s];
+    }
+  }
   // huge-front launch schedule: per level, assembly tasks (front, kAsmCols
   // columns); per (level, panel) the fronts that factor that panel, their
   // TRSM row blocks and the 32x32 tiles of their trailing lower triangle

@@ -100,6 +100,12 @@ struct Supernodal {
   // poff[2q..2q+1] = {l_off, u_off}
   std::vector<int> prec;
   std::vector<long long> poff;
+  // split extend-add of fronts with many children (symbolic.cpp): groups per
+  // front (0 = none) and offsets of the group sums (factorization: ng x f x f
+  // doubles; forward solve: ng x f)
+  std::vector<int> split_ng, usplit_ng;
+  std::vector<long long> split_off, usplit_off;
+  long long split_total = 0, usplit_total = 0;
   // wide tier: level lists (level 0 = deepest wide fronts)
   std::vector<int> lvl_ptr, lvl_nodes;
   // huge-front (three-kernel) schedule: assembly tasks {front, first
@@ -126,6 +132,10 @@ struct Supernodal {
 };
 
 constexpr int kWarpFront = 32;
+constexpr int kSplitMin = 128;       // contributions (children) per column that trigger a split
+constexpr int kSplitPerGroup = 64;   // contributions per group (8 warps x 8)
+constexpr int kSplitMaxG = 64;
+constexpr int kSplitMaxF = 512;
 constexpr int kFrontPaths = 32;     // long root paths handed out first (symbolic.cpp)
 constexpr int kFrontPathLen = 64;
 constexpr int kWidePanel = 32;  // pivots per panel of a wide front

@@ -160,14 +160,26 @@ __device__ __noinline__ void assemble_col(const SnDev& sd, const FactorDev& fd,
   __syncwarp();
   for (int q = a0 + lane; q < a1; q += 32) a[sd.asm_pos[q] & 0xffff] += __ldg(kval + sd.asm_slot[q]);
   __syncwarp();
-  for (int e = e0; e < e1; ++e) {
-    const long long ub = sd.cc_ubase[e];
-    const int rb = sd.cc_rbase[e], cw = sd.cc_cnt[e];
-    const int cnt = cw & ((1 << 30) - 1);
-    const double* U = ((cw >> 30) ? fd.lval : fd.upd) + ub;
-    const int* rel = sd.rel + rb;
-    for (int i = lane; i < cnt; i += 32) a[rel[i]] += __ldcg(U + i);
+  const int ng = sd.split_ng[s];
+  if (ng) {  // group sums of the contributions (split.cu), in group order
+    const double* P = fd.ccpart + sd.split_off[s] + static_cast<size_t>(J) * ng * f;
+    for (int r = J + lane; r < f; r += 32) {
+      double v = a[r];
+#pragma unroll 8
+      for (int g = 0; g < ng; ++g) v += __ldcg(P + static_cast<size_t>(g) * f + r);
+      a[r] = v;
+    }
     __syncwarp();
+  } else {
+    for (int e = e0; e < e1; ++e) {
+      const long long ub = sd.cc_ubase[e];
+      const int rb = sd.cc_rbase[e], cw = sd.cc_cnt[e];
+      const int cnt = cw & ((1 << 30) - 1);
+      const double* U = ((cw >> 30) ? fd.lval : fd.upd) + ub;
+      const int* rel = sd.rel + rb;
+      for (int i = lane; i < cnt; i += 32) a[rel[i]] += __ldcg(U + i);
+      __syncwarp();
+    }
   }
   if (acc)
     for (int r = J + lane; r < f; r += 32) col[r] = a[r];

@@ -109,11 +109,22 @@ k_fwd_front(SnDev sd, const double* __restrict__ lval, double* w, double* uvec,
     if (kp > 0 && !par) issue(0, 0, 0);
     for (int r = tid; r < f; r += kSolveThreads) T[r] = r < k ? __ldcg(w + c0 + r) : 0.0;
     __syncthreads();
-    for (int cc = sd.ch_ptr[s]; cc < sd.ch_ptr[s + 1]; ++cc) {
-      const int c = sd.ch[cc];
-      const int fu = f_minus_k(sd, c), rp = sd.rel_ptr[c];
-      for (int i = tid; i < fu; i += kSolveThreads) T[sd.rel[rp + i]] += __ldcg(uvec + rp + i);
+    if (const int ng = sd.usplit_ng[s]) {  // group sums (split.cu), in group order
+      const double* P = sd.uvpart + sd.usplit_off[s];
+      for (int r = tid; r < f; r += kSolveThreads) {
+        double v = T[r];
+#pragma unroll 8
+        for (int g = 0; g < ng; ++g) v += __ldcg(P + static_cast<size_t>(g) * f + r);
+        T[r] = v;
+      }
       __syncthreads();
+    } else {
+      for (int cc = sd.ch_ptr[s]; cc < sd.ch_ptr[s + 1]; ++cc) {
+        const int c = sd.ch[cc];
+        const int fu = f_minus_k(sd, c), rp = sd.rel_ptr[c];
+        for (int i = tid; i < fu; i += kSolveThreads) T[sd.rel[rp + i]] += __ldcg(uvec + rp + i);
+        __syncthreads();
+      }
     }
     for (; kp > 0 && !par;) {
       const int p0 = sb * kBlk, p1 = min(p0 + kBlk, k), nb = p1 - p0;
