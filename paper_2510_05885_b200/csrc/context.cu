@@ -332,7 +332,8 @@ class LdlSystem {
   // r = b - A x; norm slot (device) receives max|r| (must be zeroed by caller)
   void residual_async(const double* kval, const double* x, const double* b, double* r,
                       double* norm) {
-    launch_residual(N_, fr_ptr_.p, fr_col_.p, fr_slot_.p, kval, x, b, r, norm, st_);
+    launch_residual(N_, fr_ptr_.p, fr_col_.p, fr_slot_.p, kval, x, b, r, norm, long_rows_.p,
+                    static_cast<int>(long_rows_.n), st_);
     launches_ += 1;
   }
 
@@ -635,6 +636,12 @@ class LdlSystem {
         fslot[nx[j]++] = p;
       }
     fr_ptr_.upload(cnt);
+    {
+      std::vector<int> lr;
+      for (int i = 0; i < N_; ++i)
+        if (cnt[i + 1] - cnt[i] > 256) lr.push_back(i);  // kkt_kernels.cu kLongRow
+      long_rows_.upload(lr);
+    }
     fr_col_.upload(fcol);
     fr_slot_.upload(fslot);
     sd_.nsn = T.nsn;
@@ -705,7 +712,7 @@ class LdlSystem {
   SnDev sd_{};
   DBuf<int> first_, f_, sparent_, rows_ptr_, rows_, u_ld_, asm_ptr_, asm_pos_, asm_slot_,
       ch_ptr_, ch_, rel_ptr_, rel_, path_ptr_, path_nodes_, lvl_nodes_, perm_, flags_,
-      counter_, fr_ptr_, fr_col_, fr_slot_, dg_nodes_, asm_cp_, cc_off_, cc_ptr_, cc_rbase_,
+      counter_, fr_ptr_, fr_col_, fr_slot_, long_rows_, dg_nodes_, asm_cp_, cc_off_, cc_ptr_, cc_rbase_,
       cc_cnt_, lt_ptr_, ls_ptr_, bwd_path_, split_ng_, usplit_ng_;
   DBuf<long long> cc_ubase_, lt_ent_, ls_ent_, split_off_, usplit_off_;
   DBuf<double> dscr_, ccpart_, uvpart_;
@@ -767,6 +774,17 @@ class KktSystem {
     asm_.pair_row = pair_row_.p;
     asm_.pair_pa = pair_pa_.p;
     asm_.pair_pb = pair_pb_.p;
+    {  // long in-order sums get a warp each (kkt_kernels.cu)
+      std::vector<int> ls, lc;
+      for (int q = 0; q < P_.K.nnz(); ++q)
+        if (P_.c_ptr[q + 1] - P_.c_ptr[q] > kLongSum) ls.push_back(q);
+      for (int c = 0; c < P_.nt; ++c)
+        if (P_.jt_ptr[c + 1] - P_.jt_ptr[c] > kLongSum) lc.push_back(c);
+      long_slots_.upload(ls);
+      long_cols_.upload(lc);
+      asm_.long_slots = long_slots_.p;
+      asm_.nlong = static_cast<int>(ls.size());
+    }
     CK(cudaStreamSynchronize(st_));
   }
 
@@ -834,7 +852,7 @@ class KktSystem {
       if (F.ok && F.n_pos == tgt[0] && F.n_neg == tgt[1]) {
         const int e3 = tick();
         launch_rhs(P_, jt_ptr_.p, jt_row_.p, jt_slot_.p, jv, sg, r1, r2, r3, rho, delta, v_.p,
-                   wk_.p, rs_.p, pk_.p, rhs_.p, st_);
+                   wk_.p, rs_.p, pk_.p, rhs_.p, long_cols_.p, static_cast<int>(long_cols_.n), st_);
         launches_ += P_.form == kK1s ? 2 : 1;
         double rel = 0.0;
         int conv = 0;
@@ -906,7 +924,7 @@ class KktSystem {
   void rhs_async(const double* jv, const double* sg, const double* r1, const double* r2,
                  const double* r3, double rho, double delta, double* out) {
     launch_rhs(P_, jt_ptr_.p, jt_row_.p, jt_slot_.p, jv, sg, r1, r2, r3, rho, delta, v_.p, wk_.p,
-               rs_.p, pk_.p, out, st_);
+               rs_.p, pk_.p, out, long_cols_.p, static_cast<int>(long_cols_.n), st_);
     launches_ += P_.form == kK1s ? 2 : 1;
   }
   void recover_async(const double* jv, const double* sol, const double* r2, double rho,
@@ -963,6 +981,7 @@ class KktSystem {
   cudaStream_t st_ = nullptr;
   std::unique_ptr<LdlSystem> ldl_;
   AsmDev asm_{};
+  DBuf<int> long_slots_, long_cols_;
   DBuf<int> c_ptr_, pair_row_, pair_pa_, pair_pb_, jp_ptr_, jp_idx_, jt_ptr_, jt_row_,
       jt_slot_;
   DBuf<uint32_t> c_code_;

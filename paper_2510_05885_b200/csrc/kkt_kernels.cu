@@ -31,6 +31,34 @@ __global__ void k_row_weight(int m, int m_eq, int nt, const double* __restrict__
   wrow[i] = __dmul_rn(rho_hat, omega);
 }
 
+// one refill contribution (kkt.cpp:149-186 term types)
+__device__ __forceinline__ double refill_term(const AsmDev& a, int q, const double* __restrict__ hval,
+                                              const double* __restrict__ jval,
+                                              const double* __restrict__ sigma,
+                                              const double* __restrict__ wrow, double rho_hat,
+                                              double delta) {
+  const uint32_t code = a.c_code[q];
+  const uint32_t idx = code & kIdxMask;
+  switch (code >> kTypeShift) {
+    case kCH: return hval[idx];
+    case kCDiag: return __dadd_rn(sigma[idx], delta);
+    case kCPair:
+      return __dmul_rn(__dmul_rn(wrow[a.pair_row[idx]], jval[a.pair_pa[idx]]), jval[a.pair_pb[idx]]);
+    case kCJ: return jval[idx];
+    case kCMinus1: return -1.0;
+    case kCYdiag: return __ddiv_rn(-1.0, rho_hat);
+    case kCRho: return rho_hat;
+    default: return 1.0;
+  }
+}
+
+// acc + v_0 + v_1 + ... + v_{n-1} left to right (v_i held by lane i), every
+// lane returning the same bitwise result of the sequential sum
+__device__ __forceinline__ double ordered_warp_sum(double acc, double v, int n) {
+  for (int i = 0; i < n; ++i) acc = __dadd_rn(acc, __shfl_sync(0xffffffffu, v, i));
+  return acc;
+}
+
 // one thread per K slot: acc = 0; acc += contribution, in refill order
 __global__ void k_assemble(AsmDev a, const double* __restrict__ hval,
                            const double* __restrict__ jval,
@@ -39,28 +67,34 @@ __global__ void k_assemble(AsmDev a, const double* __restrict__ hval,
                            double delta, double* kval) {
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= a.nnz) return;
+  const int b = a.c_ptr[s], e = a.c_ptr[s + 1];
+  if (e - b > kLongSum) return;  // k_assemble_long
   double acc = 0.0;
-  const int e = a.c_ptr[s + 1];
-  for (int q = a.c_ptr[s]; q < e; ++q) {
-    const uint32_t code = a.c_code[q];
-    const uint32_t idx = code & kIdxMask;
-    double v;
-    switch (code >> kTypeShift) {
-      case kCH: v = hval[idx]; break;
-      case kCDiag: v = __dadd_rn(sigma[idx], delta); break;
-      case kCPair:
-        v = __dmul_rn(__dmul_rn(wrow[a.pair_row[idx]], jval[a.pair_pa[idx]]),
-                      jval[a.pair_pb[idx]]);
-        break;
-      case kCJ: v = jval[idx]; break;
-      case kCMinus1: v = -1.0; break;
-      case kCYdiag: v = __ddiv_rn(-1.0, rho_hat); break;
-      case kCRho: v = rho_hat; break;
-      default: v = 1.0; break;
-    }
-    acc = __dadd_rn(acc, v);
-  }
+  for (int q = b; q < e; ++q)
+    acc = __dadd_rn(acc, refill_term(a, q, hval, jval, sigma, wrow, rho_hat, delta));
   kval[s] = acc;
+}
+
+// slots with more than kLongSum contributions (SCOPF: the coupling rows sum
+// over every contingency block): one warp per slot, 32 terms evaluated at a
+// time (their loads in flight together), then added in the refill order by
+// every lane (shuffle broadcast) -- bitwise the sequential sum
+__global__ void k_assemble_long(AsmDev a, const double* __restrict__ hval,
+                                const double* __restrict__ jval,
+                                const double* __restrict__ sigma,
+                                const double* __restrict__ wrow, double rho_hat,
+                                double delta, double* kval) {
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (w >= a.nlong) return;
+  const int s = a.long_slots[w];
+  const int b = a.c_ptr[s], e = a.c_ptr[s + 1];
+  double acc = 0.0;
+  for (int q0 = b; q0 < e; q0 += 32) {
+    const int q = q0 + lane;
+    const double v = q < e ? refill_term(a, q, hval, jval, sigma, wrow, rho_hat, delta) : 0.0;
+    acc = ordered_warp_sum(acc, v, min(32, e - q0));
+  }
+  if (lane == 0) kval[s] = acc;
 }
 
 // hmax = max(|hval|, |sigma[0:n]|) (kkt.cpp:269-271); out must be zeroed
@@ -128,8 +162,9 @@ __global__ void k_rhs_k1s(int nt, int m_eq, const int* __restrict__ jt_ptr,
                           double* rhs) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= nt) return;
-  double acc = -r1[c];
   const int b = jt_ptr[c], e = jt_ptr[c + 1];
+  if (e - b > kLongSum) return;  // k_rhs_k1s_long
+  double acc = -r1[c];
   for (int q = b; q < e; ++q)
     acc = __dadd_rn(acc, __dmul_rn(jval[jt_slot[q]], v[jt_row[q]]));
   for (int q = b; q < e; ++q) {
@@ -137,6 +172,39 @@ __global__ void k_rhs_k1s(int nt, int m_eq, const int* __restrict__ jt_ptr,
     if (i >= m_eq) acc = __dadd_rn(acc, __dmul_rn(jval[jt_slot[q]], wk[i - m_eq]));
   }
   rhs[c] = acc;
+}
+
+// columns with more than kLongSum Jacobian entries: one warp each, the two
+// passes of k_rhs_k1s as chunked in-order sums (bitwise the same)
+__global__ void k_rhs_k1s_long(int m_eq, const int* __restrict__ long_cols, int nlong,
+                               const int* __restrict__ jt_ptr, const int* __restrict__ jt_row,
+                               const int* __restrict__ jt_slot, const double* __restrict__ jval,
+                               const double* __restrict__ r1, const double* __restrict__ v,
+                               const double* __restrict__ wk, double* rhs) {
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (w >= nlong) return;
+  const int c = long_cols[w];
+  const int b = jt_ptr[c], e = jt_ptr[c + 1];
+  double acc = -r1[c];
+  for (int q0 = b; q0 < e; q0 += 32) {
+    const int q = q0 + lane;
+    const double t = q < e ? __dmul_rn(jval[jt_slot[q]], v[jt_row[q]]) : 0.0;
+    acc = ordered_warp_sum(acc, t, min(32, e - q0));
+  }
+  for (int q0 = b; q0 < e; q0 += 32) {
+    const int q = q0 + lane;
+    const int i = q < e ? jt_row[q] : -1;
+    const bool ineq = i >= m_eq;
+    const double t = ineq ? __dmul_rn(jval[jt_slot[q]], wk[i - m_eq]) : 0.0;
+    // only the inequality rows are added (in order)
+    unsigned msk = __ballot_sync(0xffffffffu, ineq);
+    while (msk) {
+      const int src = __ffs(msk) - 1;
+      acc = __dadd_rn(acc, __shfl_sync(0xffffffffu, t, src));
+      msk &= msk - 1;
+    }
+  }
+  if (lane == 0) rhs[c] = acc;
 }
 
 // ---- recovery ---------------------------------------------------------------
@@ -200,12 +268,15 @@ __global__ void k_nonfinite(int n, const double* __restrict__ a, int* flag) {
 // r = b - A x over the full symmetric row pattern; norm = max |r_i| (NaN
 // entries skipped exactly as std::max(nrm, nan) skips them, sparse.cpp:296)
 constexpr int kRowLanes = 8;
+constexpr int kLongRow = 256;  // longer residual rows: k_residual_long
 __global__ void k_residual(int N, const int* __restrict__ fr_ptr, const int* __restrict__ fr_col,
                            const int* __restrict__ fr_slot, const double* __restrict__ kval,
                            const double* __restrict__ x, const double* __restrict__ b,
                            double* r, double* norm) {
   const int gt = blockIdx.x * blockDim.x + threadIdx.x;
-  const int row = gt / kRowLanes, sub = gt % kRowLanes;
+  int row = gt / kRowLanes;
+  const int sub = gt % kRowLanes;
+  if (row < N && fr_ptr[row + 1] - fr_ptr[row] > kLongRow) row = N;  // k_residual_long
   double acc = 0.0;
   if (row < N)
     for (int q = fr_ptr[row] + sub; q < fr_ptr[row + 1]; q += kRowLanes)
@@ -226,6 +297,31 @@ __global__ void k_residual(int N, const int* __restrict__ fr_ptr, const int* __r
   if ((threadIdx.x & 31) == 0) atomic_max_nonneg(norm, mag);
 }
 
+// rows longer than kLongRow: one CTA each, fixed-order tree reduction
+__global__ void __launch_bounds__(256)
+k_residual_long(const int* __restrict__ long_rows, const int* __restrict__ fr_ptr,
+                const int* __restrict__ fr_col, const int* __restrict__ fr_slot,
+                const double* __restrict__ kval, const double* __restrict__ x,
+                const double* __restrict__ b, double* r, double* norm) {
+  __shared__ double red[8];
+  const int row = long_rows[blockIdx.x];
+  double acc = 0.0;
+  for (int q = fr_ptr[row] + threadIdx.x; q < fr_ptr[row + 1]; q += 256) acc += kval[fr_slot[q]] * x[fr_col[q]];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int i = 0; i < 8; ++i) t += red[i];
+    const double ri = b[row] - t;
+    r[row] = ri;
+    double mag = fabs(ri);
+    if (mag != mag) mag = 0.0;
+    atomic_max_nonneg(norm, mag);
+  }
+}
+
 __global__ void k_axpy_to(int n, const double* __restrict__ x, const double* __restrict__ dx,
                           double* out) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -244,6 +340,8 @@ void launch_assemble(const AsmDev& a, int form, int m, int m_eq, int nt,
     k_row_weight<<<nb(m), 256, 0, st>>>(m, m_eq, nt, sigma, rho_hat, delta, wrow);
   if (a.nnz > 0)
     k_assemble<<<nb(a.nnz), 256, 0, st>>>(a, hval, jval, sigma, wrow, rho_hat, delta, kval);
+  if (a.nlong > 0)
+    k_assemble_long<<<nb(a.nlong * 32), 256, 0, st>>>(a, hval, jval, sigma, wrow, rho_hat, delta, kval);
 }
 
 void launch_absmax2(int n1, const double* a, int n2, const double* b, double* out,
@@ -258,7 +356,8 @@ void launch_absmax2(int n1, const double* a, int n2, const double* b, double* ou
 void launch_rhs(const KktPlan& P, const int* jt_ptr, const int* jt_row, const int* jt_slot,
                 const double* jval, const double* sigma, const double* r1,
                 const double* r2, const double* r3, double rho, double delta, double* v,
-                double* wk, double* rs, double* pk, double* rhs, cudaStream_t st) {
+                double* wk, double* rs, double* pk, double* rhs, const int* long_cols, int nlong_cols,
+                cudaStream_t st) {
   const double rho_hat = rho + delta;
   const int n = P.n, m = P.m;
   const int big = n > m ? n : m;
@@ -271,6 +370,9 @@ void launch_rhs(const KktPlan& P, const int* jt_ptr, const int* jt_row, const in
                                              delta, v, wk, rs, pk);
     if (P.nt) k_rhs_k1s<<<nb(P.nt), 256, 0, st>>>(P.nt, P.m_eq, jt_ptr, jt_row, jt_slot, jval,
                                                 r1, v, wk, rhs);
+    if (nlong_cols)
+      k_rhs_k1s_long<<<nb(nlong_cols * 32), 256, 0, st>>>(P.m_eq, long_cols, nlong_cols, jt_ptr, jt_row,
+                                                        jt_slot, jval, r1, v, wk, rhs);
   }
 }
 
@@ -303,11 +405,13 @@ void launch_nonfinite(int n, const double* a, int* flag, cudaStream_t st) {
 
 void launch_residual(int N, const int* fr_ptr, const int* fr_col, const int* fr_slot,
                      const double* kval, const double* x, const double* b, double* r,
-                     double* norm, cudaStream_t st) {
+                     double* norm, const int* long_rows, int nlong_rows, cudaStream_t st) {
   if (N == 0) return;
   const long long threads = static_cast<long long>(N) * kRowLanes;
   k_residual<<<static_cast<int>((threads + 255) / 256), 256, 0, st>>>(N, fr_ptr, fr_col, fr_slot,
                                                                      kval, x, b, r, norm);
+  if (nlong_rows)
+    k_residual_long<<<nlong_rows, 256, 0, st>>>(long_rows, fr_ptr, fr_col, fr_slot, kval, x, b, r, norm);
 }
 
 void launch_axpy_to(int n, const double* x, const double* dx, double* out, cudaStream_t st) {

@@ -16,7 +16,11 @@ struct AsmDev {
   const int* pair_row;
   const int* pair_pa;
   const int* pair_pb;
+  const int* long_slots;  // slots with more than kLongSum contributions (k_assemble_long)
+  int nlong;
 };
+
+constexpr int kLongSum = 64;  // in-order sums longer than this: a warp each
 
 // ldl_kernels.cu
 void launch_factor_warp(const SnDev& sd, const FactorDev& fd, const double* kval,
@@ -79,7 +83,8 @@ void launch_absmax2(int n1, const double* a, int n2, const double* b, double* ou
 void launch_rhs(const KktPlan& P, const int* jt_ptr, const int* jt_row, const int* jt_slot,
                 const double* jval, const double* sigma, const double* r1,
                 const double* r2, const double* r3, double rho, double delta, double* v,
-                double* wk, double* rs, double* pk, double* rhs, cudaStream_t st);
+                double* wk, double* rs, double* pk, double* rhs, const int* long_cols, int nlong_cols,
+                cudaStream_t st);
 void launch_recover(const KktPlan& P, const int* jp_ptr, const int* jp_idx,
                     const double* jval, const double* sol, const double* v,
                     const double* rs, const double* pk, const double* r2, double rho,
@@ -87,7 +92,7 @@ void launch_recover(const KktPlan& P, const int* jp_ptr, const int* jp_idx,
 void launch_nonfinite(int n, const double* a, int* flag, cudaStream_t st);
 void launch_residual(int N, const int* fr_ptr, const int* fr_col, const int* fr_slot,
                      const double* kval, const double* x, const double* b, double* r,
-                     double* norm, cudaStream_t st);
+                     double* norm, const int* long_rows, int nlong_rows, cudaStream_t st);
 void launch_axpy_to(int n, const double* x, const double* dx, double* out, cudaStream_t st);
 
 }  // namespace nclb

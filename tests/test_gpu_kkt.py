@@ -203,3 +203,29 @@ def test_gpu_full_size_against_oracle(spec, form):
     o = O.OrcKkt(prob, form).solve(case, 0.0)
     check_same_decisions(g, o, borderline=lambda: pre_refinement_residual(prob, form, case))
     assert step_err(g, o) <= STEP_RTOL
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("form", ("k2r", "k1s"))
+def test_gpu_long_sums_match_oracle(form):
+    """the whole SCOPF system as one instance: the coupling set-points appear in
+    every contingency block, so K slots with hundreds of refill terms, rhs
+    columns with hundreds of Jacobian entries and residual rows longer than
+    256 entries take the warp-per-sum kernels (kkt_kernels.cu *_long) -- still
+    bitwise the reference's K and within tolerance on the step"""
+    from paper_2510_05885_b200 import scopf as SC
+    D = SC.scopf_data(14, 160, 3)
+    inst = SC.subproblem(D, 0, D.K, True)
+    prob = O.Problem(inst.name, inst.nt, inst.ns, inst.m_eq, inst.m, inst.hp_ptr, inst.hp_idx,
+                     inst.jp_ptr, inst.jp_idx)
+    assert np.bincount(np.asarray(inst.jp_idx), minlength=inst.nt).max() > 64  # long rhs columns
+    ctx = gpu_context(prob, form)
+    Q = O.OrcKkt(prob, form)
+    cs = SC.scopf_case(inst, 5)
+    case = O.KktCase(*(cs[k] for k in ("hval", "jval", "sigma", "rbar1", "rbar2", "rbar3")), cs["rho"])
+    g, o = ctx.solve(gpu_input(case), 0.0), Q.solve(case, 0.0)
+    cp, _, v = ctx.matrix()
+    assert np.diff(cp).max() > 0
+    assert np.array_equal(bits(v), bits(Q.matrix()[2]))
+    check_same_decisions(g, o, borderline=lambda: pre_refinement_residual(prob, form, case))
+    assert step_err(g, o) <= STEP_RTOL
