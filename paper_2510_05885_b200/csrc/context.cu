@@ -57,6 +57,8 @@ struct FactorInfo {
 };
 
 // ---------------------------------------------------------------------------
+constexpr int kSmallSolveMinFronts = 8;
+
 class LdlSystem {
  public:
   // S: the reference's symbolic analysis (exposed, and the layout factors()
@@ -212,6 +214,13 @@ class LdlSystem {
   }
 
   int nlevels() const { return static_cast<int>(sn_.lvl_ptr.size()) - 1; }
+  // a warp per front for levels of many small fronts; a level of a few
+  // fronts (the dense Schur system: one 118-row front) takes the cluster
+  // solve, which spreads each front over up to 16 CTAs
+  bool small_solve(int l) const {
+    return lvl_fmax_[l] <= small_solve_limit() &&
+           (lvl_fmax_[l] <= 32 || sn_.lvl_ptr[l + 1] - sn_.lvl_ptr[l] >= kSmallSolveMinFronts);
+  }
   long long launches() const { return launches_; }
 
   FactorInfo read_factor_info() {
@@ -241,7 +250,7 @@ class LdlSystem {
         launch_uv_partial(sd_, uvec_.p, s, sn_.f[s], sn_.usplit_ng[s], st_);
         launches_ += 1;
       }
-      if (lvl_fmax_[l] <= small_solve_limit()) {
+      if (small_solve(l)) {
         launch_fwd_small(sd_, lval_.p, wp_.p, uvec_.p, lvl_nodes_.p + sn_.lvl_ptr[l],
                          sn_.lvl_ptr[l + 1] - sn_.lvl_ptr[l], lvl_fmax_[l], st_);
         continue;
@@ -257,7 +266,7 @@ class LdlSystem {
   }
   void bwd_seq(double* x) {
     for (int l = nlevels() - 1; l >= 0; --l) {
-      if (lvl_fmax_[l] <= small_solve_limit()) {
+      if (small_solve(l)) {
         launch_bwd_small(sd_, lval_.p, d_.p, wp_.p, xp_.p, lvl_nodes_.p + sn_.lvl_ptr[l],
                          sn_.lvl_ptr[l + 1] - sn_.lvl_ptr[l], lvl_fmax_[l], st_);
         continue;
