@@ -141,7 +141,16 @@ class LdlSystem {
     }
     launches_ += npaths() > 0 ? 1 : 0;
     const auto& T = sn_;
+    // diagnostic (NCL_LEVEL_TIMES=1, with NCL_NO_GRAPH=1): device time per level
+    static const bool lvl_times = std::getenv("NCL_LEVEL_TIMES") != nullptr;
+    std::vector<cudaEvent_t> lev;
+    if (lvl_times) {
+      lev.resize(static_cast<size_t>(nlevels()) + 1);
+      for (auto& e : lev) CK(cudaEventCreate(&e));
+      CK(cudaEventRecord(lev[0], st_));
+    }
     for (int l = 0; l < nlevels(); ++l) {
+      if (lvl_times && l > 0) CK(cudaEventRecord(lev[l], st_));
       for (int s : lvl_split_[l]) {  // fronts with very many children: group sums first
         launch_cc_partial(sd_, fd, s, T.f[s], T.split_ng[s], st_);
         launches_ += 1;
@@ -190,6 +199,18 @@ class LdlSystem {
         launches_ += (np > 0) + (ns > 0 || nd > 0) + (nt > 0);
       }
       if (g1 > g0) CK(cudaStreamWaitEvent(st_, ev_rest(g1 - 1), 0));  // join before the next level
+    }
+    if (lvl_times) {
+      CK(cudaEventRecord(lev[nlevels()], st_));
+      CK(cudaStreamSynchronize(st_));
+      std::fprintf(stderr, "[ncl level times] us:");
+      for (int l = 0; l < nlevels(); ++l) {
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, lev[l], lev[l + 1]));
+        std::fprintf(stderr, " %d:%.0f", l, ms * 1e3f);
+      }
+      std::fprintf(stderr, "\n");
+      for (auto& e : lev) cudaEventDestroy(e);
     }
     CK(cudaGetLastError());
   }

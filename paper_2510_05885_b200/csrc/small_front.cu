@@ -75,7 +75,42 @@ k_small_front(SnDev sd, FactorDev fd, const double* __restrict__ kval,
   const int kp = s == sd.schur ? 0 : k;
   const size_t ld = wide_ld(f);
   double* F = fd.lval + sd.l_off[s];
-  for (int J = 0; J < f; ++J) small_assemble_col(sd, fd, kval, s, c0, k, f, J, S + J * LDS);
+  if (sd.split_ng[s]) {
+    for (int J = 0; J < f; ++J) small_assemble_col(sd, fd, kval, s, c0, k, f, J, S + J * LDS);
+  } else {
+    // whole-front assembly: zero, every A entry of the front at once, then the
+    // children one by one with all of a child's loads in flight (a column-
+    // by-column pass waits one L2 round trip per child column); per position
+    // the same order as the column pass: A, then the children in order
+    for (int J = 0; J < f; ++J)
+      for (int r = lane; r < f; r += 32) S[J * LDS + r] = 0.0;
+    __syncwarp();
+    for (int q = sd.asm_ptr[s] + lane; q < sd.asm_ptr[s + 1]; q += 32) {
+      const int pos = sd.asm_pos[q];
+      S[(pos >> 16) * LDS + (pos & 0xffff)] += __ldg(kval + sd.asm_slot[q]);
+    }
+    __syncwarp();
+    for (int cc = sd.ch_ptr[s]; cc < sd.ch_ptr[s + 1]; ++cc) {
+      const int c = sd.ch[cc];
+      const int fu = f_minus_k(sd, c);
+      const size_t uld = sd.u_ld[c];
+      const double* U = (sd.wide[c] ? fd.lval : fd.upd) + sd.u_off[c];
+      const int* rel = sd.rel + sd.rel_ptr[c];
+      int ri[R];  // this lane's rows of the child, as front positions
+#pragma unroll
+      for (int r = 0; r < R; ++r) ri[r] = lane + 32 * r < fu ? rel[lane + 32 * r] : 0;
+#pragma unroll 4
+      for (int j = 0; j < fu; ++j) {
+        const int cj = rel[j];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const int i = lane + 32 * r;
+          if (i >= j && i < fu) S[cj * LDS + ri[r]] += __ldcg(U + i + j * uld);
+        }
+      }
+      __syncwarp();
+    }
+  }
   __syncwarp();
   int npos = 0, nneg = 0, pert = 0;
   bool bad = false;
