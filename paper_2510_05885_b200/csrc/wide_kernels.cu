@@ -171,13 +171,44 @@ __device__ __noinline__ void assemble_col(const SnDev& sd, const FactorDev& fd,
     }
     __syncwarp();
   } else {
-    for (int e = e0; e < e1; ++e) {
-      const long long ub = sd.cc_ubase[e];
-      const int rb = sd.cc_rbase[e], cw = sd.cc_cnt[e];
-      const int cnt = cw & ((1 << 30) - 1);
-      const double* U = ((cw >> 30) ? fd.lval : fd.upd) + ub;
-      const int* rel = sd.rel + rb;
-      for (int i = lane; i < cnt; i += 32) a[rel[i]] += __ldcg(U + i);
+    // contributions in groups of four: the four children's column segments
+    // are loaded together, then added one child after the other (a warp
+    // barrier each); per position the order is fixed by (32-row chunk, child),
+    // so sums are deterministic, though not child by child for columns
+    // taller than 32 rows
+    constexpr int G = 4;
+    for (int eg = e0; eg < e1; eg += G) {
+      const double* U[G];
+      const int* rel[G];
+      int cnt[G], mc = 0;
+#pragma unroll
+      for (int t = 0; t < G; ++t) {
+        const int e = eg + t;
+        cnt[t] = 0;
+        U[t] = nullptr;
+        rel[t] = nullptr;
+        if (e < e1) {
+          const int cw = sd.cc_cnt[e];
+          cnt[t] = cw & ((1 << 30) - 1);
+          U[t] = ((cw >> 30) ? fd.lval : fd.upd) + sd.cc_ubase[e];
+          rel[t] = sd.rel + sd.cc_rbase[e];
+          mc = max(mc, cnt[t]);
+        }
+      }
+      for (int i = lane; i < mc; i += 32) {
+        double v[G];
+        int r[G];
+#pragma unroll
+        for (int t = 0; t < G; ++t) {
+          v[t] = i < cnt[t] ? __ldcg(U[t] + i) : 0.0;
+          r[t] = i < cnt[t] ? rel[t][i] : -1;
+        }
+#pragma unroll
+        for (int t = 0; t < G; ++t) {
+          if (r[t] >= 0) a[r[t]] += v[t];
+          __syncwarp(__activemask());
+        }
+      }
       __syncwarp();
     }
   }
