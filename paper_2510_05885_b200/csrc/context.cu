@@ -259,14 +259,45 @@ class LdlSystem {
   // 1) and the warp-tier flags are cleared at the start of every forward
   // pass, so a whole solve is one argument-free CUDA graph from the second
   // call on; the caller's vectors are copied in / out around it.
+  // NCL_LEVEL_TIMES diagnostic: events between the phases of a sequence
+  struct PhaseTimer {
+    bool on;
+    cudaStream_t st;
+    std::vector<cudaEvent_t> ev;
+    explicit PhaseTimer(cudaStream_t s) : on(std::getenv("NCL_LEVEL_TIMES") != nullptr), st(s) { mark(); }
+    void mark() {
+      if (!on) return;
+      cudaEvent_t e;
+      CK(cudaEventCreate(&e));
+      CK(cudaEventRecord(e, st));
+      ev.push_back(e);
+    }
+    void report(const char* what) {
+      if (!on) return;
+      mark();
+      CK(cudaStreamSynchronize(st));
+      std::fprintf(stderr, "[ncl %s times] us:", what);
+      for (size_t i = 0; i + 1 < ev.size(); ++i) {
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, ev[i], ev[i + 1]));
+        std::fprintf(stderr, " %.0f", ms * 1e3f);
+      }
+      std::fprintf(stderr, "\n");
+      for (auto e : ev) cudaEventDestroy(e);
+    }
+  };
+
   void fwd_seq(const double* b) {
+    PhaseTimer pt(st_);
     launch_permute_in(N_, perm_.p, b, wp_.p, st_);
     if (npaths()) {
       CK(cudaMemsetAsync(counter_.p, 0, sizeof(int), st_));
       CK(cudaMemsetAsync(flags_.p, 0, sizeof(int) * flags_.n, st_));
       launch_fwd_warp(sd_, lval_.p, wp_.p, uvec_.p, flags_.p, 2, counter_.p, npaths(), sgrid_, st_);
     }
+    pt.mark();
     for (int l = 0; l < nlevels(); ++l) {
+      if (l) pt.mark();
       for (int s : lvl_usplit_[l]) {
         launch_uv_partial(sd_, uvec_.p, s, sn_.f[s], sn_.usplit_ng[s], st_);
         launches_ += 1;
@@ -282,11 +313,14 @@ class LdlSystem {
       if (used == 0) throw CudaError("k_fwd_front: no cluster configuration fits");
       solve_cluster_[l] = used;
     }
+    pt.report("fwd (warp, levels)");
     launches_ += 1 + (npaths() > 0 ? 1 : 0) + nlevels();
     CK(cudaGetLastError());
   }
   void bwd_seq(double* x) {
+    PhaseTimer pt(st_);
     for (int l = nlevels() - 1; l >= 0; --l) {
+      if (l < nlevels() - 1) pt.mark();
       if (small_solve(l)) {
         launch_bwd_small(sd_, lval_.p, d_.p, wp_.p, xp_.p, lvl_nodes_.p + sn_.lvl_ptr[l],
                          sn_.lvl_ptr[l + 1] - sn_.lvl_ptr[l], lvl_fmax_[l], st_);
@@ -299,12 +333,14 @@ class LdlSystem {
       if (used == 0) throw CudaError("k_bwd_front: no cluster configuration fits");
       solve_cluster_[l] = used;
     }
+    pt.mark();
     if (npaths()) {
       CK(cudaMemsetAsync(counter_.p, 0, sizeof(int), st_));
       launch_bwd_warp(sd_, lval_.p, d_.p, wp_.p, xp_.p, flags_.p, 3, wide_.p, counter_.p,
                       npaths(), sgrid_, st_);
     }
     launch_permute_out(N_, perm_.p, xp_.p, x, st_);
+    pt.report("bwd (levels top-down, warp)");
     launches_ += 1 + (npaths() > 0 ? 1 : 0) + nlevels();
     CK(cudaGetLastError());
   }

@@ -119,6 +119,15 @@ __device__ __forceinline__ double ldcg_pin(const double* p) {
   return v;
 }
 
+// Programmatic dependent launch (launches with
+// cudaLaunchAttributeProgrammaticStreamSerialization): let the next kernel of
+// the stream be scheduled now, and wait here until the previous kernel has
+// completed and its writes are visible (no-ops for ordinary launches)
+__device__ __forceinline__ void pdl_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 __device__ __forceinline__ void flag_wait_done() {
   __syncwarp();
   asm volatile("" ::: "memory");

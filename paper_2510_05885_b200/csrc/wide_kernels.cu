@@ -31,6 +31,7 @@
 // k_wide_update) so one front spreads over every SM.
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
+#include <cstdlib>
 #include <stdint.h>
 
 #include "device.cuh"
@@ -478,6 +479,8 @@ k_wide_front(SnDev sd, FactorDev fd, const double* __restrict__ kval,
   const int c0 = sd.first[s], k = sd.first[s + 1] - c0, f = sd.f[s];
   const size_t ld = wide_ld(f);
   double* F = fd.lval + sd.l_off[s];
+  pdl_launch_dependents();
+  pdl_wait();  // the children's update blocks (previous level)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int grp = warp >> 2, gt = threadIdx.x & 127;
   const bool tr = trace && rank == 0 && threadIdx.x == 0;
@@ -676,13 +679,15 @@ int launch_wide_front(const SnDev& sd, const FactorDev& fd, const double* kval, 
     cfg.blockDim = dim3(kThreads);
     cfg.dynamicSmemBytes = static_cast<size_t>(wide_front_smem(max_f));
     cfg.stream = st;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = static_cast<unsigned>(cluster);
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // device: pdl_wait()
+    attr[1].val.programmaticStreamSerializationAllowed = std::getenv("NCL_NO_PDL") == nullptr ? 1 : 0;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = 2;
     int nclusters = 0;
     cudaError_t e = cudaOccupancyMaxActiveClusters(&nclusters, k_wide_front, &cfg);
     if (e != cudaSuccess || nclusters < 1) {

@@ -21,6 +21,7 @@
 // No atomics on values; every sum has a fixed order (bitwise reproducible).
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
+#include <cstdlib>
 #include <stdint.h>
 
 #include "device.cuh"
@@ -94,6 +95,11 @@ k_fwd_front(SnDev sd, const double* __restrict__ lval, double* w, double* uvec,
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   double* u = uvec + sd.rel_ptr[s];
   const int kp = s == sd.schur ? 0 : k;  // Schur mode: assemble the coupling rhs only
+  pdl_launch_dependents();
+  // the children's update vectors (previous level) are read by rank 0 only,
+  // after its first L11 stage is in flight; the other CTAs read nothing of
+  // the previous level before the cluster barrier that follows rank 0's work
+  if (rank == 0 && !(k > 0)) pdl_wait();
   // big pivot blocks: the L11 solve itself is spread over the cluster
   // (per 32-block: rank 0's chain, then every CTA's share of the rows below)
   const bool par = PAR && kp >= kParK && C > 1;
@@ -107,6 +113,7 @@ k_fwd_front(SnDev sd, const double* __restrict__ lval, double* w, double* uvec,
       cp_commit();
     };
     if (kp > 0 && !par) issue(0, 0, 0);
+    pdl_wait();
     for (int r = tid; r < f; r += kSolveThreads) T[r] = r < k ? __ldcg(w + c0 + r) : 0.0;
     __syncthreads();
     if (const int ng = sd.usplit_ng[s]) {  // group sums (split.cu), in group order
@@ -294,6 +301,8 @@ k_bwd_front(SnDev sd, const double* __restrict__ lval, const double* __restrict_
   const double* L = lval + sd.l_off[s];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int* rows = sd.rows + sd.rows_ptr[s];
+  pdl_launch_dependents();
+  pdl_wait();  // the parent's solution rows (previous level)
   if (k == 0 || s == sd.schur) return;  // Schur mode: coupling solution set by the host
   for (int r = k + tid; r < f; r += kSolveThreads) X[r] = __ldcg(x + rows[r]);
   __syncthreads();
@@ -457,6 +466,12 @@ k_bwd_front(SnDev sd, const double* __restrict__ lval, const double* __restrict_
 }
 
 // ---------------------------------------------------------------------------
+// programmatic dependent launch of the level kernels (NCL_NO_PDL=1: off)
+static bool pdl_enabled() {
+  static const bool on = std::getenv("NCL_NO_PDL") == nullptr;
+  return on;
+}
+
 template <typename Kern, typename... Args>
 static int launch_clustered(Kern kern, int count, int cluster, size_t smem, cudaStream_t st,
                             Args... args) {
@@ -466,13 +481,15 @@ static int launch_clustered(Kern kern, int count, int cluster, size_t smem, cuda
     cfg.blockDim = dim3(kSolveThreads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = static_cast<unsigned>(cluster);
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // device: pdl_wait()
+    attr[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = 2;
     int ncl = 0;
     if (cudaOccupancyMaxActiveClusters(&ncl, kern, &cfg) != cudaSuccess || ncl < 1) {
       cudaGetLastError();
