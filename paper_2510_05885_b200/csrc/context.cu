@@ -137,7 +137,8 @@ class LdlSystem {
     if (sn_.path_ptr.size() > 1) {
       CK(cudaMemsetAsync(counter_.p, 0, sizeof(int), st_));
       CK(cudaMemsetAsync(flags_.p, 0, sizeof(int) * flags_.n, st_));
-      launch_factor_warp(sd_, fd, kval, flags_.p, 1, counter_.p, npaths(), eps, grid_, st_);
+      launch_factor_warp(sd_, fd, kval, flags_.p, 1, counter_.p, npaths(), eps,
+                         pipe_ ? grid_ : lgrid_, pipe_, st_);
     }
     launches_ += npaths() > 0 ? 1 : 0;
     const auto& T = sn_;
@@ -748,8 +749,15 @@ class LdlSystem {
     sd_.poff = poff_.p;
     sd_.wide = wide_.p;
     sd_.schur = T.schur;
-    grid_ = warp_tier_grid(false);
-    sgrid_ = warp_tier_grid(true);
+    grid_ = warp_tier_grid(0);
+    sgrid_ = warp_tier_grid(1);
+    lgrid_ = warp_tier_grid(2);
+    {  // long chains: the pipelined walk; only short paths: the lean one
+      int longest = 0;
+      for (size_t p = 0; p + 1 < T.path_ptr.size(); ++p)
+        longest = std::max(longest, T.path_ptr[p + 1] - T.path_ptr[p]);
+      pipe_ = longest >= kFrontPathLen;
+    }
     CK(cudaStreamSynchronize(st_));
   }
 
@@ -758,7 +766,8 @@ class LdlSystem {
   Supernodal sn_;
   cudaStream_t st_;
   int N_ = 0;
-  int grid_ = 1, sgrid_ = 1;  // warp-tier factor / solve grids (resident CTAs)
+  int grid_ = 1, sgrid_ = 1, lgrid_ = 1;  // warp-tier factor / solve / lean-factor grids (resident CTAs)
+  bool pipe_ = true;                       // pipelined warp-tier factor walk (long chains)
   int epoch_ = 1;  // the factorization uses epoch 1, solves 2, 3, ...
   bool use_graph_ = std::getenv("NCL_NO_GRAPH") == nullptr;
   int nfact_ = 0;

@@ -25,7 +25,7 @@ constexpr int kLongSum = 64;  // in-order sums longer than this: a warp each
 // ldl_kernels.cu
 void launch_factor_warp(const SnDev& sd, const FactorDev& fd, const double* kval,
                         int* flags, int epoch, int* counter, int npaths,
-                        double eps, int grid, cudaStream_t st);
+                        double eps, int grid, bool pipe, cudaStream_t st);
 // wide_kernels.cu
 // returns the cluster size used (0: launch impossible); max_f = largest
 // front of the level (sizes the per-warp assembly accumulators)
@@ -69,7 +69,7 @@ void launch_permute_in(int n, const int* perm, const double* b, double* w,
                        cudaStream_t st);
 void launch_permute_out(int n, const int* perm, const double* xp, double* x,
                         cudaStream_t st);
-int warp_tier_grid(bool solves);
+int warp_tier_grid(int which);  // resident CTAs: 0 factor (pipelined), 1 solves, 2 factor (lean)
 void launch_cc_partial(const SnDev& sd, const FactorDev& fd, int s, int f, int ng, cudaStream_t st);
 void launch_uv_partial(const SnDev& sd, const double* uvec, int s, int f, int ng, cudaStream_t st);  // resident CTAs of the factor / solve kernels
 

@@ -106,7 +106,7 @@ constexpr size_t kWarpFactorBytes = sizeof(double) * kWarpFactorDoubles;
 // pivot is shuffled out as soon as its column is updated, and l = u * (1/d)
 // with the wide tier's reciprocal.  l is written to column p of the shared
 // front F, d stays in lane p (myd, perturbed flag mypf).
-template <int NC>
+template <int NC, int BATCH>
 __device__ __forceinline__ void warp_pivots(double (&fr)[kWF + 1], double* F, double* cb, int k, int f,
                                             double eps, int lane, double& myd, bool& mypf, int& fail) {
   double dnext = __shfl_sync(0xffffffffu, fr[0], 0);
@@ -125,16 +125,22 @@ __device__ __forceinline__ void warp_pivots(double (&fr)[kWF + 1], double* F, do
     if (mine) F[p * kFLD + lane] = l;
     fail |= !isfinite(l);
     __syncwarp();
-    double2 v[NC / 2];
-    v[0].y = cbp[1];
+    // column values in batches of BATCH (128-bit loads): bounded registers
+    constexpr int B = NC < BATCH ? NC : BATCH;
 #pragma unroll
-    for (int j = 2; j < NC; j += 2) v[j / 2] = *reinterpret_cast<const double2*>(cbp + j);
-    fr[0] = fr[1] - l * v[0].y;
-    dnext = __shfl_sync(0xffffffffu, fr[0], (p + 1) & 31);
+    for (int j0 = 0; j0 < NC; j0 += B) {
+      double2 v[B / 2];  // issued before the dependent chain of the batch
 #pragma unroll
-    for (int j = 2; j < NC; j += 2) {
-      fr[j - 1] = fr[j] - l * v[j / 2].x;
-      fr[j] = fr[j + 1] - l * v[j / 2].y;
+      for (int j = 0; j < B; j += 2) v[j / 2] = *reinterpret_cast<const double2*>(cbp + j0 + j);
+      if (j0 == 0) {  // the next pivot's column first, then its diagonal out
+        fr[0] = fr[1] - l * v[0].y;
+        dnext = __shfl_sync(0xffffffffu, fr[0], (p + 1) & 31);
+      }
+#pragma unroll
+      for (int j = (j0 == 0 ? 2 : 0); j < B; j += 2) {
+        fr[j0 + j - 1] = fr[j0 + j] - l * v[j / 2].x;
+        fr[j0 + j] = fr[j0 + j + 1] - l * v[j / 2].y;
+      }
     }
     fr[NC - 1] = 0.0;
   }
@@ -174,7 +180,11 @@ __device__ __forceinline__ void load_fidx(const SnDev& sd, const WRec& R, int la
   X.myrel = (lane >= R.k && lane < R.f) ? ldg_pin(sd.rel + R.relp + lane - R.k) : 0;
 }
 
-__global__ void __launch_bounds__(kWarpsPerCta * 32)
+// PIPE: the software pipeline along the path (long chains: latency-bound).
+// !PIPE: each node's index words loaded at its start, fewer registers and
+// three CTAs per SM (many short paths: throughput-bound, e.g. SCOPF blocks).
+template <bool PIPE>
+__global__ void __launch_bounds__(kWarpsPerCta * 32, PIPE ? 0 : 3)
 k_factor_warp(SnDev sd, FactorDev fd, const double* __restrict__ kval,
               int* flags, int epoch, int* counter, int npaths, double eps) {
   extern __shared__ double wsm[];
@@ -206,9 +216,9 @@ k_factor_warp(SnDev sd, FactorDev fd, const double* __restrict__ kval,
     int heavy = -1;
 #if defined(NCL_WTRACE) || defined(NCL_WTRACE_DEAD)
 #ifdef NCL_WTRACE
-    const bool trc = pi == 0;  // the longest root path is handed out first
+    const bool trc = PIPE && pi == 0;  // the longest root path is handed out first
 #else
-    const bool trc = pi == 0 && epoch == 0x7fffffff;
+    const bool trc = PIPE && pi == 0 && epoch == 0x7fffffff;
 #endif
     if (trc && lane == 0) g_wtime[1] = gtimer();
     unsigned long long tph[11] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
@@ -236,6 +246,12 @@ k_factor_warp(SnDev sd, FactorDev fd, const double* __restrict__ kval,
       const int k = R.k, f = R.f;
       WRec Rn = R;
       if (!top) Rn = load_rec(sd, q + 1);
+      if (!PIPE && q > pb) {
+        load_fidx(sd, R, lane, X);
+        fl = (X.chid >= 0 && X.chid != heavy) ? ld_relaxed(flags + X.chid) : epoch;
+#pragma unroll
+        for (int t = 0; t < kLtA; ++t) av[t] = X.ap[t] >= 0 ? ldg_pin(kval + X.as[t]) : 0.0;
+      }
       WT(0);
       if (X.chid >= 0 && X.chid != heavy && fl != epoch)
         wait_flag(flags + X.chid, epoch);
@@ -284,19 +300,22 @@ k_factor_warp(SnDev sd, FactorDev fd, const double* __restrict__ kval,
       const int myrel = X.myrel;
       // node q+1's index loads, in flight during the pivots
       WT(6);
-      if (!top) load_fidx(sd, Rn, lane, X);
+      if (PIPE && !top) load_fidx(sd, Rn, lane, X);
       WT(7);
       double myd = 0.0;
       bool mypf = false;
+      // (the pipelined walk loads a pivot's whole column at once; the lean
+      // one in halves, to stay within three CTAs' registers)
+      constexpr int kBatch = PIPE ? kWF : 16;
       if (f <= 8)
-        warp_pivots<8>(fr, F, cb, k, f, eps, lane, myd, mypf, fail);
+        warp_pivots<8, kBatch>(fr, F, cb, k, f, eps, lane, myd, mypf, fail);
       else if (f <= 16)
-        warp_pivots<16>(fr, F, cb, k, f, eps, lane, myd, mypf, fail);
+        warp_pivots<16, kBatch>(fr, F, cb, k, f, eps, lane, myd, mypf, fail);
       else
-        warp_pivots<kWF>(fr, F, cb, k, f, eps, lane, myd, mypf, fail);
+        warp_pivots<kWF, kBatch>(fr, F, cb, k, f, eps, lane, myd, mypf, fail);
       WT(8);
       // node q+1's light-child flags (its heavy child is this node)
-      if (!top) {
+      if (PIPE && !top) {
         fl = (X.chid >= 0 && X.chid != R.s) ? ld_relaxed(flags + X.chid) : epoch;
 #pragma unroll
         for (int t = 0; t < kLtA; ++t) av[t] = X.ap[t] >= 0 ? ldg_pin(kval + X.as[t]) : 0.0;
@@ -594,16 +613,22 @@ __global__ void k_permute_out(int n, const int* __restrict__ perm,
 // launch helpers (host)
 void launch_factor_warp(const SnDev& sd, const FactorDev& fd, const double* kval,
                         int* flags, int epoch, int* counter, int npaths,
-                        double eps, int grid, cudaStream_t st) {
+                        double eps, int grid, bool pipe, cudaStream_t st) {
   if (npaths == 0) return;
   static bool init = false;
   if (!init) {
-    cudaFuncSetAttribute(k_factor_warp, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(k_factor_warp<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(kWarpsPerCta * kWarpFactorBytes));
+    cudaFuncSetAttribute(k_factor_warp<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(kWarpsPerCta * kWarpFactorBytes));
     init = true;
   }
-  k_factor_warp<<<grid, kWarpsPerCta * 32, kWarpsPerCta * kWarpFactorBytes, st>>>(
-      sd, fd, kval, flags, epoch, counter, npaths, eps);
+  if (pipe)
+    k_factor_warp<true><<<grid, kWarpsPerCta * 32, kWarpsPerCta * kWarpFactorBytes, st>>>(
+        sd, fd, kval, flags, epoch, counter, npaths, eps);
+  else
+    k_factor_warp<false><<<grid, kWarpsPerCta * 32, kWarpsPerCta * kWarpFactorBytes, st>>>(
+        sd, fd, kval, flags, epoch, counter, npaths, eps);
 #ifdef NCL_WTRACE  // diagnostic build: phase cycles of the last path's warp (NCL_NO_GRAPH=1)
   {
     unsigned long long t[11], tt[4];
@@ -612,8 +637,8 @@ void launch_factor_warp(const SnDev& sd, const FactorDev& fd, const double* kval
     cudaMemcpyFromSymbol(tt, g_wtime, sizeof(tt));
     std::fprintf(stderr, "[ncl wtime] spine starts %.3f ms, ends %.3f ms, other paths end %.3f ms\n",
                  (tt[1] - tt[0]) * 1e-6, (tt[2] - tt[0]) * 1e-6, (tt[3] - tt[0]) * 1e-6);
-    const unsigned long long init[4] = {~0ull, 0, 0, 0};
-    cudaMemcpyToSymbol(g_wtime, init, sizeof(init));
+    const unsigned long long init2[4] = {~0ull, 0, 0, 0};
+    cudaMemcpyToSymbol(g_wtime, init2, sizeof(init2));
     std::fprintf(stderr,
                  "[ncl wtrace] static %llu flags %llu A %llu light %llu fr %llu fidx %llu pivots %llu "
                  "flagpf %llu Lstore %llu d+stats %llu next %llu\n",
@@ -660,20 +685,24 @@ void launch_permute_out(int n, const int* perm, const double* xp, double* x,
   k_permute_out<<<(n + 255) / 256, 256, 0, st>>>(n, perm, xp, x);
 }
 
-int warp_tier_grid(bool solves) {
+int warp_tier_grid(int which) {
   int dev = 0, sms = 0, per_sm = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  if (solves) {
+  if (which == 1) {
     int a = 0, b = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, k_fwd_warp, kWarpsPerCta * 32, 0);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_bwd_warp, kWarpsPerCta * 32, 0);
     per_sm = a < b ? a : b;
   } else {
-    cudaFuncSetAttribute(k_factor_warp, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(kWarpsPerCta * kWarpFactorBytes));
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_factor_warp, kWarpsPerCta * 32,
-                                                  kWarpsPerCta * kWarpFactorBytes);
+    const size_t smem = kWarpsPerCta * kWarpFactorBytes;
+    if (which == 0) {
+      cudaFuncSetAttribute(k_factor_warp<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_factor_warp<true>, kWarpsPerCta * 32, smem);
+    } else {
+      cudaFuncSetAttribute(k_factor_warp<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_factor_warp<false>, kWarpsPerCta * 32, smem);
+    }
   }
   if (per_sm < 1) per_sm = 1;
   return sms * per_sm;

@@ -302,23 +302,37 @@ k_bwd_front(SnDev sd, const double* __restrict__ lval, const double* __restrict_
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int* rows = sd.rows + sd.rows_ptr[s];
   pdl_launch_dependents();
-  pdl_wait();  // the parent's solution rows (previous level)
-  if (k == 0 || s == sd.schur) return;  // Schur mode: coupling solution set by the host
-  for (int r = k + tid; r < f; r += kSolveThreads) X[r] = __ldcg(x + rows[r]);
-  __syncthreads();
+  if (k == 0 || s == sd.schur) {  // Schur mode: coupling solution set by the host
+    pdl_wait();
+    return;
+  }
   // z_p = w_p / d_p - sum_{r >= k} L(r, p) x_r for this CTA's pivot columns,
-  // 32 columns x kRows rows per staged chunk, two columns per warp
+  // 32 columns x kRows rows per staged chunk, two columns per warp.  The
+  // first chunk of L is staged before waiting for the parent's solution rows
+  // (the previous level's output)
   {
     const int pc = (k + C - 1) / C;
     const int pa = rank * pc, pb = min(k, pa + pc);
+    const int nch = (f - k + kRows - 1) / kRows;
+    int shv0 = 0;
+    if (pa < pb && nch > 0) {
+      shv0 = stage_cols(sm.P[0], L, ld, k, min(kRows, f - k), pa, min(kBlk, pb - pa), warp, lane);
+      cp_commit();
+    }
+    pdl_wait();
+    for (int r = k + tid; r < f; r += kSolveThreads) X[r] = __ldcg(x + rows[r]);
+    __syncthreads();
     for (int q0 = pa; q0 < pb; q0 += kBlk) {
       const int nq = min(kBlk, pb - q0);
       double part0 = 0.0, part1 = 0.0;
       int shv[2];
-      const int nch = (f - k + kRows - 1) / kRows;
       if (nch > 0) {
-        shv[0] = stage_cols(sm.P[0], L, ld, k, min(kRows, f - k), q0, nq, warp, lane);
-        cp_commit();
+        if (q0 == pa) {
+          shv[0] = shv0;
+        } else {
+          shv[0] = stage_cols(sm.P[0], L, ld, k, min(kRows, f - k), q0, nq, warp, lane);
+          cp_commit();
+        }
       }
       for (int ci = 0; ci < nch; ++ci) {
         const int bf = ci & 1, r0 = k + ci * kRows, nr = min(kRows, f - r0);
