@@ -251,8 +251,9 @@ def main():
     # ------------------------------------------------ e2e (host buffers)
     pinned = {k: torch.tensor(case[k], dtype=torch.float64).pin_memory() for k in keys}
     host_in = P.KktInput(*[pinned[k].numpy() for k in keys], case["rho"])
+    host_out = tuple(torch.zeros(n, dtype=torch.float64).pin_memory().numpy() for n in (inst.n, inst.m, inst.m))
     e2e_ms = 0.0
-    ctx.solve(host_in, 0.0)
+    ctx.solve(host_in, 0.0, out=host_out)
     if world > 1:
         dist.barrier()
     for _ in range(args.steps):
@@ -261,7 +262,7 @@ def main():
         s = torch.cuda.Event(enable_timing=True)
         e = torch.cuda.Event(enable_timing=True)
         s.record(stream)
-        stp = ctx.solve(host_in, 0.0)
+        stp = ctx.solve(host_in, 0.0, out=host_out)
         e.record(stream)
         e.synchronize()
         e2e_ms += s.elapsed_time(e)

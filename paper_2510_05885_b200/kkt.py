@@ -194,15 +194,21 @@ class KktContext:
     def system_size(self) -> int:
         return int(self.info.n)
 
-    def solve(self, inp: KktInput, warm_delta: float) -> KktStep:
+    def solve(self, inp: KktInput, warm_delta: float, out=None) -> KktStep:
+        """kkt.hpp:61 KktContext::solve.  out: optional caller-owned (dx, dr, dy)
+        float64 arrays to receive the step (e.g. pinned host memory)."""
         hv, jv = f64(inp.hval), f64(inp.jval)
         sg, r1, r2, r3 = f64(inp.sigma), f64(inp.rbar1), f64(inp.rbar2), f64(inp.rbar3)
         if (len(hv) != self.hnnz or len(jv) != self.jnnz or len(sg) != self.n or len(r1) != self.n
                 or len(r2) != self.m or len(r3) != self.m):
             raise ValueError("kkt: input lengths do not match the problem shape")
-        dx = np.zeros(self.n)
-        dr = np.zeros(self.m)
-        dy = np.zeros(self.m)
+        if out is None:
+            dx, dr, dy = np.zeros(self.n), np.zeros(self.m), np.zeros(self.m)
+        else:
+            dx, dr, dy = out
+            if not all(a.dtype == np.float64 and a.flags.c_contiguous for a in out) or \
+                    (len(dx), len(dr), len(dy)) != (self.n, self.m, self.m):
+                raise ValueError("kkt: out must be contiguous float64 arrays of lengths (n, m, m)")
         st = KktStats()
         check(self._L.ncl_kkt_solve(self._h, dp(hv), dp(jv), dp(sg), dp(r1), dp(r2), dp(r3),
                                     float(inp.rho), float(warm_delta), dp(dx), dp(dr), dp(dy),
