@@ -168,7 +168,7 @@ std::string check_warp_schedule(const Supernodal& T);
 // (NCL_HUGE_MIN_F overrides; measured on the 78,400-bus mesh: 7.02 ms per
 // Newton step with the cluster kernel on those levels, 6.47 ms with this path)
 constexpr int kHugeMinF = 256;
-constexpr int kHugeMaxN = 16;
+constexpr int kHugeMaxN = 24;
 bool level_is_huge(int fmax, int nfronts);
 
 }  // namespace nclb
