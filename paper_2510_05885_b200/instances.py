@@ -385,6 +385,74 @@ def elec(npt: int, seed: int) -> Instance:
     return inst
 
 
+class _BearingEval:
+    """COPS 3.0 'bearing' (journal bearing, b = 10, eps = 0.1): pressure v >= 0
+    on an nx x ny interior grid of [0, 2 pi] x [0, 2b], v = 0 on the boundary,
+    minimising sum_edges 0.5 hx hy wq (dv/dh)^2 - hx hy sum_nodes wl v with
+    wq = (1 + eps cos xi)^3 (at edge midpoints), wl = eps sin xi.  Quadratic:
+    the Hessian is the constant weighted 5-point stencil; no constraints (m = 0,
+    so K2r = K1s = H + Sigma + delta I).  Not in the reference (SURVEY.md 8(d)
+    config #2): a repo generator of the COPS shape."""
+
+    def __init__(self, nx, ny, inst):
+        b, eps = 10.0, 0.1
+        self.nx, self.ny = nx, ny
+        hx, hy = 2.0 * np.pi / (nx + 1), 2.0 * b / (ny + 1)
+        xi = hx * np.arange(1, nx + 1)
+        wq_mid = (1.0 + eps * np.cos(hx * (np.arange(nx + 1) + 0.5))) ** 3   # x-edges i -> i+1 (i = 0..nx)
+        wq_node = (1.0 + eps * np.cos(xi)) ** 3                            # y-edges at column xi
+        ax = hy / hx * wq_mid              # weight of an x-edge
+        ay = hx / hy * wq_node             # weight of a y-edge (per column)
+        n = nx * ny
+        diag = np.zeros(n)
+        I = np.arange(nx)
+        for j in range(ny):
+            c = j * nx + I
+            diag[c] += ax[I] + ax[I + 1] + 2.0 * ay[I]
+        self.diag = diag
+        self.offx = -ax[1:nx]              # (i, i+1) inside a grid row
+        self.offy = -ay                    # (j, j+1) per column i
+        self.lin = -hx * hy * eps * np.sin(xi)
+        self.inst = inst
+
+    def hval(self):
+        nx, ny = self.nx, self.ny
+        ptr = self.inst.hp_ptr
+        c = np.arange(nx * ny)
+        i, j = c % nx, c // nx
+        hx_, hy_ = i + 1 < nx, j + 1 < ny
+        h = np.empty(int(ptr[-1]))
+        h[ptr[:-1]] = self.diag
+        h[ptr[:-1][hx_] + 1] = self.offx[i[hx_]]
+        h[ptr[:-1][hy_] + 1 + hx_[hy_]] = self.offy[i[hy_]]
+        return h
+
+    def eval(self, t, y):
+        import scipy.sparse as sp
+        h = self.hval()
+        n = len(t)
+        ip, ix = self.inst.hp_ptr, self.inst.hp_idx
+        L = sp.csc_matrix((h, ix, ip), shape=(n, n))
+        g = L @ t + L.T @ t - h[ip[:-1]] * t   # symmetric product from the lower triangle
+        return h, np.zeros(0), g + np.tile(self.lin, self.ny), np.zeros(0)
+
+
+def bearing(nx: int, ny: int) -> Instance:
+    n = nx * ny
+    c = np.arange(n)
+    has_x, has_y = (c % nx) + 1 < nx, (c // nx) + 1 < ny
+    cnt = 1 + has_x.astype(np.int32) + has_y.astype(np.int32)
+    hp_ptr = np.zeros(n + 1, np.int32)
+    hp_ptr[1:] = np.cumsum(cnt)
+    hp_idx = np.empty(int(hp_ptr[-1]), np.int32)
+    hp_idx[hp_ptr[:-1]] = c
+    hp_idx[hp_ptr[:-1][has_x] + 1] = c[has_x] + 1
+    hp_idx[hp_ptr[:-1][has_y] + 1 + has_x[has_y]] = c[has_y] + nx
+    inst = Instance(f"bearing:{nx}:{ny}", n, 0, 0, 0, hp_ptr, hp_idx, np.zeros(1, np.int32),
+                    np.zeros(0, np.int32), np.zeros(n), np.full(n, np.inf), np.full(n, 0.5))
+    inst.evaluator = _BearingEval(nx, ny, inst)
+    return inst
+
 def rng_bits(seed: int, k: int) -> np.ndarray:
     """k draws of problems.cpp:20-23's u = (gen() >> 11) * 2^-53"""
     g = MT19937_64(seed)
@@ -401,6 +469,8 @@ def build(spec: str) -> Instance:
         return mpcc_sep(int(t[1]))
     if t[0] == "elec":
         return elec(int(t[1]), int(t[2]))
+    if t[0] == "bearing":
+        return bearing(int(t[1]), int(t[2]))
     raise ValueError(f"unknown instance spec {spec}")
 
 

@@ -98,7 +98,7 @@ def test_gpu_matches_reference_fixture(path):
 
 
 GEN = ["opf_toy:1500:7", "opf_mesh:30:30:3", "mpcc_sep:2000", "opf_toy:11:2", "opf_mesh:2:3:1",
-       "elec:60:3"]
+       "elec:60:3", "bearing:40:30"]
 
 
 @pytest.mark.parametrize("spec", GEN)

@@ -64,3 +64,21 @@ def test_mesh_is_bushier_than_ring():
         return pl.info.sn_height
 
     assert height("opf_mesh:60:60:1") * 20 < height("opf_toy:3600:1")
+
+
+def test_bearing_is_a_weighted_5_point_stencil():
+    """COPS bearing (repo generator): lower CSC with
+    sorted rows, m = 0, symmetric positive definite Hessian"""
+    import scipy.sparse as sp
+    inst = I.build("bearing:9:7")
+    n = inst.nt
+    assert (inst.m, inst.m_eq, inst.ns) == (0, 0, 0) and n == 63
+    for c in range(n):
+        rows = inst.hp_idx[inst.hp_ptr[c]:inst.hp_ptr[c + 1]]
+        assert rows[0] == c and np.all(np.diff(rows) > 0) and set(rows[1:]) <= {c + 1, c + 9}
+    h, jv, g, cv = inst.evaluator.eval(np.ones(n), np.zeros(0))
+    assert len(jv) == 0 and len(cv) == 0
+    L = sp.csc_matrix((h, inst.hp_idx, inst.hp_ptr), shape=(n, n))
+    A = (L + L.T - sp.diags(L.diagonal())).toarray()
+    assert np.allclose(A, A.T) and np.linalg.eigvalsh(A).min() > 0
+    assert np.allclose(g, A @ np.ones(n) + np.tile(inst.evaluator.lin, 7))

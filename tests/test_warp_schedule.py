@@ -37,6 +37,7 @@ def plan(spec, form):
     ("opf_mesh:12:9:3", "k2"),
     ("mpcc_sep:500", "k2r"),        # many tiny independent trees
     ("elec:60:1", "k2r"),           # dense block: everything wide
+    ("bearing:40:30", "k2r"),       # 2-D grid, no constraints
 ])
 @pytest.mark.parametrize("internal", [0, 1])
 def test_warp_schedule_invariants(spec, form, internal):
