@@ -193,9 +193,9 @@ class LdlSystem {
         CK(cudaEventRecord(ev_panel(g), st_));
         if (g - 1 >= g0) CK(cudaStreamWaitEvent(st_, ev_rest(g - 1), 0));
         launch_wide_update(sd_, fd, tiles_s_.p + T.ts_ptr[g], ns, dg_nodes_.p + T.dg_ptr[g], nd,
-                           g - g0, st_);
+                           g - g0, st_, true);
         CK(cudaStreamWaitEvent(st2_, ev_panel(g), 0));
-        launch_wide_update(sd_, fd, tiles_.p + T.tl_ptr[g], nt, nullptr, 0, g - g0, st2_);
+        launch_wide_update(sd_, fd, tiles_.p + T.tl_ptr[g], nt, nullptr, 0, g - g0, st2_, false);
         CK(cudaEventRecord(ev_rest(g), st2_));
         launches_ += (np > 0) + (ns > 0 || nd > 0) + (nt > 0);
       }

@@ -38,7 +38,7 @@ void launch_wide_assemble(const SnDev& sd, const FactorDev& fd, const double* kv
 void launch_wide_panel(const SnDev& sd, const FactorDev& fd, const int4* tasks, int count,
                        int panel, double eps, cudaStream_t st);
 void launch_wide_update(const SnDev& sd, const FactorDev& fd, const int4* tiles, int count,
-                        const int* fronts, int nd, int panel, cudaStream_t st);
+                        const int* fronts, int nd, int panel, cudaStream_t st, bool pdl);
 void launch_fwd_warp(const SnDev& sd, const double* lval, double* w, double* uvec,
                      int* flags, int epoch, int* counter, int npaths, int grid,
                      cudaStream_t st);

@@ -577,6 +577,8 @@ k_wide_assemble(SnDev sd, FactorDev fd, const double* __restrict__ kval,
                 const int4* __restrict__ tasks) {
   const int4 t = tasks[blockIdx.x];
   const int s = t.x, J = t.y + (threadIdx.x >> 5);
+  pdl_launch_dependents();
+  pdl_wait();  // the previous level (programmatic launch)
   const int c0 = sd.first[s], f = sd.f[s], k = sd.first[s + 1] - c0;
   if (J < min(f, t.y + kAsmCols))
     assemble_col(sd, fd, kval, s, c0, k, f, fd.lval + sd.l_off[s], wide_ld(f), J, nullptr);
@@ -601,6 +603,8 @@ k_wide_panel(SnDev sd, FactorDev fd, const int4* __restrict__ tasks, int panel, 
   double* F = fd.lval + sd.l_off[s];
   const int lo = p1 + rb * kPanelRows, hi = min(f, lo + kPanelRows);
   if (threadIdx.x == 0) sm.prog = 0;
+  pdl_launch_dependents();
+  pdl_wait();  // the previous panel's strip update (programmatic launch)
   __syncthreads();
   if (threadIdx.x < 32) {
     diag_block(F, ld, p0, nb, eps, sm, D, rb == 0 ? fd.d + c0 + p0 : nullptr,
@@ -622,6 +626,8 @@ __global__ void __launch_bounds__(128)
 k_wide_update(SnDev sd, FactorDev fd, const int4* __restrict__ tiles, int count,
               const int* __restrict__ fronts, int nd, int panel) {
   __shared__ __align__(16) GroupSmem G;
+  pdl_launch_dependents();
+  pdl_wait();  // the panel kernel (programmatic launch on the main stream)
   if (blockIdx.x == 0) {
     for (int di = 0; di < nd; ++di) {
       const int s = fronts[di];
@@ -703,9 +709,27 @@ int launch_wide_front(const SnDev& sd, const FactorDev& fd, const double* kval, 
   return 0;
 }
 
+// ordinary launch, or programmatic dependent launch (the kernel waits in
+// pdl_wait() for its predecessor on the stream); NCL_NO_PDL=1 turns it off
+template <typename Kern, typename... Args>
+static void launch_pdl(Kern kern, int grid, int block, size_t smem, cudaStream_t st, bool pdl, Args... args) {
+  static const bool allowed = std::getenv("NCL_NO_PDL") == nullptr;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(grid));
+  cfg.blockDim = dim3(static_cast<unsigned>(block));
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = (pdl && allowed) ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
 void launch_wide_assemble(const SnDev& sd, const FactorDev& fd, const double* kval,
                           const int4* tasks, int count, cudaStream_t st) {
-  if (count) k_wide_assemble<<<count, 256, 0, st>>>(sd, fd, kval, tasks);
+  if (count) launch_pdl(k_wide_assemble, count, 256, 0, st, true, sd, fd, kval, tasks);
 }
 
 void launch_wide_panel(const SnDev& sd, const FactorDev& fd, const int4* tasks, int count,
@@ -716,13 +740,13 @@ void launch_wide_panel(const SnDev& sd, const FactorDev& fd, const int4* tasks, 
     cudaFuncSetAttribute(k_wide_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, tr_bytes);
     init = true;
   }
-  if (count) k_wide_panel<<<count, kHugeRows, tr_bytes, st>>>(sd, fd, tasks, panel, eps);
+  if (count) launch_pdl(k_wide_panel, count, kHugeRows, tr_bytes, st, true, sd, fd, tasks, panel, eps);
 }
 
 void launch_wide_update(const SnDev& sd, const FactorDev& fd, const int4* tiles, int count,
-                        const int* fronts, int nd, int panel, cudaStream_t st) {
+                        const int* fronts, int nd, int panel, cudaStream_t st, bool pdl) {
   const int blocks = count > 0 ? count : (nd > 0 ? 1 : 0);
-  if (blocks) k_wide_update<<<blocks, 128, 0, st>>>(sd, fd, tiles, count, fronts, nd, panel);
+  if (blocks) launch_pdl(k_wide_update, blocks, 128, 0, st, pdl, sd, fd, tiles, count, fronts, nd, panel);
 }
 
 }  // namespace nclb
