@@ -63,13 +63,16 @@ __device__ __forceinline__ void small_assemble_col(const SnDev& sd, const Factor
 template <int R, int W>
 __global__ void __launch_bounds__(W * 32)
 k_small_front(SnDev sd, FactorDev fd, const double* __restrict__ kval,
-              const int* __restrict__ nodes, int count, double eps) {
-  constexpr int FM = 32 * R, LDS = FM + 1;  // conflict-free column-major shared front
+              const int* __restrict__ nodes, int count, double eps, int fm) {
+  // column-major shared front sized for the level's largest front (fm <= 32 R
+  // rows): leading dimension fm + 1 (odd: conflict-free); a level of 48-row
+  // fronts then fits three CTAs per SM instead of one
+  const int LDS = fm + 1;
   extern __shared__ double small_smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int fi = blockIdx.x * W + warp;
   if (fi >= count) return;  // warp-level work only below: no CTA barriers
-  double* S = small_smem + static_cast<size_t>(warp) * FM * LDS;
+  double* S = small_smem + static_cast<size_t>(warp) * fm * LDS;
   const int s = nodes[fi];
   const int c0 = sd.first[s], k = sd.first[s + 1] - c0, f = sd.f[s];
   const int kp = s == sd.schur ? 0 : k;
@@ -273,27 +276,28 @@ k_bwd_small(SnDev sd, const double* __restrict__ lval, const double* __restrict_
 
 // ---------------------------------------------------------------------------
 template <int R, int W>
-static size_t small_front_smem() { return sizeof(double) * W * (32 * R) * (32 * R + 1); }
+static size_t small_front_smem(int fm) { return sizeof(double) * W * fm * (fm + 1); }
 
 int small_factor_limit() { return kSmallFactorF; }
 int small_solve_limit() { return kSmallSolveF; }
 
 template <int R, int W>
 static void small_launch(const SnDev& sd, const FactorDev& fd, const double* kval, const int* nodes,
-                         int count, double eps, cudaStream_t st) {
+                         int count, int fmax, double eps, cudaStream_t st) {
   static bool init = false;
   if (!init) {
     cudaFuncSetAttribute(k_small_front<R, W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(small_front_smem<R, W>()));
+                         static_cast<int>(small_front_smem<R, W>(32 * R)));
     init = true;
   }
-  k_small_front<R, W><<<(count + W - 1) / W, W * 32, small_front_smem<R, W>(), st>>>(sd, fd, kval, nodes,
-                                                                                     count, eps);
+  const int fm = fmax < 1 ? 1 : fmax;
+  k_small_front<R, W><<<(count + W - 1) / W, W * 32, small_front_smem<R, W>(fm), st>>>(sd, fd, kval, nodes,
+                                                                                       count, eps, fm);
 }
 
 void launch_small_front(const SnDev& sd, const FactorDev& fd, const double* kval, const int* nodes,
                         int count, int fmax, double eps, cudaStream_t st) {
-  if (count && fmax <= kSmallFactorF) small_launch<2, 4>(sd, fd, kval, nodes, count, eps, st);
+  if (count && fmax <= kSmallFactorF) small_launch<2, 4>(sd, fd, kval, nodes, count, fmax, eps, st);
 }
 
 void launch_fwd_small(const SnDev& sd, const double* lval, double* w, double* uvec,
