@@ -39,7 +39,7 @@ constexpr int kBlk = 32;
 constexpr int kRows = 240;        // rows per staged panel chunk
 constexpr int kSLP = kRows + 2;   // its column stride in shared memory
 constexpr unsigned kFull = 0xffffffffu;
-constexpr int kParK = 2048;       // pivot blocks from which the L11 solve is cluster-parallel
+constexpr int kParK = 1024;       // pivot blocks from which the L11 solve is cluster-parallel
 
 // dynamic shared memory: the front vector (f doubles) after two panel buffers
 struct SolveSmem {
