@@ -480,9 +480,9 @@ def reference_arm(args, world, rank):
         return
     inst, case = make_workload(args.workload, world=world)
     budget = max(30.0, min(150.0, 6.0 * args.steps))
-    n_warm = min(args.warmup, 1)
-    if n_warm:
-        cpu_reference_run(inst, case, args.form, n_warm, budget)
+    n_warm = max(1, args.warmup)  # the requested warm-up, bounded by the same time budget
+    _, wt, _ = cpu_reference_run(inst, case, args.form, n_warm, budget)
+    n_warm = len(wt)
     kind, times, st = cpu_reference_run(inst, case, args.form, args.steps, budget)
     v = 1e3 * float(np.mean(times))
     out = {
