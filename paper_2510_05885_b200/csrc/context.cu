@@ -613,6 +613,22 @@ class LdlSystem {
       while (c > 1 && nf * c > 2 * sms) c >>= 1;
       lvl_cluster_[l] = c;
     }
+    if (std::getenv("NCL_LEVEL_STATS")) {  // diagnostic: split fronts
+      int ns = 0, nu = 0;
+      for (int q = 0; q < T.nsn; ++q) {
+        ns += T.split_ng[q] > 0;
+        nu += T.usplit_ng[q] > 0;
+      }
+      std::fprintf(stderr, "[ncl split] fronts with split extend-add: %d (factor), %d (forward gather)\n", ns, nu);
+      if (T.schur >= 0) {
+        const int sc = T.schur;
+        int maxc = 0;
+        for (int J = 0; J < T.f[sc]; ++J)
+          maxc = std::max(maxc, T.cc_ptr[T.cc_off[sc] + J + 1] - T.cc_ptr[T.cc_off[sc] + J]);
+        std::fprintf(stderr, "[ncl split] coupling front: f %d, children %d, most contributions per column %d\n",
+                     T.f[sc], T.ch_ptr[sc + 1] - T.ch_ptr[sc], maxc);
+      }
+    }
     if (std::getenv("NCL_LEVEL_STATS")) {  // diagnostic: warp-tier paths, wide-tier levels
       int longest = 0, lp = -1;
       for (int p = 0; p + 1 < static_cast<int>(T.path_ptr.size()); ++p)

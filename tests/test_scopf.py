@@ -221,7 +221,8 @@ def _gpu_check(st, ref, D, sub, G):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("nbus,K,seed,scale", [(30, 8, 3, 1.0), (118, 12, 4, 1.0), (40, 6, 2, -3.0)])
+@pytest.mark.parametrize("nbus,K,seed,scale", [(30, 8, 3, 1.0), (118, 12, 4, 1.0), (40, 6, 2, -3.0),
+                                                 (14, 140, 5, 1.0)])  # >= 128 blocks: split extend-add
 def test_gpu_schur_single_rank_matches_oracle(nbus, K, seed, scale):
     import torch
     D = SC.scopf_data(nbus, K, seed)
