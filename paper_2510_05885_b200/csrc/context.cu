@@ -294,7 +294,8 @@ class LdlSystem {
     if (npaths()) {
       CK(cudaMemsetAsync(counter_.p, 0, sizeof(int), st_));
       CK(cudaMemsetAsync(flags_.p, 0, sizeof(int) * flags_.n, st_));
-      launch_fwd_warp(sd_, lval_.p, wp_.p, uvec_.p, flags_.p, 2, counter_.p, npaths(), sgrid_, st_);
+      launch_fwd_warp(sd_, lval_.p, wp_.p, uvec_.p, flags_.p, 2, counter_.p, npaths(),
+                      pipe_ ? sgrid_ : fgrid_, pipe_, st_);
     }
     pt.mark();
     for (int l = 0; l < nlevels(); ++l) {
@@ -338,7 +339,7 @@ class LdlSystem {
     if (npaths()) {
       CK(cudaMemsetAsync(counter_.p, 0, sizeof(int), st_));
       launch_bwd_warp(sd_, lval_.p, d_.p, wp_.p, xp_.p, flags_.p, 3, wide_.p, counter_.p,
-                      npaths(), sgrid_, st_);
+                      npaths(), pipe_ ? sgrid_ : fgrid_, pipe_, st_);
     }
     launch_permute_out(N_, perm_.p, xp_.p, x, st_);
     pt.report("bwd (levels top-down, warp)");
@@ -768,6 +769,7 @@ class LdlSystem {
     grid_ = warp_tier_grid(0);
     sgrid_ = warp_tier_grid(1);
     lgrid_ = warp_tier_grid(2);
+    fgrid_ = warp_tier_grid(3);
     {  // long chains: the pipelined walk; only short paths: the lean one
       int longest = 0;
       for (size_t p = 0; p + 1 < T.path_ptr.size(); ++p)
@@ -782,7 +784,7 @@ class LdlSystem {
   Supernodal sn_;
   cudaStream_t st_;
   int N_ = 0;
-  int grid_ = 1, sgrid_ = 1, lgrid_ = 1;  // warp-tier factor / solve / lean-factor grids (resident CTAs)
+  int grid_ = 1, sgrid_ = 1, lgrid_ = 1, fgrid_ = 1;  // warp-tier factor / solve / lean-factor grids (resident CTAs)
   bool pipe_ = true;                       // pipelined warp-tier factor walk (long chains)
   int epoch_ = 1;  // the factorization uses epoch 1, solves 2, 3, ...
   bool use_graph_ = std::getenv("NCL_NO_GRAPH") == nullptr;

@@ -40,11 +40,11 @@ void launch_wide_panel(const SnDev& sd, const FactorDev& fd, const int4* tasks, 
 void launch_wide_update(const SnDev& sd, const FactorDev& fd, const int4* tiles, int count,
                         const int* fronts, int nd, int panel, cudaStream_t st, bool pdl);
 void launch_fwd_warp(const SnDev& sd, const double* lval, double* w, double* uvec,
-                     int* flags, int epoch, int* counter, int npaths, int grid,
+                     int* flags, int epoch, int* counter, int npaths, int grid, bool pipe,
                      cudaStream_t st);
 void launch_bwd_warp(const SnDev& sd, const double* lval, const double* d,
                      const double* w, double* x, int* flags, int epoch,
-                     const int8_t* wide, int* counter, int npaths, int grid,
+                     const int8_t* wide, int* counter, int npaths, int grid, bool pipe,
                      cudaStream_t st);
 // small_front.cu: levels whose fronts all have <= small_*_limit() rows, one
 // warp per front (factorization; forward and backward solve)

@@ -409,7 +409,8 @@ k_factor_warp(SnDev sd, FactorDev fd, const double* __restrict__ kval,
 // their index words loaded before the children's flags are awaited.
 constexpr int kLsR = 4;  // light-child solve chunks held in registers
 
-__global__ void __launch_bounds__(kWarpsPerCta * 32)
+template <bool PIPE>
+__global__ void __launch_bounds__(kWarpsPerCta * 32, PIPE ? 0 : 6)
 k_fwd_warp(SnDev sd, const double* __restrict__ lval, double* w, double* uvec,
            int* flags, int epoch, int* counter, int npaths) {
   __shared__ double Ts[kWarpsPerCta][kWF];
@@ -447,9 +448,9 @@ k_fwd_warp(SnDev sd, const double* __restrict__ lval, double* w, double* uvec,
     int heavy = -1, hfu = 0, hri = 0;
 #if defined(NCL_WTRACE) || defined(NCL_WTRACE_DEAD)
 #ifdef NCL_WTRACE
-    const bool trc = pi == 0;
+    const bool trc = PIPE && pi == 0;
 #else
-    const bool trc = pi == 0 && epoch == 0x7fffffff;
+    const bool trc = PIPE && pi == 0 && epoch == 0x7fffffff;
 #endif
     unsigned long long tph[6] = {0, 0, 0, 0, 0, 0};
     long long tq = clock64();
@@ -459,6 +460,11 @@ k_fwd_warp(SnDev sd, const double* __restrict__ lval, double* w, double* uvec,
       const int k = R.k, f = R.f;
       WRec Rn = R;
       if (!top) Rn = load_rec(sd, q + 1);
+      if (!PIPE && q > pb) {
+        load_node(R);
+        load_idx(R);
+        fl = (chid >= 0 && chid != heavy) ? ld_relaxed(flags + chid) : epoch;
+      }
       if (chid >= 0 && chid != heavy && fl != epoch) wait_flag(flags + chid, epoch);
       for (int c = R.chb + 32 + lane; c < R.che; c += 32) {
         const int ch = sd.ch[c];
@@ -487,7 +493,7 @@ k_fwd_warp(SnDev sd, const double* __restrict__ lval, double* w, double* uvec,
         __syncwarp();
       }
       WT(1);
-      if (!top) load_idx(Rn);  // node q+1's index words, in flight during the substitution
+      if (PIPE && !top) load_idx(Rn);  // node q+1's index words, in flight during the substitution
       double t = (lane < f) ? T[lane] : 0.0;
 #pragma unroll
       for (int p = 0; p < kWF; ++p) {
@@ -498,7 +504,7 @@ k_fwd_warp(SnDev sd, const double* __restrict__ lval, double* w, double* uvec,
       }
       WT(2);
       const int hri_n = (!top && lane < f - k) ? ldg_pin(sd.rel + R.relp + lane) : 0;
-      if (!top) {
+      if (PIPE && !top) {
         load_node(Rn);
         fl = (chid >= 0 && chid != R.s) ? ld_relaxed(flags + chid) : epoch;
       }
@@ -533,7 +539,8 @@ k_fwd_warp(SnDev sd, const double* __restrict__ lval, double* w, double* uvec,
 // a shuffle; only a path's top node reads x from memory, and only nodes with
 // light children (other paths' tops) publish a flag.  Node q-1's record, L
 // columns, w, d and rel are loaded while node q is solved.
-__global__ void __launch_bounds__(kWarpsPerCta * 32)
+template <bool PIPE>  // !PIPE: trees of short paths, register-capped for 6 CTAs per SM
+__global__ void __launch_bounds__(kWarpsPerCta * 32, PIPE ? 0 : 6)
 k_bwd_warp(SnDev sd, const double* __restrict__ lval, const double* __restrict__ d,
            const double* __restrict__ w, double* x, int* flags, int epoch,
            const int8_t* __restrict__ wide, int* counter, int npaths) {
@@ -648,11 +655,13 @@ void launch_factor_warp(const SnDev& sd, const FactorDev& fd, const double* kval
 }
 
 void launch_fwd_warp(const SnDev& sd, const double* lval, double* w, double* uvec,
-                     int* flags, int epoch, int* counter, int npaths, int grid,
+                     int* flags, int epoch, int* counter, int npaths, int grid, bool pipe,
                      cudaStream_t st) {
   if (npaths == 0) return;
-  k_fwd_warp<<<grid, kWarpsPerCta * 32, 0, st>>>(sd, lval, w, uvec, flags, epoch,
-                                                counter, npaths);
+  if (pipe)
+    k_fwd_warp<true><<<grid, kWarpsPerCta * 32, 0, st>>>(sd, lval, w, uvec, flags, epoch, counter, npaths);
+  else
+    k_fwd_warp<false><<<grid, kWarpsPerCta * 32, 0, st>>>(sd, lval, w, uvec, flags, epoch, counter, npaths);
 #ifdef NCL_WTRACE
   {
     unsigned long long t[5];
@@ -666,11 +675,13 @@ void launch_fwd_warp(const SnDev& sd, const double* lval, double* w, double* uve
 
 void launch_bwd_warp(const SnDev& sd, const double* lval, const double* d,
                      const double* w, double* x, int* flags, int epoch,
-                     const int8_t* wide, int* counter, int npaths, int grid,
+                     const int8_t* wide, int* counter, int npaths, int grid, bool pipe,
                      cudaStream_t st) {
   if (npaths == 0) return;
-  k_bwd_warp<<<grid, kWarpsPerCta * 32, 0, st>>>(sd, lval, d, w, x, flags, epoch,
-                                                wide, counter, npaths);
+  if (pipe)
+    k_bwd_warp<true><<<grid, kWarpsPerCta * 32, 0, st>>>(sd, lval, d, w, x, flags, epoch, wide, counter, npaths);
+  else
+    k_bwd_warp<false><<<grid, kWarpsPerCta * 32, 0, st>>>(sd, lval, d, w, x, flags, epoch, wide, counter, npaths);
 }
 
 void launch_permute_in(int n, const int* perm, const double* b, double* w,
@@ -689,10 +700,15 @@ int warp_tier_grid(int which) {
   int dev = 0, sms = 0, per_sm = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  if (which == 1) {
+  if (which == 3) {  // lean solves
     int a = 0, b = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, k_fwd_warp, kWarpsPerCta * 32, 0);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_bwd_warp, kWarpsPerCta * 32, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, k_fwd_warp<false>, kWarpsPerCta * 32, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_bwd_warp<false>, kWarpsPerCta * 32, 0);
+    per_sm = a < b ? a : b;
+  } else if (which == 1) {
+    int a = 0, b = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, k_fwd_warp<true>, kWarpsPerCta * 32, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_bwd_warp<true>, kWarpsPerCta * 32, 0);
     per_sm = a < b ? a : b;
   } else {
     const size_t smem = kWarpsPerCta * kWarpFactorBytes;
