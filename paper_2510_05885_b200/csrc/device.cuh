@@ -70,8 +70,9 @@ __device__ __forceinline__ int ld_acquire(const int* p) {
 
 // Flag polling of the warp tier.  A relaxed load (no L1 invalidation, which
 // ld.acquire.gpu costs: CCTL.IVALL after every poll, and with it the L1 hits
-// of all static index data).  Ordering: the producer stores its data, fences
-// (__threadfence) and releases the flag; the consumer branches on the polled
+// of all static index data).  Ordering: the producer's lanes store their data,
+// meet at a warp barrier and lane 0 releases the flag (st.release.gpu,
+// ldl_kernels.cu publish); the consumer branches on the polled
 // value and only then issues its loads of the produced data, all of which
 // are L2 loads (ld.global.cg): L2 is the point of coherence and a load cannot
 // issue before the branch it follows has resolved.  flag_wait_done() keeps
