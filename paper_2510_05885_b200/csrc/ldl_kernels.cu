@@ -27,7 +27,6 @@ namespace nclb {
 constexpr int kWF = 32;       // warp-tier front limit (rows)
 constexpr int kFLD = 33;      // padded leading dimension of a warp front
 constexpr int kWarpsPerCta = 4;
-constexpr int kWideThreads = 256;
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
@@ -228,20 +227,11 @@ k_factor_warp(SnDev sd, FactorDev fd, const double* __restrict__ kval,
     if (trc && lane == 0) g_wtime[1] = gtimer();
     unsigned long long tph[11] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
     long long tq = clock64();
-#ifndef NCL_WT_MASK
-#define NCL_WT_MASK 0xffff
-#endif
-#define WT(i)                           \
-  if (((NCL_WT_MASK >> (i)) & 1) && trc) { \
-    const long long tn = clock64();     \
-    tph[i] += tn - tq;                  \
-    tq = tn;                            \
-  }
-#elif defined(NCL_WT_CLK)
-#define WT(i)                            \
-  {                                      \
-    const long long t_ = clock64();      \
-    asm volatile("" ::"l"(t_));          \
+#define WT(i)                       \
+  if (trc) {                        \
+    const long long tn = clock64(); \
+    tph[i] += tn - tq;              \
+    tq = tn;                        \
   }
 #else
 #define WT(i)
