@@ -830,6 +830,8 @@ class KktSystem {
   KktSystem(KktPlan plan, const ncl_kkt_opts& opt)
       : P_(std::move(plan)), opt_(opt) {
     CK(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&cst_, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&rev_, cudaEventDisableTiming));
     ldl_ = std::make_unique<LdlSystem>(
         P_.K, P_.sym, st_, P_.sn.schur >= 0 ? P_.N - P_.sn.first[P_.sn.schur] : 0);
     c_ptr_.upload(P_.c_ptr);
@@ -884,6 +886,8 @@ class KktSystem {
   ~KktSystem() {
     ldl_.reset();
     for (auto& e : pool_) cudaEventDestroy(e);
+    if (rev_) cudaEventDestroy(rev_);
+    if (cst_) cudaStreamDestroy(cst_);
     if (st_) cudaStreamDestroy(st_);
   }
 
@@ -912,9 +916,18 @@ class KktSystem {
     h2d(hval_.p, hv, hval_.n);
     h2d(jval_.p, jv, jval_.n);
     h2d(sigma_.p, sg, sigma_.n);
-    if (r1) h2d(r1_.p, r1, r1_.n);
-    if (r2) h2d(r2_.p, r2, r2_.n);
-    if (r3) h2d(r3_.p, r3, r3_.n);
+    // the right-hand sides are first read after the factorization: their
+    // copies overlap the refill and the factorization on a copy stream
+    CK(cudaEventRecord(rev_, st_));  // the previous solve is done with r1..r3
+    CK(cudaStreamWaitEvent(cst_, rev_, 0));
+    auto h2dc = [&](double* dst, const double* src, size_t k) {
+      if (k && src) CK(cudaMemcpyAsync(dst, src, k * sizeof(double), cudaMemcpyHostToDevice, cst_));
+    };
+    h2dc(r1_.p, r1, r1_.n);
+    h2dc(r2_.p, r2, r2_.n);
+    h2dc(r3_.p, r3, r3_.n);
+    CK(cudaEventRecord(rev_, cst_));
+    r_pending_ = true;
   }
 
   // KktContext::solve (kkt.cpp:266-314) on device-resident inputs
@@ -944,6 +957,10 @@ class KktSystem {
       const FactorInfo F = ldl_->read_factor_info();
       if (F.ok && F.n_pos == tgt[0] && F.n_neg == tgt[1]) {
         const int e3 = tick();
+        if (r_pending_) {  // host-buffer call: the right-hand sides' copies
+          CK(cudaStreamWaitEvent(st_, rev_, 0));
+          r_pending_ = false;
+        }
         launch_rhs(P_, jt_ptr_.p, jt_row_.p, jt_slot_.p, jv, sg, r1, r2, r3, rho, delta, v_.p,
                    wk_.p, rs_.p, pk_.p, rhs_.p, long_cols_.p, static_cast<int>(long_cols_.n), st_);
         launches_ += P_.form == kK1s ? 2 : 1;
@@ -1008,6 +1025,10 @@ class KktSystem {
       d2h(dx, dx_.p, dx_.n);
       d2h(dr, dr_.p, dr_.n);
       d2h(dy, dy_.p, dy_.n);
+    }
+    if (r_pending_) {  // no attempt reached the right-hand sides: still join their copies
+      CK(cudaStreamWaitEvent(st_, rev_, 0));
+      r_pending_ = false;
     }
     CK(cudaStreamSynchronize(st_));
   }
@@ -1075,6 +1096,9 @@ class KktSystem {
   std::unique_ptr<LdlSystem> ldl_;
   AsmDev asm_{};
   DBuf<int> long_slots_, long_cols_;
+  cudaStream_t cst_ = nullptr;  // host-buffer calls: copy stream of the right-hand sides
+  cudaEvent_t rev_ = nullptr;
+  bool r_pending_ = false;
   DBuf<int> c_ptr_, pair_row_, pair_pa_, pair_pb_, jp_ptr_, jp_idx_, jt_ptr_, jt_row_,
       jt_slot_;
   DBuf<uint32_t> c_code_;
