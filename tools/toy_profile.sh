@@ -12,6 +12,7 @@ cp paper_2510_05885_b200/libncl_b200.so /tmp/orig.so
 cp _var/trace.so paper_2510_05885_b200/libncl_b200.so
 NCL_NO_GRAPH=1 timeout 300 python bench.py --workload opf_toy:78484:1 --steps 2 --warmup 3 --no-cpu-baseline 2>&1 >/dev/null | grep "ncl wtrace\|ncl wtime\|ncl ftrace" | tail -3 > gpurun_out/toy/warp_phase_trace.txt
 cp /tmp/orig.so paper_2510_05885_b200/libncl_b200.so
+for b in ubench_piv ubench_lat; do [ -x tools/$b ] || nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/$b tools/$b.cu; done
 ./tools/ubench_piv > gpurun_out/toy/ubench_pivots.txt 2>&1
 ./tools/ubench_lat > gpurun_out/toy/ubench_latency.txt 2>&1
 ls -la gpurun_out/toy
