@@ -1488,7 +1488,7 @@ int ncl_kkt_create(int nt, const int* hp_ptr, const int* hp_idx, int m, const in
   *out = nullptr;
   return guard([&] {
     nclb::KktPlan plan =
-        nclb::make_kkt_plan(nt, hp_ptr, hp_idx, m, jp_ptr, jp_idx, ns, m_eq, form);
+        nclb::make_kkt_plan(nt, hp_ptr, hp_idx, m, jp_ptr, jp_idx, ns, m_eq, form, 0, false);
     auto* c = new ncl_kkt;
     try {
       c->sys = std::make_unique<nclb::KktSystem>(std::move(plan), opt ? *opt : default_opts());

@@ -21,7 +21,7 @@ int slot_of(const LowerCsc& A, int i, int j) {
 
 KktPlan make_kkt_plan(int nt, const int* hp_ptr, const int* hp_idx, int m,
                       const int* jp_ptr, const int* jp_idx, int ns, int m_eq,
-                      int form, int schur_n0) {
+                      int form, int schur_n0, bool supernodal) {
   KktPlan P;
   if (form < 0 || form > 2) throw std::invalid_argument("unknown kkt form");
   if (nt < 0 || m < 0 || ns < 0 || m_eq < 0 || m - m_eq != ns)
@@ -194,7 +194,7 @@ KktPlan make_kkt_plan(int nt, const int* hp_ptr, const int* hp_idx, int m,
     P.sn = build_supernodal(K, P.sym, schur_n0);
   } else {
     P.sym = analyze_with_permutation(K, amd_order(K));
-    P.sn = build_supernodal(K, P.sym);
+    if (supernodal) P.sn = build_supernodal(K, P.sym);
   }
   return P;
 }

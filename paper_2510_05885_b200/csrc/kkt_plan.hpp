@@ -50,8 +50,10 @@ struct KktPlan {
 // schur_n0 > 0 (K1s only): Schur mode for a block-arrowhead sub-problem whose
 // first schur_n0 variables couple the blocks -- they are ordered last (AMD on
 // the rest) and form the unfactored coupling supernode
+// supernodal = false (non-Schur only): skip the plan's own supernodal
+// structure (the device factorization builds its re-postordered one)
 KktPlan make_kkt_plan(int nt, const int* hp_ptr, const int* hp_idx, int m,
                       const int* jp_ptr, const int* jp_idx, int ns, int m_eq,
-                      int form, int schur_n0 = 0);
+                      int form, int schur_n0 = 0, bool supernodal = true);
 
 }  // namespace nclb
