@@ -51,6 +51,10 @@ typedef struct {
   int perturbed_pivots;
   double rel_residual;
   int ok;
+  int accepted;  /* an attempt passed the acceptance test: delta, refine_steps,
+                    perturbed_pivots, rel_residual and dx/dr/dy are filled
+                    (KktStep keeps them even when ok = 0 for a non-finite step,
+                    kkt.cpp:291-298) */
 } ncl_kkt_stats;
 
 /* symbolic / structural facts of a context (for parity checks and roofline
@@ -145,6 +149,13 @@ int ncl_plan_pattern(const ncl_plan* plan, int* col_ptr, int* row_ind);
  * device factorization uses.  NCL_ELOGIC + ncl_last_error() on a violation.
  * Test hook, no reference counterpart. */
 int ncl_plan_check_schedule(const ncl_plan* plan, int internal);
+/* Builds the tile-dataflow schedules of the wide tier (one per segment of
+ * wide levels, for `workers` resident workers) exactly as a context would and
+ * replays them: every task runs once, in panel order per tile, without
+ * deadlock.  stats4 (may be NULL): segments, tasks, simulated makespan and
+ * critical path (us, summed over segments).  NCL_ELOGIC on a violation.
+ * Test hook, no reference counterpart. */
+int ncl_plan_check_dag(const ncl_plan* plan, int workers, double* stats4);
 /* Eigen AMDOrdering<int> restated (the ordering the reference calls at
  * sparse.cpp:81-100) on a full symmetric CSC pattern with sorted rows:
  * perm[k] = node eliminated k-th.  Lets a reference build without Eigen use

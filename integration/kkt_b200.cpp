@@ -99,13 +99,11 @@ KktStep KktContext::solve(const KktInput& in, double warm_delta) {
   mat_stale_ = true;
   st.factor_attempts = s.factor_attempts;
   st.ok = s.ok != 0;
-  if (st.ok || s.delta != 0.0 || s.refine_steps) {
+  if (s.accepted) {  // kkt.cpp:291-298: every field of an accepted attempt, finite or not
     st.delta = s.delta;
     st.refine_steps = s.refine_steps;
     st.perturbed_pivots = s.perturbed_pivots;
     st.rel_residual = s.rel_residual;
-  }
-  if (st.ok) {
     st.dx = std::move(dx);
     st.dr = std::move(dr);
     st.dy = std::move(dy);

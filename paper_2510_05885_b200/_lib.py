@@ -29,7 +29,8 @@ class KktOpts(C.Structure):
 
 class KktStats(C.Structure):
     _fields_ = [("delta", _d), ("factor_attempts", _i), ("refine_steps", _i),
-                ("perturbed_pivots", _i), ("rel_residual", _d), ("ok", _i)]
+                ("perturbed_pivots", _i), ("rel_residual", _d), ("ok", _i),
+                ("accepted", _i)]
 
 
 class KktInfo(C.Structure):
@@ -74,6 +75,7 @@ SIGS = {
     "ncl_plan_symbolic": ([_p, _ip, _ip, _ip], _i),
     "ncl_plan_pattern": ([_p, _ip, _ip], _i),
     "ncl_plan_check_schedule": ([_p, _i], _i),
+    "ncl_plan_check_dag": ([_p, _i, C.POINTER(_d)], _i),
     "ncl_amd_full_pattern": ([_i, _ip, _ip, _ip], _i),
     "ncl_analyze_host": ([_i, _i, _ip, _ip, _ip, _ip, _ip, _ip], _i),
     "ncl_sparse_create": ([_i, _i, _ip, _ip, _dp, _ip, C.POINTER(_p)], _i),

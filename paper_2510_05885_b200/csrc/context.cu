@@ -25,6 +25,7 @@
 
 #include "../../include/ncl_b200.h"
 #include "cuda_util.hpp"
+#include "dag.hpp"
 #include "kkt_plan.hpp"
 #include "launch.hpp"
 #include "layout.hpp"
@@ -150,8 +151,14 @@ class LdlSystem {
       for (auto& e : lev) CK(cudaEventCreate(&e));
       CK(cudaEventRecord(lev[0], st_));
     }
+    g_kval_cur_ = kval;
     for (int l = 0; l < nlevels(); ++l) {
       if (lvl_times && l > 0) CK(cudaEventRecord(lev[l], st_));
+      if (lvl_dag_[l] == -2) continue;  // inside a tile-dataflow segment
+      if (lvl_dag_[l] >= 0) {
+        launch_dag(lvl_dag_[l], eps);
+        continue;
+      }
       for (int s : lvl_split_[l]) {  // fronts with very many children: group sums first
         launch_cc_partial(sd_, fd, s, T.f[s], T.split_ng[s], st_);
         launches_ += 1;
@@ -614,6 +621,7 @@ class LdlSystem {
       while (c > 1 && nf * c > 2 * sms) c >>= 1;
       lvl_cluster_[l] = c;
     }
+    build_dag_segments(sms);
     if (std::getenv("NCL_LEVEL_STATS")) {  // diagnostic: split fronts
       int ns = 0, nu = 0;
       for (int q = 0; q < T.nsn; ++q) {
@@ -778,6 +786,100 @@ class LdlSystem {
     }
     CK(cudaStreamSynchronize(st_));
   }
+
+  // tile-dataflow segments (dag.hpp): maximal runs of wide levels that are
+  // not small-front levels, hold no split extend-add and no Schur front;
+  // NCL_NO_DAG=1 keeps the level-synchronous kernels
+  struct DagSeg {
+    DagSegment g;
+    DBuf<DagFront> fronts;
+    DBuf<int> ch, w_ptr, st;  // st: tile states, then per-front done counters
+    DBuf<int4> tasks;
+    DBuf<double> scr;
+    DBuf<unsigned long long> trace;
+    DagDev dev{};
+  };
+  std::vector<std::unique_ptr<DagSeg>> dag_;
+  std::vector<int> lvl_dag_;  // per level: segment starting here, or -1 (-2: inside one)
+
+  void build_dag_segments(int sms) {
+    lvl_dag_.assign(static_cast<size_t>(nlevels()), -1);
+    if (!std::getenv("NCL_DAG")) return;  // opt-in while the level kernels are faster
+    const int per_sm = dag_workers_per_sm();
+    if (per_sm < 1) return;
+    const int workers = per_sm * sms;
+    const bool trace = std::getenv("NCL_DAG_TRACE") != nullptr;
+    for (const auto& run : dag_level_runs(sn_, small_factor_limit())) {
+      const int l = run[0], e = run[1];
+      auto seg = std::make_unique<DagSeg>();
+      seg->g = build_dag_segment(sn_, l, e, workers);
+      const DagSegment& G = seg->g;
+      seg->fronts.upload(G.fronts);
+      seg->ch.upload(G.ch.empty() ? std::vector<int>{0} : G.ch);
+      seg->w_ptr.upload(G.w_ptr);
+      std::vector<int4> tk(G.tasks.size());
+      for (size_t q = 0; q < tk.size(); ++q)
+        tk[q] = make_int4(G.tasks[q][0], G.tasks[q][1], G.tasks[q][2], G.tasks[q][3]);
+      seg->tasks.upload(tk);
+      seg->st.alloc(static_cast<size_t>(G.nstate) + G.fronts.size());
+      seg->scr.alloc(static_cast<size_t>(std::max(1, G.nscr)) * kDagScr);
+      if (trace) seg->trace.alloc(4 * std::max<size_t>(1, G.tasks.size()));
+      seg->dev = DagDev{seg->fronts.p, seg->ch.p, seg->tasks.p, seg->w_ptr.p, seg->st.p,
+                        seg->st.p + G.nstate, seg->scr.p, trace ? seg->trace.p : nullptr};
+      if (std::getenv("NCL_LEVEL_STATS"))
+        std::fprintf(stderr, "[ncl dag] levels %d-%d: %zu fronts, %zu tasks on %d workers, "
+                     "simulated %.1f us (critical path %.1f us)\n", l, e - 1, G.fronts.size(),
+                     G.tasks.size(), workers, G.makespan_us, G.crit_us);
+      lvl_dag_[l] = static_cast<int>(dag_.size());
+      for (int q = l + 1; q < e; ++q) lvl_dag_[q] = -2;
+      dag_.push_back(std::move(seg));
+    }
+  }
+  void launch_dag(int si, double eps) {
+    DagSeg& D = *dag_[si];
+    CK(cudaMemsetAsync(D.st.p, 0, D.st.n * sizeof(int), st_));
+    launch_front_dag(sd_, factor_dev(), g_kval_cur_, D.dev, D.g.workers, eps, st_);
+    launches_ += 1;
+    if (D.dev.trace && std::getenv("NCL_DAG_TRACE")) dump_dag_trace(D);
+  }
+  // diagnostic (NCL_DAG_TRACE=1, with NCL_NO_GRAPH=1): per task type the
+  // mean wait and work time, and the segment's span
+  void dump_dag_trace(DagSeg& D) {
+    const size_t nt = D.g.tasks.size();
+    std::vector<unsigned long long> h(4 * nt);
+    CK(cudaMemcpyAsync(h.data(), D.trace.p, h.size() * sizeof(unsigned long long),
+                       cudaMemcpyDeviceToHost, st_));
+    CK(cudaStreamSynchronize(st_));
+    unsigned long long t0 = ~0ull, t1 = 0;
+    double wsum[4] = {0, 0, 0, 0}, xsum[4] = {0, 0, 0, 0};
+    int cnt[4] = {0, 0, 0, 0};
+    for (size_t q = 0; q < nt; ++q) {
+      const int type = D.g.tasks[q][1] >> 24;
+      t0 = std::min(t0, h[4 * q]);
+      t1 = std::max(t1, h[4 * q + 2]);
+      wsum[type] += (h[4 * q + 1] - h[4 * q]) * 1e-3;
+      xsum[type] += (h[4 * q + 2] - h[4 * q + 1]) * 1e-3;
+      cnt[type]++;
+    }
+    const char* nm[4] = {"asm", "diag", "trsm", "upd"};
+    std::fprintf(stderr, "[ncl dag trace] levels %d-%d span %.1f us (simulated %.1f):", D.g.l0, D.g.l1 - 1,
+                 (t1 - t0) * 1e-3, D.g.makespan_us);
+    for (int c = 0; c < 4; ++c)
+      if (cnt[c])
+        std::fprintf(stderr, " %s n=%d wait %.2f work %.2f us;", nm[c], cnt[c], wsum[c] / cnt[c],
+                     xsum[c] / cnt[c]);
+    std::fprintf(stderr, "\n");
+    if (const char* path = std::getenv("NCL_DAG_TRACE_FILE")) {
+      if (FILE* fp = std::fopen(path, "a")) {
+        for (size_t q = 0; q < nt; ++q)
+          std::fprintf(fp, "%d %d %d %d %d %llu %llu %llu %llu\n", D.g.l0, D.g.tasks[q][0],
+                       D.g.tasks[q][1], D.g.tasks[q][2], D.g.tasks[q][3], h[4 * q] - t0,
+                       h[4 * q + 1] - t0, h[4 * q + 2] - t0, h[4 * q + 3]);
+        std::fclose(fp);
+      }
+    }
+  }
+  const double* g_kval_cur_ = nullptr;
 
   LowerCsc K_;
   Symbolic S_, S2_;
@@ -976,6 +1078,7 @@ class KktSystem {
         const bool accept =
             F.perturbed == 0 || abs_res <= opt_.accept_tol * std::max(1.0, bn);
         if (accept) {
+          st->accepted = 1;
           st->delta = delta;
           st->refine_steps = steps;
           st->perturbed_pivots = F.perturbed;
@@ -1021,7 +1124,7 @@ class KktSystem {
     auto d2h = [&](double* dst, const double* src, size_t k) {
       if (k && dst) CK(cudaMemcpyAsync(dst, src, k * sizeof(double), cudaMemcpyDeviceToHost, st_));
     };
-    if (st->factor_attempts && (st->ok || st->refine_steps >= 0)) {
+    if (st->accepted) {
       d2h(dx, dx_.p, dx_.n);
       d2h(dr, dr_.p, dr_.n);
       d2h(dy, dy_.p, dy_.n);
@@ -1678,6 +1781,27 @@ int ncl_plan_check_schedule(const ncl_plan* plan, int internal) {
       err = nclb::check_warp_schedule(P.sn);
     }
     if (!err.empty()) throw std::logic_error("warp schedule: " + err);
+  });
+}
+
+int ncl_plan_check_dag(const ncl_plan* plan, int workers, double* stats4) {
+  if (!plan || workers < 1) return NCL_EINVAL;
+  return guard([&] {
+    const auto& P = plan->plan;
+    const int n0 = P.sn.schur >= 0 ? P.N - P.sn.first[P.sn.schur] : 0;
+    const nclb::Symbolic S2 = nclb::analyze_with_permutation(P.K, nclb::tallest_child_last(P.K, P.sym.perm));
+    const nclb::Supernodal T = nclb::build_supernodal(P.K, S2, n0);
+    double st[4] = {0, 0, 0, 0};
+    for (const auto& run : nclb::dag_level_runs(T, nclb::small_factor_limit())) {
+      const nclb::DagSegment G = nclb::build_dag_segment(T, run[0], run[1], workers);
+      const std::string err = nclb::check_dag_segment(T, G);
+      if (!err.empty()) throw std::logic_error("dag schedule: " + err);
+      st[0] += 1;
+      st[1] += static_cast<double>(G.tasks.size());
+      st[2] += G.makespan_us;
+      st[3] += G.crit_us;
+    }
+    if (stats4) std::copy(st, st + 4, stats4);
   });
 }
 

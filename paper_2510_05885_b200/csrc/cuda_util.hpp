@@ -3,6 +3,8 @@
 
 #include <cuda_runtime.h>
 
+#include <atomic>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -46,6 +48,25 @@ struct DBuf {
   }
   void zero(cudaStream_t st) {
     if (n) CK(cudaMemsetAsync(p, 0, n * sizeof(T), st));
+  }
+};
+
+// Runs f once per current device for one call site (kernel attributes such as
+// the dynamic shared-memory opt-in are set per device); safe when contexts are
+// created from several threads at once.
+struct PerDeviceOnce {
+  std::mutex mu;
+  std::atomic<unsigned long long> done{0};  // bit d: device d
+  template <class F>
+  void operator()(F&& f) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const unsigned long long bit = 1ull << (dev & 63);
+    if (done.load(std::memory_order_acquire) & bit) return;
+    std::lock_guard<std::mutex> g(mu);
+    if (done.load(std::memory_order_relaxed) & bit) return;
+    f();
+    done.fetch_or(bit, std::memory_order_release);
   }
 };
 

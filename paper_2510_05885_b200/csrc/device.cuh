@@ -72,11 +72,12 @@ __device__ __forceinline__ int ld_acquire(const int* p) {
 // ld.acquire.gpu costs: CCTL.IVALL after every poll, and with it the L1 hits
 // of all static index data).  Ordering: the producer's lanes store their data,
 // meet at a warp barrier and lane 0 releases the flag (st.release.gpu,
-// ldl_kernels.cu publish); the consumer branches on the polled
-// value and only then issues its loads of the produced data, all of which
-// are L2 loads (ld.global.cg): L2 is the point of coherence and a load cannot
-// issue before the branch it follows has resolved.  flag_wait_done() keeps
-// the compiler from hoisting those loads above the poll.
+// ldl_kernels.cu publish).  The consumer polls relaxed and, once per node
+// after its last poll, completes the acquire pattern with fence.acq_rel.gpu
+// (flag_wait_done: "a strong read followed by fence.acq_rel" is an acquire in
+// the PTX memory model), so the producer's release synchronizes-with it and
+// the __syncwarp that follows carries the edge to every lane.  Its loads of
+// the produced data are L2 loads (ld.global.cg) issued after that.
 __device__ __forceinline__ int ld_relaxed(const int* p) {
   int v;
   asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -130,8 +131,8 @@ __device__ __forceinline__ void pdl_launch_dependents() {
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 __device__ __forceinline__ void flag_wait_done() {
+  asm volatile("fence.acq_rel.gpu;" ::: "memory");
   __syncwarp();
-  asm volatile("" ::: "memory");
 }
 
 __device__ __forceinline__ void st_release(int* p, int v) {

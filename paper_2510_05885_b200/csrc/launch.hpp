@@ -32,7 +32,23 @@ void launch_factor_warp(const SnDev& sd, const FactorDev& fd, const double* kval
 int launch_wide_front(const SnDev& sd, const FactorDev& fd, const double* kval, const int* nodes,
                       int count, int cluster, int max_f, double eps, cudaStream_t st,
                       unsigned long long* trace = nullptr);
-extern const char* wide_last_error;
+extern thread_local const char* wide_last_error;
+// tile-dataflow segment of wide levels (dag.hpp): one persistent launch of
+// `workers` resident CTAs
+struct DagFront;
+struct DagDev {
+  const DagFront* fronts;
+  const int* ch;
+  const int4* tasks;  // per worker, in order: w_ptr
+  const int* w_ptr;
+  int* st;            // tile states (zeroed before the launch)
+  int* done;          // per front: final trailing tiles (zeroed)
+  double* scr;        // DIAG pivots, kDagScr per diagonal tile
+  unsigned long long* trace;  // optional: 4 words per task
+};
+int dag_workers_per_sm();
+void launch_front_dag(const SnDev& sd, const FactorDev& fd, const double* kval, const DagDev& g,
+                      int workers, double eps, cudaStream_t st);
 void launch_wide_assemble(const SnDev& sd, const FactorDev& fd, const double* kval,
                           const int4* tasks, int count, cudaStream_t st);
 void launch_wide_panel(const SnDev& sd, const FactorDev& fd, const int4* tasks, int count,

@@ -19,6 +19,7 @@
 #include <stdint.h>
 #include <cstdio>
 
+#include "cuda_util.hpp"
 #include "device.cuh"
 #include "launch.hpp"
 
@@ -197,7 +198,7 @@ k_factor_warp(SnDev sd, FactorDev fd, const double* __restrict__ kval,
   double* F = wsm + static_cast<size_t>(wid) * kWarpFactorDoubles;
   double* N = F + kWF * kFLD;
   double* cb = N + kWF * kFLD;
-#if defined(NCL_WTRACE) || defined(NCL_WTRACE_DEAD)
+#ifdef NCL_WTRACE
   if (lane == 0) atomicMin(&g_wtime[0], gtimer());
 #endif
   cb[lane] = 0.0;
@@ -382,7 +383,9 @@ k_factor_warp(SnDev sd, FactorDev fd, const double* __restrict__ kval,
       for (int i = 0; i < 11; ++i) g_wtrace[i] = tph[i];
       g_wtime[2] = gtimer();
     }
+#ifdef NCL_WTRACE
     if (!trc && lane == 0) atomicMax(&g_wtime[3], gtimer());
+#endif
 #endif
   }
   fail = __any_sync(0xffffffffu, fail);
@@ -617,14 +620,13 @@ void launch_factor_warp(const SnDev& sd, const FactorDev& fd, const double* kval
                         int* flags, int epoch, int* counter, int npaths,
                         double eps, int grid, bool pipe, cudaStream_t st) {
   if (npaths == 0) return;
-  static bool init = false;
-  if (!init) {
+  static PerDeviceOnce init;
+  init([] {
     cudaFuncSetAttribute(k_factor_warp<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(kWarpsPerCta * kWarpFactorBytes));
     cudaFuncSetAttribute(k_factor_warp<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(kWarpsPerCta * kWarpFactorBytes));
-    init = true;
-  }
+  });
   if (pipe)
     k_factor_warp<true><<<grid, kWarpsPerCta * 32, kWarpsPerCta * kWarpFactorBytes, st>>>(
         sd, fd, kval, flags, epoch, counter, npaths, eps);

@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "cuda_util.hpp"
 #include "device.cuh"
 #include "launch.hpp"
 #include "layout.hpp"
@@ -284,12 +285,11 @@ int small_solve_limit() { return kSmallSolveF; }
 template <int R, int W>
 static void small_launch(const SnDev& sd, const FactorDev& fd, const double* kval, const int* nodes,
                          int count, int fmax, double eps, cudaStream_t st) {
-  static bool init = false;
-  if (!init) {
+  static PerDeviceOnce init;
+  init([] {
     cudaFuncSetAttribute(k_small_front<R, W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(small_front_smem<R, W>(32 * R)));
-    init = true;
-  }
+  });
   const int fm = fmax < 1 ? 1 : fmax;
   k_small_front<R, W><<<(count + W - 1) / W, W * 32, small_front_smem<R, W>(fm), st>>>(sd, fd, kval, nodes,
                                                                                        count, eps, fm);

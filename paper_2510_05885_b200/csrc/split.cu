@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "cuda_util.hpp"
 #include "device.cuh"
 #include "launch.hpp"
 
@@ -82,23 +83,21 @@ k_uv_partial(SnDev sd, const double* __restrict__ uvec, int s, int ng) {
 
 void launch_cc_partial(const SnDev& sd, const FactorDev& fd, int s, int f, int ng, cudaStream_t st) {
   const size_t smem = sizeof(double) * kSplitWarps * f;
-  static bool init = false;
-  if (!init) {
+  static PerDeviceOnce init;
+  init([] {
     cudaFuncSetAttribute(k_cc_partial, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(sizeof(double) * kSplitWarps * 512));
-    init = true;
-  }
+  });
   k_cc_partial<<<dim3(f, ng), kSplitWarps * 32, smem, st>>>(sd, fd, s, ng);
 }
 
 void launch_uv_partial(const SnDev& sd, const double* uvec, int s, int f, int ng, cudaStream_t st) {
   const size_t smem = sizeof(double) * kSplitWarps * f;
-  static bool init = false;
-  if (!init) {
+  static PerDeviceOnce init;
+  init([] {
     cudaFuncSetAttribute(k_uv_partial, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(sizeof(double) * kSplitWarps * 512));
-    init = true;
-  }
+  });
   k_uv_partial<<<ng, kSplitWarps * 32, smem, st>>>(sd, uvec, s, ng);
 }
 

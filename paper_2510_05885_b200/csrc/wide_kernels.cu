@@ -31,13 +31,16 @@
 // k_wide_update) so one front spreads over every SM.
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
+#include <cstddef>
 #include <cstdlib>
 #include <stdint.h>
 
+#include "cuda_util.hpp"
 #include "device.cuh"
 #include "launch.hpp"
 #include "layout.hpp"
 #include "symbolic.hpp"
+#include "dag.hpp"
 
 namespace cg = cooperative_groups;
 
@@ -652,11 +655,11 @@ k_wide_update(SnDev sd, FactorDev fd, const int4* __restrict__ tiles, int count,
 }
 
 // ---------------------------------------------------------------------------
-const char* wide_last_error = "";
+thread_local const char* wide_last_error = "";
 
 static void wide_init() {
-  static bool done = false;
-  if (done) return;
+  static PerDeviceOnce once;
+  once([] {
   cudaFuncSetAttribute(k_wide_front, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   int dev = 0, optin = 0;
   cudaGetDevice(&dev);
@@ -666,7 +669,7 @@ static void wide_init() {
   cudaFuncSetAttribute(k_wide_front, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        optin - static_cast<int>(fa.sharedSizeBytes));
   cudaGetLastError();
-  done = true;
+  });
 }
 
 int wide_front_smem(int max_f) {
@@ -734,12 +737,9 @@ void launch_wide_assemble(const SnDev& sd, const FactorDev& fd, const double* kv
 
 void launch_wide_panel(const SnDev& sd, const FactorDev& fd, const int4* tasks, int count,
                        int panel, double eps, cudaStream_t st) {
-  static bool init = false;
+  static PerDeviceOnce init;
   constexpr int tr_bytes = static_cast<int>(sizeof(double)) * kWidePanel * (kTrsRows + 2);
-  if (!init) {
-    cudaFuncSetAttribute(k_wide_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, tr_bytes);
-    init = true;
-  }
+  init([] { cudaFuncSetAttribute(k_wide_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, tr_bytes); });
   if (count) launch_pdl(k_wide_panel, count, kHugeRows, tr_bytes, st, true, sd, fd, tasks, panel, eps);
 }
 
@@ -747,6 +747,161 @@ void launch_wide_update(const SnDev& sd, const FactorDev& fd, const int4* tiles,
                         const int* fronts, int nd, int panel, cudaStream_t st, bool pdl) {
   const int blocks = count > 0 ? count : (nd > 0 ? 1 : 0);
   if (blocks) launch_pdl(k_wide_update, blocks, 128, 0, st, pdl, sd, fd, tiles, count, fronts, nd, panel);
+}
+
+// ---------------------------------------------------------------------------
+// Tile dataflow over a segment of wide levels (dag.hpp): one persistent
+// launch, one 128-thread worker per CTA running its task list in order.
+// Waits: warp 0's lanes poll the tile states a task needs (ld.acquire.gpu,
+// back-off), then a CTA barrier; publication: CTA barrier, then one thread's
+// st.release.gpu (cumulative over the CTA's writes ordered by the barrier).
+struct DagSmem {
+  PanelSmem pm;
+  union alignas(16) {  // cp.async destinations: 16-byte aligned
+    GroupSmem g;
+    struct {
+      double D[kWidePanel * kSL];
+      double TR[kWidePanel * (kWidePanel + 2)];
+    } t;
+  } u;
+};
+
+static_assert(offsetof(DagSmem, u) % 16 == 0 && sizeof(PanelSmem) % 8 == 0, "DagSmem alignment");
+
+__device__ __forceinline__ void dag_wait(const int* p, int v) {
+  if (ld_acquire(p) >= v) return;
+  unsigned ns = 32;
+  while (ld_acquire(p) < v) {
+    __nanosleep(ns);
+    if (ns < 256) ns <<= 1;
+  }
+}
+
+__device__ __forceinline__ void red_release_add(int* p, int v) {
+  asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ int dag_tri(int i, int j) { return i * (i + 1) / 2 + j; }
+
+__global__ void __launch_bounds__(128, 4)
+k_front_dag(SnDev sd, FactorDev fd, const double* __restrict__ kval, DagDev g, double eps) {
+  extern __shared__ __align__(16) double dyn_smem[];
+  DagSmem& S = *reinterpret_cast<DagSmem*>(dyn_smem);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  pdl_launch_dependents();
+  pdl_wait();  // the previous kernels (warp tier, earlier levels)
+  const int t0 = g.w_ptr[blockIdx.x], t1 = g.w_ptr[blockIdx.x + 1];
+  for (int ti = t0; ti < t1; ++ti) {
+    const int4 tk = g.tasks[ti];
+    const DagFront& Fr = g.fronts[tk.x];
+    const int type = tk.y >> 24, i = tk.y & 0xfff, j = (tk.y >> 12) & 0xfff, p = tk.z;
+    const int k = Fr.k, f = Fr.f, P = Fr.P, NB = Fr.NB, c0 = Fr.c0;
+    int* stf = g.st + Fr.st_off;
+    double* F = fd.lval + Fr.loff;
+    const size_t ld = wide_ld(f);
+    unsigned long long tw = 0;
+    if (g.trace && tid == 0) tw = globaltimer();
+    // ---- waits
+    if (warp == 0) {
+      if (type == kDagAsm) {
+        for (int q = Fr.ch_b + lane; q < Fr.ch_e; q += 32) {
+          const int c = g.ch[q];
+          dag_wait(g.done + c, g.fronts[c].ntrail);
+        }
+      } else if (type == kDagDiag) {
+        if (lane == 0) dag_wait(stf + dag_tri(p, p), p + 1);
+      } else if (type == kDagTrsm) {
+        if (lane == 0) dag_wait(stf + dag_tri(i, p), p + 1);
+        if (lane == 1) dag_wait(stf + dag_tri(p, p), p + 2);
+      } else {
+        if (lane == 0) dag_wait(stf + dag_tri(i, p), p + 2);
+        if (lane == 1) dag_wait(stf + dag_tri(j, p), p + 2);
+        if (lane == 2) dag_wait(stf + dag_tri(i, j), p + 1);
+      }
+    }
+    __syncthreads();
+    unsigned long long tb = 0;
+    if (g.trace && tid == 0) tb = globaltimer();
+    // ---- work
+    if (type == kDagAsm) {
+      const int j0 = dag_block_start(k, P, j), nb = dag_block_size(k, f, P, j);
+      for (int J = j0 + warp; J < j0 + nb; J += 4)
+        assemble_col(sd, fd, kval, Fr.s, c0, k, f, F, ld, J, nullptr);
+    } else if (type == kDagDiag) {
+      const int p0 = 32 * p, nb = min(32, k - p0);
+      if (warp == 0)
+        diag_block(F, ld, p0, nb, eps, S.pm, S.u.t.D, fd.d + c0 + p0, fd.stats, nullptr);
+      __syncthreads();
+      double* scr = g.scr + static_cast<size_t>(Fr.scr_off + p) * kDagScr;
+      for (int x = tid; x < kWidePanel * kWidePanel; x += 128) {
+        const int r = x >> 5, q = x & 31;
+        scr[x] = (&S.pm.Us[0][0])[x];
+        if (r > q && r < nb) F[(p0 + r) + (p0 + q) * ld] = S.pm.Lsh[r][q];
+      }
+      if (tid < 32) scr[kWidePanel * kWidePanel + tid] = S.pm.rinv[tid];
+    } else if (type == kDagTrsm) {
+      const int p0 = 32 * p, nb = min(32, k - p0);
+      const int r0 = dag_block_start(k, P, i), nr = dag_block_size(k, f, P, i);
+      const double* scr = g.scr + static_cast<size_t>(Fr.scr_off + p) * kDagScr;
+      double* us = &S.pm.Us[0][0];
+      for (int x = tid; x < kDagScr / 2; x += 128) {
+        double* dst = x < 512 ? us + 2 * x : S.pm.rinv + 2 * (x - 512);
+        cp16(dst, scr + 2 * x);
+      }
+      cp_wait_all();
+      __syncthreads();
+      if (warp == 0)
+        trsm_rows<32>(F, ld, p0, nb, r0, r0 + nr, us, S.pm.rinv, fd.stats, lane, S.u.t.TR, nullptr, 1);
+    } else {
+      const int p0 = 32 * p, nb = min(32, k - p0);
+      const int ri = dag_block_start(k, P, i), nr = dag_block_size(k, f, P, i);
+      const int rj = dag_block_start(k, P, j), nc = dag_block_size(k, f, P, j);
+      GroupSmem& G = S.u.g;
+      const bool dg = i == j;
+      const int shA = stage_block<kNR2>(G.A, kSL, F, ld, ri, p0, nb, tid, 128);
+      const int shB = dg ? shA : stage_block<kNR2>(G.B, kSL, F, ld, rj, p0, nb, tid, 128);
+      const int shC = stage_block<kNR2>(G.C, kSL, F, ld, ri, rj, nc, tid, 128);
+      if (tid < nb) G.d[tid] = __ldcg(fd.d + c0 + p0 + tid);
+      cp_wait_all();
+      __syncthreads();
+      tile_mma_store(F, ld, G.A, shA, dg ? G.A : G.B, shB, G.C, shC, G.d, nb, ri, nr, rj, nc, tid);
+    }
+    __syncthreads();  // the task's writes, then its state (and the smem reuse)
+    // ---- publish
+    if (type == kDagAsm) {
+      for (int a = j + tid; a < NB; a += 128) st_release(stf + dag_tri(a, j), 1);
+    } else if (tid == 0) {
+      st_release(stf + dag_tri(i, type == kDagUpd ? j : p), p + 2);
+      if (type == kDagUpd && j >= P && p == P - 1) red_release_add(g.done + tk.x, 1);
+    }
+    if (g.trace && tid == 0) {
+      unsigned long long* tr = g.trace + 4 * static_cast<size_t>(ti);
+      tr[0] = tw;
+      tr[1] = tb;
+      tr[2] = globaltimer();
+      tr[3] = blockIdx.x;
+    }
+  }
+}
+
+int dag_smem_bytes() { return static_cast<int>(sizeof(DagSmem)); }
+
+int dag_workers_per_sm() {
+  static PerDeviceOnce init;
+  init([] {
+    cudaFuncSetAttribute(k_front_dag, cudaFuncAttributeMaxDynamicSharedMemorySize, dag_smem_bytes());
+  });
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_front_dag, 128, dag_smem_bytes());
+  cudaGetLastError();
+  return per_sm;
+}
+
+void launch_front_dag(const SnDev& sd, const FactorDev& fd, const double* kval, const DagDev& g,
+                      int workers, double eps, cudaStream_t st) {
+  dag_workers_per_sm();  // the smem opt-in on this device
+  launch_pdl(k_front_dag, workers, 128, static_cast<size_t>(dag_smem_bytes()), st, true, sd, fd, kval, g,
+             eps);
 }
 
 }  // namespace nclb

@@ -24,6 +24,7 @@
 #include <cstdlib>
 #include <stdint.h>
 
+#include "cuda_util.hpp"
 #include "device.cuh"
 #include "launch.hpp"
 #include "symbolic.hpp"
@@ -524,14 +525,14 @@ static void solve_init_one(int optin) {
 }
 
 static void solve_init() {
-  static bool done = false;
-  if (done) return;
-  int dev = 0, optin = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-  solve_init_one<false>(optin);
-  solve_init_one<true>(optin);
-  done = true;
+  static PerDeviceOnce once;
+  once([] {
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    solve_init_one<false>(optin);
+    solve_init_one<true>(optin);
+  });
 }
 
 // par: the level holds a front with >= kParK pivots (cluster-parallel L11)

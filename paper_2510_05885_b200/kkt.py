@@ -213,7 +213,7 @@ class KktContext:
         check(self._L.ncl_kkt_solve(self._h, dp(hv), dp(jv), dp(sg), dp(r1), dp(r2), dp(r3),
                                     float(inp.rho), float(warm_delta), dp(dx), dp(dr), dp(dy),
                                     C.byref(st)), "KktContext.solve")
-        if not st.ok:
+        if not st.accepted:  # kkt.cpp:291-298: an accepted attempt keeps its step, finite or not
             dx, dr, dy = np.zeros(0), np.zeros(0), np.zeros(0)
         return KktStep(dx, dr, dy, st.delta, st.factor_attempts, st.refine_steps,
                        st.perturbed_pivots, st.rel_residual, bool(st.ok))
