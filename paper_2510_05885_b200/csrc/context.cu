@@ -307,6 +307,12 @@ class LdlSystem {
     pt.mark();
     for (int l = 0; l < nlevels(); ++l) {
       if (l) pt.mark();
+      if (l == tr_l0_ && tree_on()) {  // levels [tr_l0_, tr_l1_): one dataflow launch
+        CK(cudaMemsetAsync(tr_flags_.p, 0, sizeof(int) * tr_flags_.n, st_));
+        launch_fwd_tree(sd_, td_, lval_.p, wp_.p, uvec_.p, tr_grid_, tr_fmax_, st_);
+        l = tr_l1_ - 1;
+        continue;
+      }
       for (int s : lvl_usplit_[l]) {
         launch_uv_partial(sd_, uvec_.p, s, sn_.f[s], sn_.usplit_ng[s], st_);
         launches_ += 1;
@@ -323,13 +329,19 @@ class LdlSystem {
       solve_cluster_[l] = used;
     }
     pt.report("fwd (warp, levels)");
-    launches_ += 1 + (npaths() > 0 ? 1 : 0) + nlevels();
+    launches_ += 1 + (npaths() > 0 ? 1 : 0) + nlevels() - (tree_on() ? tr_l1_ - tr_l0_ - 1 : 0);
     CK(cudaGetLastError());
   }
   void bwd_seq(double* x) {
     PhaseTimer pt(st_);
     for (int l = nlevels() - 1; l >= 0; --l) {
       if (l < nlevels() - 1) pt.mark();
+      if (l == tr_l1_ - 1 && tree_on()) {
+        launch_bwd_tree(sd_, td_, lval_.p, d_.p, wp_.p, xp_.p, tr_grid_, tr_fmax_, tr_pmax_, st_);
+        if (tr_dump_) dump_tree_trace();
+        l = tr_l0_;
+        continue;
+      }
       if (small_solve(l)) {
         launch_bwd_small(sd_, lval_.p, d_.p, wp_.p, xp_.p, lvl_nodes_.p + sn_.lvl_ptr[l],
                          sn_.lvl_ptr[l + 1] - sn_.lvl_ptr[l], lvl_fmax_[l], st_);
@@ -350,7 +362,7 @@ class LdlSystem {
     }
     launch_permute_out(N_, perm_.p, xp_.p, x, st_);
     pt.report("bwd (levels top-down, warp)");
-    launches_ += 1 + (npaths() > 0 ? 1 : 0) + nlevels();
+    launches_ += 1 + (npaths() > 0 ? 1 : 0) + nlevels() - (tree_on() ? tr_l1_ - tr_l0_ - 1 : 0);
     CK(cudaGetLastError());
   }
 
@@ -622,6 +634,7 @@ class LdlSystem {
       lvl_cluster_[l] = c;
     }
     build_dag_segments(sms);
+    build_tree(sms);
     if (std::getenv("NCL_LEVEL_STATS")) {  // diagnostic: split fronts
       int ns = 0, nu = 0;
       for (int q = 0; q < T.nsn; ++q) {
@@ -785,6 +798,125 @@ class LdlSystem {
       pipe_ = longest >= kFrontPathLen;
     }
     CK(cudaStreamSynchronize(st_));
+  }
+
+  // tree-dataflow solves (tree_solve.cu): the wide levels [tr_l0_, tr_l1_)
+  // -- from the first level that is not a small-front level up to the first
+  // one holding a Schur / split-gather front, a front above kTreeMaxF rows or
+  // one with cluster-parallel pivot blocks -- in one launch per direction.
+  // NCL_NO_TREE=1 keeps the per-level kernels.
+  int tr_l0_ = 0, tr_l1_ = 0, tr_grid_ = 0, tr_fmax_ = 0, tr_pmax_ = 0;
+  DBuf<int> tr_list_, tr_wptr_, tr_wait_, tr_par_, tr_gbase_, tr_grow_, tr_gsrc_, tr_flags_;
+  DBuf<unsigned long long> tr_trace_;
+  bool tr_dump_ = false;
+  std::vector<int> tr_lvl_;
+  // diagnostic (NCL_TREE_TRACE=1, NCL_NO_GRAPH=1): per level, the span of
+  // its fronts and their mean wait / gather / solve times, per direction
+  void dump_tree_trace() {
+    const size_t n = tr_lvl_.size();
+    std::vector<unsigned long long> h(8 * n);
+    CK(cudaMemcpyAsync(h.data(), tr_trace_.p, h.size() * 8, cudaMemcpyDeviceToHost, st_));
+    CK(cudaStreamSynchronize(st_));
+    for (int dir = 0; dir < 2; ++dir) {
+      // SM clock stamps: durations only (us at 1.965 GHz)
+      constexpr double us = 1.0 / 1965.0;
+      std::fprintf(stderr, "[ncl tree trace] %s (mean us per front: wait / gather / solve, max solve):",
+                   dir ? "bwd" : "fwd");
+      for (int l = tr_l0_; l < tr_l1_; ++l) {
+        double wt = 0, ga = 0, so = 0, mx = 0;
+        int c = 0;
+        for (size_t i = 0; i < n; ++i) {
+          if (tr_lvl_[i] != l) continue;
+          const unsigned long long* t = &h[4 * (dir * n + i)];
+          wt += (t[1] - t[0]) * us;
+          ga += (t[2] - t[1]) * us;
+          so += (t[3] - t[2]) * us;
+          mx = std::max(mx, (t[3] - t[2]) * us);
+          ++c;
+        }
+        std::fprintf(stderr, " L%d[w%.1f g%.1f s%.1f m%.1f]", l, wt / c, ga / c, so / c, mx);
+      }
+      std::fprintf(stderr, "\n");
+    }
+  }
+  TreeDev td_{};
+  bool tree_on() const { return tr_l1_ > tr_l0_; }
+  void build_tree(int sms) {
+    if (std::getenv("NCL_NO_TREE")) return;
+    const auto& T = sn_;
+    const int nl = nlevels();
+    int l0 = 0;
+    while (l0 < nl && small_solve(l0)) ++l0;
+    auto eligible = [&](int l) {
+      if (lvl_fmax_[l] > kTreeMaxF || lvl_kmax_[l] >= solve_par_k()) return false;
+      for (int q = T.lvl_ptr[l]; q < T.lvl_ptr[l + 1]; ++q) {
+        const int s = T.lvl_nodes[q];
+        if (s == T.schur || T.usplit_ng[s]) return false;
+      }
+      return true;
+    };
+    int l1 = l0;
+    while (l1 < nl && eligible(l1)) ++l1;
+    if (const char* e = std::getenv("NCL_TREE_L1")) l1 = std::min(l1, std::atoi(e));  // experiments
+    if (l1 - l0 < 2) return;
+    std::vector<int> list, pos(static_cast<size_t>(T.nsn), -1);
+    int fmax = 0, pmax = 0;
+    for (int q = T.lvl_ptr[l0]; q < T.lvl_ptr[l1]; ++q) {
+      const int s = T.lvl_nodes[q];
+      pos[s] = static_cast<int>(list.size());
+      list.push_back(s);
+      fmax = std::max(fmax, T.f[s]);
+      pmax = std::max(pmax, (T.first[s + 1] - T.first[s] + 31) / 32);
+    }
+    const int per_sm = tree_ctas_per_sm(fmax, pmax);
+    if (per_sm < 1) return;
+    std::vector<int> wptr{0}, wait, par, gbase, grow, gsrc;
+    std::vector<std::vector<int>> bucket;
+    for (int s : list) {
+      for (int q = T.ch_ptr[s]; q < T.ch_ptr[s + 1]; ++q)
+        if (pos[T.ch[q]] >= 0) wait.push_back(T.ch[q]);
+      wptr.push_back(static_cast<int>(wait.size()));
+      const int p = T.sparent[s];
+      par.push_back(p >= 0 && pos[p] >= 0 ? p : -1);
+      // gather rows: the children's update-vector entries landing on each
+      // front row, in child order (the order k_fwd_front adds them)
+      bucket.assign(static_cast<size_t>(T.f[s]), {});
+      for (int q = T.ch_ptr[s]; q < T.ch_ptr[s + 1]; ++q) {
+        const int c = T.ch[q], fu = T.f[c] - (T.first[c + 1] - T.first[c]), rp = T.rel_ptr[c];
+        for (int i = 0; i < fu; ++i) bucket[T.rel[rp + i]].push_back(rp + i);
+      }
+      gbase.push_back(static_cast<int>(grow.size()));
+      for (int r = 0; r < T.f[s]; ++r) {
+        grow.push_back(static_cast<int>(gsrc.size()));
+        gsrc.insert(gsrc.end(), bucket[r].begin(), bucket[r].end());
+      }
+      grow.push_back(static_cast<int>(gsrc.size()));
+    }
+    tr_list_.upload(list);
+    tr_wptr_.upload(wptr);
+    tr_wait_.upload(wait.empty() ? std::vector<int>{0} : wait);
+    tr_par_.upload(par);
+    tr_gbase_.upload(gbase);
+    tr_grow_.upload(grow);
+    tr_gsrc_.upload(gsrc.empty() ? std::vector<int>{0} : gsrc);
+    tr_flags_.alloc(static_cast<size_t>(T.nsn));
+    tr_flags_.zero(st_);
+    const int trmode = std::getenv("NCL_TREE_TRACE") ? std::atoi(std::getenv("NCL_TREE_TRACE")) : 0;
+    if (trmode) tr_trace_.alloc(8 * list.size());
+    tr_dump_ = trmode == 1 || trmode == 3;
+    td_ = TreeDev{tr_list_.p, static_cast<int>(list.size()), tr_wptr_.p, tr_wait_.p, tr_par_.p,
+                  tr_gbase_.p, tr_grow_.p, tr_gsrc_.p, tr_flags_.p, trmode == 3 ? nullptr : tr_trace_.p};
+    tr_lvl_.assign(list.size(), 0);
+    for (int l = l0; l < l1; ++l)
+      for (int q = T.lvl_ptr[l]; q < T.lvl_ptr[l + 1]; ++q) tr_lvl_[pos[T.lvl_nodes[q]]] = l;
+    tr_grid_ = std::min(static_cast<int>(list.size()), per_sm * sms);
+    tr_fmax_ = fmax;
+    tr_pmax_ = pmax;
+    tr_l0_ = l0;
+    tr_l1_ = l1;
+    if (std::getenv("NCL_LEVEL_STATS"))
+      std::fprintf(stderr, "[ncl tree] levels %d-%d: %zu fronts on %d CTAs (fmax %d, %zu gather entries)\n",
+                   l0, l1 - 1, list.size(), tr_grid_, fmax, gsrc.size());
   }
 
   // tile-dataflow segments (dag.hpp): maximal runs of wide levels that are

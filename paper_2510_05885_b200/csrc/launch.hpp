@@ -81,6 +81,26 @@ int launch_bwd_front(const SnDev& sd, const double* lval, const double* d, const
                      double* x, const int* nodes, int count, int cluster, int max_f, double* scr,
                      bool par, cudaStream_t st);
 int solve_par_k();  // pivot count from which a front's L11 solve is cluster-parallel
+// tree_solve.cu: the wide-tier solves of a run of levels as one persistent
+// dataflow launch per direction (one CTA per front, per-front flags)
+struct TreeDev {
+  const int* list;      // wide fronts in topological order (children first)
+  int n;
+  const int* wait_ptr;  // forward: per list position, its children in the list
+  const int* wait;
+  const int* par;       // backward: per list position, the parent if in the list, else -1
+  const int* g_base;    // per list position: offset of its f+1 gather row pointers in g_row
+  const int* g_row;
+  const int* g_src;     // update-vector offsets, child order within a row
+  int* flags;           // per supernode: 1 forward done, 2 backward done
+  unsigned long long* trace;  // diagnostic (NCL_TREE_TRACE): 4 stamps per front and direction
+};
+constexpr int kTreeMaxF = 2048;
+int tree_ctas_per_sm(int fmax, int pmax);  // 0: does not fit
+void launch_fwd_tree(const SnDev& sd, const TreeDev& td, const double* lval, double* w, double* uvec,
+                     int grid, int fmax, cudaStream_t st);
+void launch_bwd_tree(const SnDev& sd, const TreeDev& td, const double* lval, const double* d,
+                     const double* w, double* x, int grid, int fmax, int pmax, cudaStream_t st);
 void launch_permute_in(int n, const int* perm, const double* b, double* w,
                        cudaStream_t st);
 void launch_permute_out(int n, const int* perm, const double* xp, double* x,
