@@ -307,9 +307,10 @@ class LdlSystem {
     pt.mark();
     for (int l = 0; l < nlevels(); ++l) {
       if (l) pt.mark();
-      if (l == tr_l0_ && tree_on()) {  // levels [tr_l0_, tr_l1_): one dataflow launch
+      if (l == tr_l0_ && tree_on()) {  // levels [tr_l0_, tr_l1_): dataflow launches
         CK(cudaMemsetAsync(tr_flags_.p, 0, sizeof(int) * tr_flags_.n, st_));
-        launch_fwd_tree(sd_, td_, lval_.p, wp_.p, uvec_.p, tr_grid_, tr_fmax_, st_);
+        for (auto& P : tp_)
+          if (P.on()) launch_fwd_tree(sd_, P.td, lval_.p, wp_.p, uvec_.p, P.C, P.teams, P.fmax, st_);
         l = tr_l1_ - 1;
         continue;
       }
@@ -329,7 +330,7 @@ class LdlSystem {
       solve_cluster_[l] = used;
     }
     pt.report("fwd (warp, levels)");
-    launches_ += 1 + (npaths() > 0 ? 1 : 0) + nlevels() - (tree_on() ? tr_l1_ - tr_l0_ - 1 : 0);
+    launches_ += 1 + (npaths() > 0 ? 1 : 0) + nlevels() - (tree_on() ? tr_l1_ - tr_l0_ - (tp_[0].on() + tp_[1].on()) : 0);
     CK(cudaGetLastError());
   }
   void bwd_seq(double* x) {
@@ -337,7 +338,10 @@ class LdlSystem {
     for (int l = nlevels() - 1; l >= 0; --l) {
       if (l < nlevels() - 1) pt.mark();
       if (l == tr_l1_ - 1 && tree_on()) {
-        launch_bwd_tree(sd_, td_, lval_.p, d_.p, wp_.p, xp_.p, tr_grid_, tr_fmax_, tr_pmax_, st_);
+        for (int pi = 1; pi >= 0; --pi)
+          if (tp_[pi].on())
+            launch_bwd_tree(sd_, tp_[pi].td, lval_.p, d_.p, wp_.p, xp_.p, tp_[pi].C, tp_[pi].teams,
+                            tp_[pi].fmax, tp_[pi].pmax, st_);
         if (tr_dump_) dump_tree_trace();
         l = tr_l0_;
         continue;
@@ -362,7 +366,7 @@ class LdlSystem {
     }
     launch_permute_out(N_, perm_.p, xp_.p, x, st_);
     pt.report("bwd (levels top-down, warp)");
-    launches_ += 1 + (npaths() > 0 ? 1 : 0) + nlevels() - (tree_on() ? tr_l1_ - tr_l0_ - 1 : 0);
+    launches_ += 1 + (npaths() > 0 ? 1 : 0) + nlevels() - (tree_on() ? tr_l1_ - tr_l0_ - (tp_[0].on() + tp_[1].on()) : 0);
     CK(cudaGetLastError());
   }
 
@@ -803,62 +807,26 @@ class LdlSystem {
   // tree-dataflow solves (tree_solve.cu): the wide levels [tr_l0_, tr_l1_)
   // -- from the first level that is not a small-front level up to the first
   // one holding a Schur / split-gather front, a front above kTreeMaxF rows or
-  // one with cluster-parallel pivot blocks -- in one launch per direction.
-  // NCL_NO_TREE=1 keeps the per-level kernels.
-  int tr_l0_ = 0, tr_l1_ = 0, tr_grid_ = 0, tr_fmax_ = 0, tr_pmax_ = 0;
-  DBuf<int> tr_list_, tr_wptr_, tr_wait_, tr_par_, tr_gbase_, tr_grow_, tr_gsrc_, tr_flags_;
-  DBuf<unsigned long long> tr_trace_;
+  // one with cluster-parallel pivot blocks -- as one launch per direction of
+  // one CTA per front for [tr_l0_, tr_l2_) and one of a cluster per front for
+  // the top levels [tr_l2_, tr_l1_) (few big fronts: one SM's bandwidth is
+  // too little for them).  NCL_NO_TREE=1 keeps the per-level kernels;
+  // NCL_TREE_C=1 runs every tree level one CTA per front.
+  struct TreePart {
+    int l0 = 0, l1 = 0, C = 1, teams = 0, fmax = 0, pmax = 0;
+    DBuf<int> list, wptr, wait, par, gbase, grow, gsrc;
+    std::vector<int> lvl;  // per list position: level (trace)
+    TreeDev td{};
+    bool on() const { return l1 > l0; }
+  };
+  int tr_l0_ = 0, tr_l1_ = 0;
+  TreePart tp_[2];  // [0] one CTA per front (lower levels), [1] clusters (top levels)
+  DBuf<int> tr_flags_;
+  DBuf<unsigned long long> tr_trace_[2];
   bool tr_dump_ = false;
-  std::vector<int> tr_lvl_;
-  // diagnostic (NCL_TREE_TRACE=1, NCL_NO_GRAPH=1): per level, the span of
-  // its fronts and their mean wait / gather / solve times, per direction
-  void dump_tree_trace() {
-    const size_t n = tr_lvl_.size();
-    std::vector<unsigned long long> h(8 * n);
-    CK(cudaMemcpyAsync(h.data(), tr_trace_.p, h.size() * 8, cudaMemcpyDeviceToHost, st_));
-    CK(cudaStreamSynchronize(st_));
-    for (int dir = 0; dir < 2; ++dir) {
-      // SM clock stamps: durations only (us at 1.965 GHz)
-      constexpr double us = 1.0 / 1965.0;
-      std::fprintf(stderr, "[ncl tree trace] %s (mean us per front: wait / gather / solve, max solve):",
-                   dir ? "bwd" : "fwd");
-      for (int l = tr_l0_; l < tr_l1_; ++l) {
-        double wt = 0, ga = 0, so = 0, mx = 0;
-        int c = 0;
-        for (size_t i = 0; i < n; ++i) {
-          if (tr_lvl_[i] != l) continue;
-          const unsigned long long* t = &h[4 * (dir * n + i)];
-          wt += (t[1] - t[0]) * us;
-          ga += (t[2] - t[1]) * us;
-          so += (t[3] - t[2]) * us;
-          mx = std::max(mx, (t[3] - t[2]) * us);
-          ++c;
-        }
-        std::fprintf(stderr, " L%d[w%.1f g%.1f s%.1f m%.1f]", l, wt / c, ga / c, so / c, mx);
-      }
-      std::fprintf(stderr, "\n");
-    }
-  }
-  TreeDev td_{};
   bool tree_on() const { return tr_l1_ > tr_l0_; }
-  void build_tree(int sms) {
-    if (std::getenv("NCL_NO_TREE")) return;
+  bool build_tree_part(TreePart& P, int l0, int l1, int C, int trmode, int idx) {
     const auto& T = sn_;
-    const int nl = nlevels();
-    int l0 = 0;
-    while (l0 < nl && small_solve(l0)) ++l0;
-    auto eligible = [&](int l) {
-      if (lvl_fmax_[l] > kTreeMaxF || lvl_kmax_[l] >= solve_par_k()) return false;
-      for (int q = T.lvl_ptr[l]; q < T.lvl_ptr[l + 1]; ++q) {
-        const int s = T.lvl_nodes[q];
-        if (s == T.schur || T.usplit_ng[s]) return false;
-      }
-      return true;
-    };
-    int l1 = l0;
-    while (l1 < nl && eligible(l1)) ++l1;
-    if (const char* e = std::getenv("NCL_TREE_L1")) l1 = std::min(l1, std::atoi(e));  // experiments
-    if (l1 - l0 < 2) return;
     std::vector<int> list, pos(static_cast<size_t>(T.nsn), -1);
     int fmax = 0, pmax = 0;
     for (int q = T.lvl_ptr[l0]; q < T.lvl_ptr[l1]; ++q) {
@@ -868,8 +836,8 @@ class LdlSystem {
       fmax = std::max(fmax, T.f[s]);
       pmax = std::max(pmax, (T.first[s + 1] - T.first[s] + 31) / 32);
     }
-    const int per_sm = tree_ctas_per_sm(fmax, pmax);
-    if (per_sm < 1) return;
+    const int teams = tree_teams(C, fmax, pmax);
+    if (teams < 1) return false;
     std::vector<int> wptr{0}, wait, par, gbase, grow, gsrc;
     std::vector<std::vector<int>> bucket;
     for (int s : list) {
@@ -892,31 +860,104 @@ class LdlSystem {
       }
       grow.push_back(static_cast<int>(gsrc.size()));
     }
-    tr_list_.upload(list);
-    tr_wptr_.upload(wptr);
-    tr_wait_.upload(wait.empty() ? std::vector<int>{0} : wait);
-    tr_par_.upload(par);
-    tr_gbase_.upload(gbase);
-    tr_grow_.upload(grow);
-    tr_gsrc_.upload(gsrc.empty() ? std::vector<int>{0} : gsrc);
+    P.list.upload(list);
+    P.wptr.upload(wptr);
+    P.wait.upload(wait.empty() ? std::vector<int>{0} : wait);
+    P.par.upload(par);
+    P.gbase.upload(gbase);
+    P.grow.upload(grow);
+    P.gsrc.upload(gsrc.empty() ? std::vector<int>{0} : gsrc);
+    if (trmode) tr_trace_[idx].alloc(8 * list.size());
+    P.td = TreeDev{P.list.p, static_cast<int>(list.size()), P.wptr.p, P.wait.p, P.par.p,
+                   P.gbase.p, P.grow.p, P.gsrc.p, tr_flags_.p, trmode == 3 ? nullptr : tr_trace_[idx].p};
+    P.lvl.assign(list.size(), 0);
+    for (int l = l0; l < l1; ++l)
+      for (int q = T.lvl_ptr[l]; q < T.lvl_ptr[l + 1]; ++q) P.lvl[pos[T.lvl_nodes[q]]] = l;
+    P.l0 = l0;
+    P.l1 = l1;
+    P.C = C;
+    P.teams = std::min(static_cast<int>(list.size()), teams);
+    P.fmax = fmax;
+    P.pmax = pmax;
+    if (std::getenv("NCL_LEVEL_STATS"))
+      std::fprintf(stderr, "[ncl tree] levels %d-%d: %zu fronts on %d teams of %d CTAs (fmax %d, %zu gather entries)\n",
+                   l0, l1 - 1, list.size(), P.teams, C, fmax, gsrc.size());
+    return true;
+  }
+  void build_tree(int /*sms*/) {
+    if (std::getenv("NCL_NO_TREE")) return;
+    const auto& T = sn_;
+    const int nl = nlevels();
+    int l0 = 0;
+    while (l0 < nl && small_solve(l0)) ++l0;
+    auto eligible = [&](int l) {
+      if (lvl_fmax_[l] > kTreeMaxF || lvl_kmax_[l] >= solve_par_k()) return false;
+      for (int q = T.lvl_ptr[l]; q < T.lvl_ptr[l + 1]; ++q) {
+        const int s = T.lvl_nodes[q];
+        if (s == T.schur || T.usplit_ng[s]) return false;
+      }
+      return true;
+    };
+    int l1 = l0;
+    while (l1 < nl && eligible(l1)) ++l1;
+    if (const char* e = std::getenv("NCL_TREE_L1")) l1 = std::min(l1, std::atoi(e));  // experiments
+    if (l1 - l0 < 2) return;
+    // top levels for the cluster launch: a suffix of levels of at most
+    // `teams` fronts of >= kTreeClusterF rows (each front gets its cluster)
+    const int cteams = std::getenv("NCL_TREE_C") && std::atoi(std::getenv("NCL_TREE_C")) == 1
+                           ? 0
+                           : tree_teams(kTreeCluster, lvl_fmax_[l1 - 1], 1);
+    int l2 = l1;
+    while (l2 > l0 && cteams > 0 && T.lvl_ptr[l2] - T.lvl_ptr[l2 - 1] <= cteams &&
+           lvl_fmax_[l2 - 1] >= kTreeClusterF)
+      --l2;
+    if (const char* e = std::getenv("NCL_TREE_L2")) l2 = std::max(l0, std::min(l1, std::atoi(e)));
+    const int trmode = std::getenv("NCL_TREE_TRACE") ? std::atoi(std::getenv("NCL_TREE_TRACE")) : 0;
+    tr_dump_ = trmode == 1 || trmode == 3;
     tr_flags_.alloc(static_cast<size_t>(T.nsn));
     tr_flags_.zero(st_);
-    const int trmode = std::getenv("NCL_TREE_TRACE") ? std::atoi(std::getenv("NCL_TREE_TRACE")) : 0;
-    if (trmode) tr_trace_.alloc(8 * list.size());
-    tr_dump_ = trmode == 1 || trmode == 3;
-    td_ = TreeDev{tr_list_.p, static_cast<int>(list.size()), tr_wptr_.p, tr_wait_.p, tr_par_.p,
-                  tr_gbase_.p, tr_grow_.p, tr_gsrc_.p, tr_flags_.p, trmode == 3 ? nullptr : tr_trace_.p};
-    tr_lvl_.assign(list.size(), 0);
-    for (int l = l0; l < l1; ++l)
-      for (int q = T.lvl_ptr[l]; q < T.lvl_ptr[l + 1]; ++q) tr_lvl_[pos[T.lvl_nodes[q]]] = l;
-    tr_grid_ = std::min(static_cast<int>(list.size()), per_sm * sms);
-    tr_fmax_ = fmax;
-    tr_pmax_ = pmax;
+    bool ok = true;
+    if (l2 > l0) ok = build_tree_part(tp_[0], l0, l2, 1, trmode, 0);
+    if (ok && l1 > l2) ok = build_tree_part(tp_[1], l2, l1, kTreeCluster, trmode, 1);
+    if (!ok) {
+      tp_[0].l1 = tp_[0].l0;
+      tp_[1].l1 = tp_[1].l0;
+      return;
+    }
     tr_l0_ = l0;
     tr_l1_ = l1;
-    if (std::getenv("NCL_LEVEL_STATS"))
-      std::fprintf(stderr, "[ncl tree] levels %d-%d: %zu fronts on %d CTAs (fmax %d, %zu gather entries)\n",
-                   l0, l1 - 1, list.size(), tr_grid_, fmax, gsrc.size());
+  }
+  // diagnostic (NCL_TREE_TRACE=1, NCL_NO_GRAPH=1): per level, mean wait /
+  // gather / solve per front and the longest solve, per direction
+  void dump_tree_trace() {
+    for (int pi = 0; pi < 2; ++pi) {
+      const TreePart& P = tp_[pi];
+      if (!P.on() || !tr_trace_[pi].p) continue;
+      const size_t n = P.lvl.size();
+      std::vector<unsigned long long> h(8 * n);
+      CK(cudaMemcpyAsync(h.data(), tr_trace_[pi].p, h.size() * 8, cudaMemcpyDeviceToHost, st_));
+      CK(cudaStreamSynchronize(st_));
+      constexpr double us = 1.0 / 1965.0;  // SM clock stamps
+      for (int dir = 0; dir < 2; ++dir) {
+        std::fprintf(stderr, "[ncl tree trace] C=%d %s (mean us per front: wait / gather / solve, max solve):",
+                     P.C, dir ? "bwd" : "fwd");
+        for (int l = P.l0; l < P.l1; ++l) {
+          double wt = 0, ga = 0, so = 0, mx = 0;
+          int c = 0;
+          for (size_t i = 0; i < n; ++i) {
+            if (P.lvl[i] != l) continue;
+            const unsigned long long* t = &h[4 * (dir * n + i)];
+            wt += (t[1] - t[0]) * us;
+            ga += (t[2] - t[1]) * us;
+            so += (t[3] - t[2]) * us;
+            mx = std::max(mx, (t[3] - t[2]) * us);
+            ++c;
+          }
+          std::fprintf(stderr, " L%d[w%.1f g%.1f s%.1f m%.1f]", l, wt / c, ga / c, so / c, mx);
+        }
+        std::fprintf(stderr, "\n");
+      }
+    }
   }
 
   // tile-dataflow segments (dag.hpp): maximal runs of wide levels that are

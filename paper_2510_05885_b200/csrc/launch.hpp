@@ -96,11 +96,14 @@ struct TreeDev {
   unsigned long long* trace;  // diagnostic (NCL_TREE_TRACE): 4 stamps per front and direction
 };
 constexpr int kTreeMaxF = 2048;
-int tree_ctas_per_sm(int fmax, int pmax);  // 0: does not fit
+constexpr int kTreeCluster = 8;  // CTAs per front in the cluster launch (top levels)
+constexpr int kTreeClusterF = 256;  // ... for levels whose fronts reach this many rows
+// resident teams (C = 1: CTAs; C = kTreeCluster: clusters), 0 if it does not fit
+int tree_teams(int C, int fmax, int pmax);
 void launch_fwd_tree(const SnDev& sd, const TreeDev& td, const double* lval, double* w, double* uvec,
-                     int grid, int fmax, cudaStream_t st);
+                     int C, int teams, int fmax, cudaStream_t st);
 void launch_bwd_tree(const SnDev& sd, const TreeDev& td, const double* lval, const double* d,
-                     const double* w, double* x, int grid, int fmax, int pmax, cudaStream_t st);
+                     const double* w, double* x, int C, int teams, int fmax, int pmax, cudaStream_t st);
 void launch_permute_in(int n, const int* perm, const double* b, double* w,
                        cudaStream_t st);
 void launch_permute_out(int n, const int* perm, const double* xp, double* x,

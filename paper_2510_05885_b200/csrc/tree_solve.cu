@@ -13,12 +13,12 @@
 // front is only ever waited on by CTAs holding later positions: no deadlock
 // while all CTAs are resident (grid <= resident CTAs).
 //
-// Inside a front (one CTA, 9 warps):
+// Inside a front (one CTA, 8 warps):
 //   warp 0 ("chain")  -- the 32-pivot substitution chains, block by block; its
 //                        L data (the 32x32 diagonal block and the 32x32 block
 //                        next to it) is staged in shared memory by cp.async
 //                        two blocks ahead, so the chain never waits on L2;
-//   warps 1-8 ("bulk") -- apply every solved block to the rest of the front
+//   warps 1-7 ("bulk") -- apply every solved block to the rest of the front
 //                        (forward: the rows below; backward: the pivot
 //                        columns above) from register-prefetched L, one
 //                        32x32 block per step, overlapped with the chain.
@@ -34,6 +34,16 @@
 //             top] L(r, q) x_r, then x_c = L_cc^-T z_c by the shuffle chain.
 // Every sum has a fixed order, independent of the CTA that runs the front
 // (bitwise reproducible solves).
+//
+// Big fronts (the top levels: a few fronts of hundreds of rows, ~1-2 MB of L
+// each) are bandwidth-bound on one SM, so those levels run as a second
+// launch of the same kernels with thread-block clusters of C CTAs per front:
+// rank 0 keeps the chain and the pivot rows, ranks 1..C-1 split the update
+// rows (the bulk of L).  Forward, a rank reads each solved block from rank
+// 0's shared memory (DSMEM) and finishes its update rows itself; backward, a
+// rank sums its update rows' contributions per pivot column block and sends
+// the partial to rank 0, which adds the ranks' partials in rank order.
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -44,12 +54,14 @@
 #include "launch.hpp"
 #include "layout.hpp"
 
+namespace cg = cooperative_groups;
+
 namespace nclb {
 
 namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
-constexpr int kBulk = 8;                   // bulk warps
+constexpr int kBulk = 7;                   // bulk warps (8 warps: up to 255 registers)
 constexpr int kThr = 32 * (1 + kBulk);     // threads per CTA
 constexpr int kStages = 3;                 // chain head stages in flight
 constexpr int kHeadSL = 66;                // forward head: column stride (64 rows + pad; 16-byte multiple)
@@ -78,6 +90,29 @@ __device__ __forceinline__ int ld_acq_cta(const int* p) {
 // trace stamps: SM clock (durations within a CTA; %globaltimer reads slowed
 // this kernel 4x when they were used for the stamps)
 __device__ __forceinline__ unsigned long long gtime() { return static_cast<unsigned long long>(clock64()); }
+// cluster scope (generic addresses: local or another rank's shared memory)
+__device__ __forceinline__ void st_rel_cl(int* p, int v) {
+  asm volatile("st.release.cluster.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ int ld_acq_cl(const int* p) {
+  int v;
+  asm volatile("ld.acquire.cluster.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void red_rel_cl(int* p, int v) {
+  asm volatile("red.release.cluster.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ int atom_add_acqrel_cta(int* p, int v) {
+  int old;
+  asm volatile("atom.acq_rel.cta.shared::cta.add.s32 %0, [%1], %2;"
+               : "=r"(old)
+               : "r"(sptr(p)), "r"(v)
+               : "memory");
+  return old;
+}
+__device__ __forceinline__ void wait_ge_cl(const int* p, int v) {
+  while (ld_acq_cl(p) < v) __nanosleep(32);
+}
 __device__ __forceinline__ void wait_ge(const int* p, int v) {
   while (ld_acq_cta(p) < v) __nanosleep(16);
 }
@@ -103,9 +138,16 @@ __device__ __forceinline__ int rb_size(int k, int f, int P, int R) {
 
 struct FrontGeo {
   int s, c0, k, f, P, NR;
+  int rlo, rhi;  // row blocks whose bulk work this CTA owns (forward) / update blocks (backward)
   size_t ld;
   const double* L;
 };
+
+// update blocks [j0, j1) (indices from 0 at row k) of rank r >= 1 of C
+__device__ __forceinline__ void rank_share(int U, int C, int r, int& j0, int& j1) {
+  j0 = static_cast<int>((static_cast<long long>(r - 1) * U) / (C - 1));
+  j1 = static_cast<int>((static_cast<long long>(r) * U) / (C - 1));
+}
 
 __device__ __forceinline__ FrontGeo front_geo(const SnDev& sd, const double* lval, int s) {
   FrontGeo g;
@@ -117,8 +159,11 @@ __device__ __forceinline__ FrontGeo front_geo(const SnDev& sd, const double* lva
   g.NR = g.P + ((g.f - g.k + 31) >> 5);
   g.ld = wide_ld(g.f);
   g.L = lval + __ldg(sd.l_off + s);
+  g.rlo = 0;
+  g.rhi = g.NR;
   return g;
 }
+
 
 // ---------------------------------------------------------------------------
 // forward
@@ -162,7 +207,7 @@ __device__ __forceinline__ void fwd_chain(const FrontGeo& g, double* T, FwdSmem&
     }
     if (lane < nb) T[p0 + lane] = t;
     __syncwarp();
-    if (lane == 0) st_rel_cta(&sm.xdone, b + 1);
+    if (lane == 0) st_rel_cl(&sm.xdone, b + 1);  // cluster scope: other ranks read the block
     if (nxt) {  // panel b on block b+1's rows: L(32b+32+lane, 32b+q) from the head
       const bool ok = lane < nbn;
       double a0 = 0.0, a1 = 0.0;
@@ -181,20 +226,20 @@ __device__ __forceinline__ void fwd_chain(const FrontGeo& g, double* T, FwdSmem&
   cp_wait<0>();
 }
 
-// bulk items (c, R): panel c applied to row block R, R owned by this warp
-// (R % kBulk == wb), in (c, R) order; pivot blocks take panels c <= R-2
-// (panel R-1 is the chain warp's), update blocks every panel
+// bulk items (c, R): panel c applied to row block R in [rlo, rhi), R owned by
+// this warp ((R - rlo) % kBulk == wb), in (c, R) order; pivot blocks take
+// panels c <= R-2 (panel R-1 is the chain warp's), update blocks every panel
 __device__ __forceinline__ bool fwd_valid(const FrontGeo& g, int c, int R) {
   return R < g.P ? R >= c + 2 : true;
 }
 __device__ __forceinline__ bool fwd_next(const FrontGeo& g, int wb, int& c, int& R) {
   for (;;) {
     R += kBulk;
-    if (R >= g.NR) {
+    if (R >= g.rhi) {
       if (++c >= g.P) return false;
-      R = wb;
+      R = g.rlo + wb;
     }
-    if (fwd_valid(g, c, R)) return true;
+    if (R < g.rhi && fwd_valid(g, c, R)) return true;
   }
 }
 __device__ __forceinline__ void fwd_load(double (&v)[32], const FrontGeo& g, int c, int R, int lane) {
@@ -205,27 +250,43 @@ __device__ __forceinline__ void fwd_load(double (&v)[32], const FrontGeo& g, int
 #pragma unroll
   for (int q = 0; q < 32; ++q) v[q] = (ok && q < nq) ? __ldg(src + q * g.ld) : 0.0;
 }
+// T: this CTA's rows; X0/xd0: rank 0's front vector and progress (REMOTE: a
+// rank >= 1 reading them through DSMEM)
+template <bool REMOTE>
 __device__ __forceinline__ void fwd_apply(const double (&v)[32], const FrontGeo& g, int c, int R,
-                                          double* T, FwdSmem& sm, int lane) {
-  wait_ge(&sm.xdone, c + 1);
+                                          double* T, const double* X0, const int* xd0, int* cnt,
+                                          int lane) {
   const int q0 = 32 * c, nq = min(32, g.k - q0);
   double a0 = 0.0, a1 = 0.0;
+  if (REMOTE) {
+    wait_ge_cl(xd0, c + 1);
+    const double xl = lane < nq ? X0[q0 + lane] : 0.0;
 #pragma unroll
-  for (int q = 0; q < 32; q += 2) {
-    a0 = fma(v[q], q < nq ? T[q0 + q] : 0.0, a0);
-    a1 = fma(v[q + 1], q + 1 < nq ? T[q0 + q + 1] : 0.0, a1);
+    for (int q = 0; q < 32; q += 2) {
+      a0 = fma(v[q], __shfl_sync(kFull, xl, q), a0);
+      a1 = fma(v[q + 1], __shfl_sync(kFull, xl, q + 1), a1);
+    }
+  } else {
+    wait_ge(xd0, c + 1);
+#pragma unroll
+    for (int q = 0; q < 32; q += 2) {
+      a0 = fma(v[q], q < nq ? X0[q0 + q] : 0.0, a0);
+      a1 = fma(v[q + 1], q + 1 < nq ? X0[q0 + q + 1] : 0.0, a1);
+    }
   }
   const int r0 = rb_start(g.k, g.P, R), nr = rb_size(g.k, g.f, g.P, R);
   if (lane < nr) T[r0 + lane] -= a0 + a1;
   __syncwarp();
-  if (lane == 0 && R < g.P) st_rel_cta(&sm.cnt[R], c + 1);
+  if (!REMOTE && lane == 0 && R < g.P) st_rel_cta(&cnt[R], c + 1);
 }
 
-__device__ __forceinline__ void fwd_bulk(const FrontGeo& g, int wb, double* T, FwdSmem& sm) {
+template <bool REMOTE>
+__device__ __forceinline__ void fwd_bulk(const FrontGeo& g, int wb, double* T, const double* X0,
+                                         const int* xd0, int* cnt) {
   const int lane = threadIdx.x & 31;
   __syncwarp();  // the warp enters converged (the CTA's tid-0 branches)
-  int c = 0, R = wb;
-  if (R >= g.NR || g.P == 0) return;
+  int c = 0, R = g.rlo + wb;
+  if (R >= g.rhi || g.P == 0) return;
   if (!fwd_valid(g, c, R) && !fwd_next(g, wb, c, R)) return;
   double A[32], B[32];
   fwd_load(A, g, c, R, lane);
@@ -233,44 +294,67 @@ __device__ __forceinline__ void fwd_bulk(const FrontGeo& g, int wb, double* T, F
     int cb = c, Rb = R;
     const bool hb = fwd_next(g, wb, cb, Rb);
     if (hb) fwd_load(B, g, cb, Rb, lane);
-    fwd_apply(A, g, c, R, T, sm, lane);
+    fwd_apply<REMOTE>(A, g, c, R, T, X0, xd0, cnt, lane);
     if (!hb) break;
     c = cb;
     R = Rb;
     const bool ha = fwd_next(g, wb, cb, Rb);
     if (ha) fwd_load(A, g, cb, Rb, lane);
-    fwd_apply(B, g, c, R, T, sm, lane);
+    fwd_apply<REMOTE>(B, g, c, R, T, X0, xd0, cnt, lane);
     if (!ha) break;
     c = cb;
     R = Rb;
   }
 }
 
+// C = 1: one CTA per front.  C > 1: a cluster of C CTAs per front (grid =
+// clusters x C, cluster i takes list positions i, i + #clusters, ...)
+template <int C>
 __global__ void __launch_bounds__(kThr, 1)
 k_fwd_tree(SnDev sd, TreeDev td, const double* __restrict__ lval, double* w, double* uvec) {
   extern __shared__ __align__(16) double dyn[];
   FwdSmem& sm = *reinterpret_cast<FwdSmem*>(dyn);
   double* T = dyn + (sizeof(FwdSmem) + 7) / 8;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  for (int li = blockIdx.x; li < td.n; li += gridDim.x) {
-    const FrontGeo g = front_geo(sd, lval, __ldg(td.list + li));
+  cg::cluster_group cl = cg::this_cluster();
+  const int rank = C > 1 ? static_cast<int>(cl.block_rank()) : 0;
+  const int team = C > 1 ? blockIdx.x / C : blockIdx.x, nteams = C > 1 ? gridDim.x / C : gridDim.x;
+  const double* T0 = C > 1 ? cl.map_shared_rank(T, 0) : T;
+  const int* xd0 = C > 1 ? cl.map_shared_rank(&sm.xdone, 0) : &sm.xdone;
+  for (int li = team; li < td.n; li += nteams) {
+    FrontGeo g = front_geo(sd, lval, __ldg(td.list + li));
+    int row_lo = 0, row_hi = g.f;  // the front rows this CTA gathers and writes
+    if (C > 1) {
+      if (rank == 0) {
+        g.rhi = g.P;
+        row_hi = g.k;
+      } else {
+        int j0, j1;
+        rank_share(g.NR - g.P, C, rank, j0, j1);
+        g.rlo = g.P + j0;
+        g.rhi = g.P + j1;
+        row_lo = g.k + 32 * j0;
+        row_hi = min(g.f, g.k + 32 * j1);
+      }
+    }
     unsigned long long* tr = td.trace ? td.trace + 4 * static_cast<size_t>(li) : nullptr;
-    if (tr && tid == 0) tr[0] = gtime();
-    if (warp == 0)  // the chain's first L blocks do not depend on anything
+    if (tr && tid == 0 && rank == 0) tr[0] = gtime();
+    if (warp == 0 && rank == 0)  // the chain's first L blocks do not depend on anything
       for (int b = 0; b < kStages; ++b) fwd_stage(sm.head[b], g, b, lane);
     for (int i = tid; i < kMaxRB; i += kThr) sm.cnt[i] = 0;
     if (tid == 0) sm.xdone = 0;
+    if (C > 1) cl.sync();  // rank 0's progress is reset before any rank reads it
     // children's update vectors: wide children in the list publish flags
     if (warp == 1) {
       const int e0 = __ldg(td.wait_ptr + li), e1 = __ldg(td.wait_ptr + li + 1);
       for (int e = e0 + lane; e < e1; e += 32) gwait_ge(td.flags + __ldg(td.wait + e), 1);
     }
     __syncthreads();
-    if (tr && tid == 0) tr[1] = gtime();
+    if (tr && tid == 0 && rank == 0) tr[1] = gtime();
     // gather: T_r = w_r (pivot rows) + the children's entries, child order
     {
       const int* gp = td.g_row + __ldg(td.g_base + li);
-      for (int r = tid; r < g.f; r += kThr) {
+      for (int r = row_lo + tid; r < row_hi; r += kThr) {
         double v = r < g.k ? __ldcg(w + g.c0 + r) : 0.0;
         const int e0 = __ldg(gp + r), e1 = __ldg(gp + r + 1);
         for (int e = e0; e < e1; ++e) v += __ldcg(uvec + __ldg(td.g_src + e));
@@ -278,21 +362,29 @@ k_fwd_tree(SnDev sd, TreeDev td, const double* __restrict__ lval, double* w, dou
       }
     }
     __syncthreads();
-    if (tr && tid == 0) tr[2] = gtime();
-    if (warp == 0)
-      fwd_chain(g, T, sm);
-    else
-      fwd_bulk(g, warp - 1, T, sm);
+    if (tr && tid == 0 && rank == 0) tr[2] = gtime();
+    if (rank == 0) {
+      if (warp == 0)
+        fwd_chain(g, T, sm);
+      else
+        fwd_bulk<false>(g, warp - 1, T, T, &sm.xdone, sm.cnt);
+    } else if (warp > 0) {
+      fwd_bulk<true>(g, warp - 1, T, T0, xd0, sm.cnt);
+    }
     __syncthreads();
     double* u = uvec + __ldg(sd.rel_ptr + g.s);
-    for (int r = tid; r < g.f; r += kThr) {
+    for (int r = row_lo + tid; r < row_hi; r += kThr) {
       if (r < g.k)
         w[g.c0 + r] = T[r];
       else
         u[r - g.k] = T[r];
     }
-    __syncthreads();
-    if (tid == 0) {
+    if (C > 1) {
+      cl.sync();  // every rank's rows are out (and rank 0's T is no longer read)
+    } else {
+      __syncthreads();
+    }
+    if (tid == 0 && rank == 0) {
       __threadfence();
       st_release(td.flags + g.s, 1);
       if (tr) tr[3] = gtime();
@@ -308,7 +400,7 @@ struct BwdSmem {
   double head[kStages][32 * 64];
   double Ts[kBulk][32 * kTsSL];  // per bulk warp: one 32x32 block, row-major
   int xdone;                     // pivot blocks solved, counted from the last
-  int cnt[kMaxRB];               // per column block: bulk items applied
+  int cnt[kMaxRB];               // per column block: contributions applied
 };
 
 __device__ __forceinline__ void bwd_stage(double* S, const FrontGeo& g, int b, int lane) {
@@ -323,14 +415,14 @@ __device__ __forceinline__ double head_at(const double* S, int i, int q) {  // L
   return S[2 * (q * 32 + ((i >> 1) ^ (q & 7))) + (i & 1)];
 }
 
-__device__ __forceinline__ int bwd_nexp(const FrontGeo& g, int b) {
-  return (g.NR - g.P) + max(0, g.P - 2 - b);
-}
-
-__device__ __forceinline__ void bwd_chain(const FrontGeo& g, double* X, const double* acc, int pstride,
-                                          double* x, BwdSmem& sm) {
+// the chain of block b needs nexp contributions: its own CTA's items (C = 1:
+// every update block and pivot blocks b+2..P-1; C > 1: the pivot blocks) and,
+// C > 1, one partial per rank that owns update blocks
+__device__ __forceinline__ void bwd_chain(const FrontGeo& g, double* X, const double* acc, int slots,
+                                          int pstride, int nrem, double* x, BwdSmem& sm) {
   const int lane = threadIdx.x & 31;
   __syncwarp();  // the warp enters converged (the CTA's tid-0 branches)
+  const int U1 = g.rhi - g.rlo;
   for (int o = 0; o < g.P; ++o) {
     const int b = g.P - 1 - o, p0 = 32 * b, nb = min(32, g.k - p0);
     cp_wait<kStages - 1>();
@@ -352,10 +444,9 @@ __device__ __forceinline__ void bwd_chain(const FrontGeo& g, double* X, const do
     for (int i = 0; i < 32; ++i) lc[i] = (i > lane && i < nb) ? head_at(S, i, lane) : 0.0;
     __syncwarp();
     bwd_stage(sm.head[o % kStages], g, b - kStages, lane);
-    wait_ge(&sm.cnt[b], bwd_nexp(g, b));
+    wait_ge(&sm.cnt[b], U1 + max(0, g.P - 2 - b) + nrem);
     double sb = 0.0;
-#pragma unroll
-    for (int w = 0; w < kBulk; ++w) sb += acc[(w * pstride + b) * 32 + lane];
+    for (int sl = 0; sl < slots; ++sl) sb += acc[(sl * pstride + b) * 32 + lane];
     double xv = lane < nb ? X[p0 + lane] - sb - psum : 0.0;
 #pragma unroll
     for (int p = 31; p >= 0; --p) {
@@ -372,18 +463,19 @@ __device__ __forceinline__ void bwd_chain(const FrontGeo& g, double* X, const do
   cp_wait<0>();
 }
 
-// bulk items (R, b): row block R applied to column block b.  Phase 1 -- the
-// update rows, known from the start: items t = (P-1-b) * U + (R-P) (column
-// blocks from the last, where the chain starts) dealt round-robin over the
-// bulk warps; phase 2 -- pivot blocks R = P-1 .. 2 as the chain solves them,
-// items b <= R-2 with b % kBulk == wb, from b = R-2 down (the one the chain
-// needs next first).  Each warp sums into its own partials accW[wb][b]; the
-// chain adds the warps' partials in warp order.
+// bulk items (R, b): row block R applied to column block b.  Phase 1 -- this
+// CTA's update blocks [rlo, rhi), known from the start: items
+// t = (P-1-b) * U1 + (R-rlo) (column blocks from the last, where the chain
+// starts) dealt round-robin over the bulk warps; phase 2 (the chain's CTA) --
+// pivot blocks R = P-1 .. 2 as the chain solves them, items b <= R-2 with
+// b % kBulk == wb, from b = R-2 down (the one the chain needs next first).
 struct BwdIt {
   int t, R, b;
 };
-__device__ __forceinline__ bool bwd_phase2_from(const FrontGeo& g, int wb, BwdIt& it, int R) {
+__device__ __forceinline__ bool bwd_phase2_from(const FrontGeo& g, int wb, BwdIt& it, int R,
+                                                bool ph2) {
   it.t = 0x7fffffff;
+  if (!ph2) return false;
   for (; R >= 2; --R) {
     const int m = R - 2;
     if (m >= wb) {
@@ -395,26 +487,26 @@ __device__ __forceinline__ bool bwd_phase2_from(const FrontGeo& g, int wb, BwdIt
   return false;
 }
 __device__ __forceinline__ bool bwd_set1(const FrontGeo& g, BwdIt& it) {
-  const int U = g.NR - g.P;
-  if (it.t >= g.P * U) return false;
-  it.b = g.P - 1 - it.t / U;
-  it.R = g.P + it.t % U;
+  const int U1 = g.rhi - g.rlo;
+  if (it.t >= g.P * U1) return false;
+  it.b = g.P - 1 - it.t / U1;
+  it.R = g.rlo + it.t % U1;
   return true;
 }
-__device__ __forceinline__ bool bwd_first(const FrontGeo& g, int wb, BwdIt& it) {
+__device__ __forceinline__ bool bwd_first(const FrontGeo& g, int wb, BwdIt& it, bool ph2) {
   it.t = wb;
   if (bwd_set1(g, it)) return true;
-  return bwd_phase2_from(g, wb, it, g.P - 1);
+  return bwd_phase2_from(g, wb, it, g.P - 1, ph2);
 }
-__device__ __forceinline__ bool bwd_next(const FrontGeo& g, int wb, BwdIt& it) {
+__device__ __forceinline__ bool bwd_next(const FrontGeo& g, int wb, BwdIt& it, bool ph2) {
   if (it.t != 0x7fffffff) {
     it.t += kBulk;
     if (bwd_set1(g, it)) return true;
-    return bwd_phase2_from(g, wb, it, g.P - 1);
+    return bwd_phase2_from(g, wb, it, g.P - 1, ph2);
   }
   it.b -= kBulk;
   if (it.b >= 0) return true;
-  return bwd_phase2_from(g, wb, it, it.R - 1);
+  return bwd_phase2_from(g, wb, it, it.R - 1, ph2);
 }
 __device__ __forceinline__ void bwd_load(double (&v)[32], const FrontGeo& g, int R, int b, int lane) {
   const int r0 = rb_start(g.k, g.P, R), nr = rb_size(g.k, g.f, g.P, R);
@@ -427,9 +519,22 @@ __device__ __forceinline__ void bwd_load(double (&v)[32], const FrontGeo& g, int
 __device__ __forceinline__ void red_rel_cta(int* p, int v) {
   asm volatile("red.release.cta.shared::cta.add.s32 [%0], %1;" ::"r"(sptr(p)), "r"(v) : "memory");
 }
+
+// remote rank (C > 1, rank >= 1): partial sums of its update rows per column
+// block, summed over its bulk warps in warp order when the block's last item
+// lands, then sent to rank 0's slot `rank` with one release add on rank 0's
+// counter
+struct BwdRemote {
+  double* acc0;  // rank 0's partial slots (DSMEM)
+  int* cnt0;     // rank 0's counters (DSMEM)
+  const double* accw_all;  // this rank's per-warp partials
+  int pstride, rank;
+};
+
+template <bool REMOTE>
 __device__ __forceinline__ void bwd_apply(const double (&v)[32], const FrontGeo& g, int R, int b,
                                           const double* X, double* accw, double* Ts, BwdSmem& sm,
-                                          int lane) {
+                                          const BwdRemote& rm, int lane) {
   if (R < g.P) wait_ge(&sm.xdone, g.P - R);
   const int r0 = rb_start(g.k, g.P, R), nr = rb_size(g.k, g.f, g.P, R);
 #pragma unroll
@@ -441,71 +546,132 @@ __device__ __forceinline__ void bwd_apply(const double (&v)[32], const FrontGeo&
     if (i < nr) a = fma(Ts[i * kTsSL + lane], X[r0 + i], a);
   accw[32 * b + lane] = a;
   __syncwarp();
-  if (lane == 0) red_rel_cta(&sm.cnt[b], 1);
+  if (!REMOTE) {
+    if (lane == 0) red_rel_cta(&sm.cnt[b], 1);
+    return;
+  }
+  int last = 0;
+  if (lane == 0) last = atom_add_acqrel_cta(&sm.cnt[b], 1) == (g.rhi - g.rlo) - 1;
+  last = __shfl_sync(kFull, last, 0);
+  if (!last) return;
+  __syncwarp();
+  double s = 0.0;
+  for (int w = 0; w < kBulk; ++w) s += rm.accw_all[(w * rm.pstride + b) * 32 + lane];
+  rm.acc0[(rm.rank * rm.pstride + b) * 32 + lane] = s;
+  __syncwarp();
+  if (lane == 0) red_rel_cl(rm.cnt0 + b, 1);
 }
 
+template <bool REMOTE>
 __device__ __forceinline__ void bwd_bulk(const FrontGeo& g, int wb, const double* X, double* accw,
-                                         BwdSmem& sm) {
+                                         BwdSmem& sm, bool ph2, const BwdRemote& rm) {
   const int lane = threadIdx.x & 31;
   __syncwarp();  // the warp enters converged (the CTA's tid-0 branches)
   BwdIt it;
-  if (!bwd_first(g, wb, it)) return;
+  if (!bwd_first(g, wb, it, ph2)) return;
   double* Ts = sm.Ts[wb];
   double A[32], B[32];
   bwd_load(A, g, it.R, it.b, lane);
   for (;;) {
     BwdIt nx = it;
-    const bool hb = bwd_next(g, wb, nx);
+    const bool hb = bwd_next(g, wb, nx, ph2);
     if (hb) bwd_load(B, g, nx.R, nx.b, lane);
-    bwd_apply(A, g, it.R, it.b, X, accw, Ts, sm, lane);
+    bwd_apply<REMOTE>(A, g, it.R, it.b, X, accw, Ts, sm, rm, lane);
     if (!hb) break;
     it = nx;
-    const bool ha = bwd_next(g, wb, nx);
+    const bool ha = bwd_next(g, wb, nx, ph2);
     if (ha) bwd_load(A, g, nx.R, nx.b, lane);
-    bwd_apply(B, g, it.R, it.b, X, accw, Ts, sm, lane);
+    bwd_apply<REMOTE>(B, g, it.R, it.b, X, accw, Ts, sm, rm, lane);
     if (!ha) break;
     it = nx;
   }
 }
 
+// partial slots: C = 1, one per bulk warp; C > 1, rank 0 keeps slot 0 for its
+// pivot-row items (each column block belongs to one warp there) and slot r
+// for rank r's partials, ranks >= 1 one per bulk warp
+template <int C>
 __global__ void __launch_bounds__(kThr, 1)
 k_bwd_tree(SnDev sd, TreeDev td, const double* __restrict__ lval, const double* __restrict__ d,
            const double* __restrict__ w, double* x, int pmax) {
   extern __shared__ __align__(16) double dyn[];
   BwdSmem& sm = *reinterpret_cast<BwdSmem*>(dyn);
-  double* acc = dyn + (sizeof(BwdSmem) + 7) / 8;  // kBulk x pmax x 32: the bulk warps' partials
-  double* X = acc + kBulk * 32 * pmax;             // front rows
+  constexpr int kSlots = C > kBulk ? C : kBulk;
+  double* acc = dyn + (sizeof(BwdSmem) + 7) / 8;  // kSlots x pmax x 32
+  double* X = acc + kSlots * 32 * pmax;            // front rows
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  for (int li0 = blockIdx.x; li0 < td.n; li0 += gridDim.x) {
+  cg::cluster_group cl = cg::this_cluster();
+  const int rank = C > 1 ? static_cast<int>(cl.block_rank()) : 0;
+  const int team = C > 1 ? blockIdx.x / C : blockIdx.x, nteams = C > 1 ? gridDim.x / C : gridDim.x;
+  BwdRemote rm{};
+  if (C > 1) {
+    rm.acc0 = cl.map_shared_rank(acc, 0);
+    rm.cnt0 = cl.map_shared_rank(sm.cnt, 0);
+    rm.accw_all = acc;
+    rm.pstride = pmax;
+    rm.rank = rank;
+  }
+  for (int li0 = team; li0 < td.n; li0 += nteams) {
     const int li = td.n - 1 - li0;
-    const FrontGeo g = front_geo(sd, lval, __ldg(td.list + li));
+    FrontGeo g = front_geo(sd, lval, __ldg(td.list + li));
+    const int U = g.NR - g.P;
+    int nrem = 0;
+    if (C > 1) {
+      for (int r = 1; r < C; ++r) {
+        int j0, j1;
+        rank_share(U, C, r, j0, j1);
+        nrem += j1 > j0;
+      }
+      if (rank == 0) {
+        g.rlo = g.rhi = g.P;  // no update rows
+      } else {
+        int j0, j1;
+        rank_share(U, C, rank, j0, j1);
+        g.rlo = g.P + j0;
+        g.rhi = g.P + j1;
+      }
+    } else {
+      g.rlo = g.P;
+      g.rhi = g.NR;
+    }
     unsigned long long* tr = td.trace ? td.trace + 4 * static_cast<size_t>(td.n + li) : nullptr;
-    if (tr && tid == 0) tr[0] = gtime();
-    if (warp == 0)
+    if (tr && tid == 0 && rank == 0) tr[0] = gtime();
+    if (warp == 0 && rank == 0)
       for (int o = 0; o < kStages; ++o) bwd_stage(sm.head[o], g, g.P - 1 - o, lane);
     for (int i = tid; i < kMaxRB; i += kThr) sm.cnt[i] = 0;
-    for (int w = 0; w < kBulk; ++w)
-      for (int i = tid; i < 32 * g.P; i += kThr) acc[w * 32 * pmax + i] = 0.0;
+    for (int sl = 0; sl < kSlots; ++sl)
+      for (int i = tid; i < 32 * g.P; i += kThr) acc[sl * 32 * pmax + i] = 0.0;
     if (tid == 0) sm.xdone = 0;
     // z_q = w_q / d_q for the pivots (the forward result, final)
-    for (int q = tid; q < g.k; q += kThr) X[q] = __ldg(w + g.c0 + q) / __ldg(d + g.c0 + q);
-    // the parent's solution rows
+    if (rank == 0)
+      for (int q = tid; q < g.k; q += kThr) X[q] = __ldg(w + g.c0 + q) / __ldg(d + g.c0 + q);
+    if (C > 1) cl.sync();  // rank 0's slots and counters are reset before any rank adds to them
+    // the parent's solution rows (the CTAs that own update rows)
     const int par = __ldg(td.par + li);
-    if (tid == 0 && par >= 0) gwait_ge(td.flags + par, 2);
+    if (tid == 0 && par >= 0 && g.rhi > g.rlo) gwait_ge(td.flags + par, 2);
     __syncthreads();
-    if (tr && tid == 0) tr[1] = gtime();
-    {
+    if (tr && tid == 0 && rank == 0) tr[1] = gtime();
+    if (g.rhi > g.rlo) {
       const int* rows = sd.rows + __ldg(sd.rows_ptr + g.s);
-      for (int r = g.k + tid; r < g.f; r += kThr) X[r] = __ldcg(x + __ldg(rows + r));
+      const int r1 = min(g.f, rb_start(g.k, g.P, g.rhi - 1) + 32);
+      for (int r = rb_start(g.k, g.P, g.rlo) + tid; r < r1; r += kThr) X[r] = __ldcg(x + __ldg(rows + r));
     }
     __syncthreads();
-    if (tr && tid == 0) tr[2] = gtime();
-    if (warp == 0)
-      bwd_chain(g, X, acc, pmax, x, sm);
-    else
-      bwd_bulk(g, warp - 1, X, acc + (warp - 1) * 32 * pmax, sm);
-    __syncthreads();
-    if (tid == 0) {
+    if (tr && tid == 0 && rank == 0) tr[2] = gtime();
+    if (rank == 0) {
+      if (warp == 0)
+        bwd_chain(g, X, acc, C > 1 ? C : kBulk, pmax, C > 1 ? nrem : 0, x, sm);
+      else
+        bwd_bulk<false>(g, warp - 1, X, C > 1 ? acc : acc + (warp - 1) * 32 * pmax, sm, true, rm);
+    } else if (warp > 0) {
+      bwd_bulk<true>(g, warp - 1, X, acc + (warp - 1) * 32 * pmax, sm, false, rm);
+    }
+    if (C > 1) {
+      cl.sync();  // rank 0 is done with its slots; every rank's x rows are out
+    } else {
+      __syncthreads();
+    }
+    if (tid == 0 && rank == 0) {
       __threadfence();
       st_release(td.flags + g.s, 2);
       if (tr) tr[3] = gtime();
@@ -515,9 +681,16 @@ k_bwd_tree(SnDev sd, TreeDev td, const double* __restrict__ lval, const double* 
 
 }  // namespace
 
-size_t fwd_tree_smem(int fmax) { return (sizeof(FwdSmem) + 7) / 8 * 8 + sizeof(double) * fmax; }
-size_t bwd_tree_smem(int fmax, int pmax) {
-  return (sizeof(BwdSmem) + 7) / 8 * 8 + sizeof(double) * (kBulk * 32 * pmax + fmax);
+static size_t fwd_tree_smem(int fmax) { return (sizeof(FwdSmem) + 7) / 8 * 8 + sizeof(double) * fmax; }
+static size_t bwd_tree_smem(int fmax, int pmax, int C) {
+  const int slots = C > kBulk ? C : kBulk;
+  return (sizeof(BwdSmem) + 7) / 8 * 8 + sizeof(double) * (static_cast<size_t>(slots) * 32 * pmax + fmax);
+}
+
+template <int C>
+static void tree_init_c(int optin) {
+  cudaFuncSetAttribute(k_fwd_tree<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
+  cudaFuncSetAttribute(k_bwd_tree<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
 }
 
 static void tree_init() {
@@ -526,36 +699,88 @@ static void tree_init() {
     int dev = 0, optin = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    cudaFuncSetAttribute(k_fwd_tree, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
-    cudaFuncSetAttribute(k_bwd_tree, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
+    tree_init_c<1>(optin);
+    tree_init_c<kTreeCluster>(optin);
   });
 }
 
-// resident CTAs per SM for both directions at these sizes (0: does not fit)
-int tree_ctas_per_sm(int fmax, int pmax) {
+// resident teams (C = 1: CTAs, C > 1: clusters) for both directions at these
+// sizes (0: does not fit)
+int tree_teams(int C, int fmax, int pmax) {
   tree_init();
   if (fmax > kTreeMaxF || (fmax + 31) / 32 + 2 > kMaxRB) return 0;
-  int a = 0, b = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, k_fwd_tree, kThr, fwd_tree_smem(fmax)) !=
-          cudaSuccess ||
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_bwd_tree, kThr, bwd_tree_smem(fmax, pmax)) !=
-          cudaSuccess) {
-    cudaGetLastError();
-    return 0;
+  if (C != 1 && C != kTreeCluster) return 0;
+  int res[2] = {0, 0};
+  for (int dir = 0; dir < 2; ++dir) {
+    const void* fn = C == 1 ? (dir ? reinterpret_cast<const void*>(k_bwd_tree<1>)
+                                   : reinterpret_cast<const void*>(k_fwd_tree<1>))
+                            : (dir ? reinterpret_cast<const void*>(k_bwd_tree<kTreeCluster>)
+                                   : reinterpret_cast<const void*>(k_fwd_tree<kTreeCluster>));
+    const size_t smem = dir ? bwd_tree_smem(fmax, pmax, C) : fwd_tree_smem(fmax);
+    if (C == 1) {
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&res[dir], fn, kThr, smem) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+      }
+      int dev = 0, sms = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      res[dir] *= sms;
+    } else {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(static_cast<unsigned>(C));
+      cfg.blockDim = dim3(kThr);
+      cfg.dynamicSmemBytes = smem;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = static_cast<unsigned>(C);
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      if (cudaOccupancyMaxActiveClusters(&res[dir], fn, &cfg) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+      }
+    }
   }
-  return a < b ? a : b;
+  return res[0] < res[1] ? res[0] : res[1];
+}
+
+template <class Kern, class... Args>
+static void launch_c(Kern kern, int C, int teams, size_t smem, cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(teams * C));
+  cfg.blockDim = dim3(kThr);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = static_cast<unsigned>(C);
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  CK(cudaLaunchKernelEx(&cfg, kern, args...));
 }
 
 void launch_fwd_tree(const SnDev& sd, const TreeDev& td, const double* lval, double* w, double* uvec,
-                     int grid, int fmax, cudaStream_t st) {
+                     int C, int teams, int fmax, cudaStream_t st) {
   tree_init();
-  k_fwd_tree<<<grid, kThr, fwd_tree_smem(fmax), st>>>(sd, td, lval, w, uvec);
+  if (C == 1)
+    launch_c(k_fwd_tree<1>, 1, teams, fwd_tree_smem(fmax), st, sd, td, lval, w, uvec);
+  else
+    launch_c(k_fwd_tree<kTreeCluster>, kTreeCluster, teams, fwd_tree_smem(fmax), st, sd, td, lval, w, uvec);
 }
 
 void launch_bwd_tree(const SnDev& sd, const TreeDev& td, const double* lval, const double* d,
-                     const double* w, double* x, int grid, int fmax, int pmax, cudaStream_t st) {
+                     const double* w, double* x, int C, int teams, int fmax, int pmax, cudaStream_t st) {
   tree_init();
-  k_bwd_tree<<<grid, kThr, bwd_tree_smem(fmax, pmax), st>>>(sd, td, lval, d, w, x, pmax);
+  if (C == 1)
+    launch_c(k_bwd_tree<1>, 1, teams, bwd_tree_smem(fmax, pmax, 1), st, sd, td, lval, d, w, x, pmax);
+  else
+    launch_c(k_bwd_tree<kTreeCluster>, kTreeCluster, teams, bwd_tree_smem(fmax, pmax, kTreeCluster), st,
+             sd, td, lval, d, w, x, pmax);
 }
 
 }  // namespace nclb
