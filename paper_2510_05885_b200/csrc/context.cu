@@ -190,6 +190,27 @@ class LdlSystem {
       // overlaps it on st2_ (every tile still sees the panels in order: the
       // strip of g waits for the rest of g-1, the panel of g for the rest of g-2)
       const int g0 = T.lp_ptr[l], g1 = T.lp_ptr[l + 1];
+      if (fused_panel_) {
+        // the strip update of panel g-1 runs inside panel g's kernel; panel g
+        // waits for the rest update of g-2, the rest update of g (stream 2,
+        // also writing panel g's L11) for panel g; L11 scratch by parity
+        for (int g = g0; g < g1; ++g) {
+          const int nd = T.dg_ptr[g + 1] - T.dg_ptr[g];
+          const int np = T.pn_ptr[g + 1] - T.pn_ptr[g];
+          const int nt = T.tl_ptr[g + 1] - T.tl_ptr[g];
+          double* scr = dscr_.p + static_cast<size_t>((g - g0) & 1) * std::max(1, T.max_dg) * (kWidePanel * kWidePanel);
+          if (g - 2 >= g0) CK(cudaStreamWaitEvent(st_, ev_rest(g - 2), 0));
+          launch_wide_panel_f(sd_, fd, pn_tasks_.p + T.pn_ptr[g], np, g - g0, eps, scr, st_);
+          CK(cudaEventRecord(ev_panel(g), st_));
+          CK(cudaStreamWaitEvent(st2_, ev_panel(g), 0));
+          launch_wide_update(sd_, fd, tiles_.p + T.tl_ptr[g], nt, dg_nodes_.p + T.dg_ptr[g], nd, g - g0,
+                             st2_, false, scr);
+          CK(cudaEventRecord(ev_rest(g), st2_));
+          launches_ += (np > 0) + (nt > 0 || nd > 0);
+        }
+        if (g1 > g0) CK(cudaStreamWaitEvent(st_, ev_rest(g1 - 1), 0));
+        continue;
+      }
       for (int g = g0; g < g1; ++g) {
         const int nd = T.dg_ptr[g + 1] - T.dg_ptr[g];
         const int np = T.pn_ptr[g + 1] - T.pn_ptr[g];
@@ -574,7 +595,7 @@ class LdlSystem {
       pt[i] = make_int4(T.pn_tasks[i][0], T.pn_tasks[i][1], T.pn_tasks[i][2], T.pn_tasks[i][3]);
     pn_tasks_.upload(pt);
     dg_nodes_.upload(T.dg_nodes);
-    dscr_.alloc(static_cast<size_t>(std::max(1, T.max_dg)) * (kWidePanel * kWidePanel));
+    dscr_.alloc(2 * static_cast<size_t>(std::max(1, T.max_dg)) * (kWidePanel * kWidePanel));
     split_ng_.upload(T.split_ng);
     split_off_.upload(T.split_off);
     usplit_ng_.upload(T.usplit_ng);
@@ -1063,6 +1084,8 @@ class LdlSystem {
   bool pipe_ = true;                       // pipelined warp-tier factor walk (long chains)
   int epoch_ = 1;  // the factorization uses epoch 1, solves 2, 3, ...
   bool use_graph_ = std::getenv("NCL_NO_GRAPH") == nullptr;
+  // huge levels: strip update folded into the panel kernel (NCL_NO_FUSED_PANEL=1: separate launch)
+  bool fused_panel_ = std::getenv("NCL_NO_FUSED_PANEL") == nullptr;
   int nfact_ = 0;
   cudaGraphExec_t graph_exec_ = nullptr;
   const double* g_kval_ = nullptr;

@@ -53,8 +53,14 @@ void launch_wide_assemble(const SnDev& sd, const FactorDev& fd, const double* kv
                           const int4* tasks, int count, cudaStream_t st);
 void launch_wide_panel(const SnDev& sd, const FactorDev& fd, const int4* tasks, int count,
                        int panel, double eps, cudaStream_t st);
+// scr: the scaled L11 blocks of the nd fronts (nullptr: fd.dscr)
 void launch_wide_update(const SnDev& sd, const FactorDev& fd, const int4* tiles, int count,
-                        const int* fronts, int nd, int panel, cudaStream_t st, bool pdl);
+                        const int* fronts, int nd, int panel, cudaStream_t st, bool pdl,
+                        const double* scr = nullptr);
+// k_wide_panel with the previous panel's strip update folded in (scr: this
+// panel's L11 scratch slots)
+void launch_wide_panel_f(const SnDev& sd, const FactorDev& fd, const int4* tasks, int count, int panel,
+                         double eps, double* scr, cudaStream_t st);
 void launch_fwd_warp(const SnDev& sd, const double* lval, double* w, double* uvec,
                      int* flags, int epoch, int* counter, int npaths, int grid, bool pipe,
                      cudaStream_t st);

@@ -300,9 +300,10 @@ __device__ __forceinline__ void diag_steps(int pb, int pe, int nb, double eps, d
 // cycles per pivot are serial and the rest of the row update overlaps it.
 __device__ __noinline__ void diag_block(const double* F, size_t ld, int p0, int nb, double eps,
                                         PanelSmem& sm, double* D, double* dout, int* stats,
-                                        int* prog) {
+                                        int* prog, bool staged = false) {
   const int lane = threadIdx.x & 31;
-  const int sh = stage_block<kNR2>(D, kSL, F, ld, p0, p0, nb, lane, 32);
+  // staged: D already holds the block (p0 is even: no shift)
+  const int sh = staged ? 0 : stage_block<kNR2>(D, kSL, F, ld, p0, p0, nb, lane, 32);
   double* us = &sm.Us[0][0];
   for (int i = lane; i < kWidePanel * kWidePanel; i += 32) us[i] = 0.0;
   cp_wait_all();
@@ -364,13 +365,15 @@ __device__ __forceinline__ void trsm_steps(int pb, int pe, double (&x)[kWidePane
 template <int NTHR>
 __device__ __noinline__ void trsm_rows(double* F, size_t ld, int p0, int nb, int row_lo,
                                        int row_hi, const double* us, const double* rinv,
-                                       int* stats, int vt, double* TR, const int* prog, int bar) {
+                                       int* stats, int vt, double* TR, const int* prog, int bar,
+                                       bool staged = false) {
   constexpr int nthr = NTHR, SLT = NTHR + 2;
   bool bad = false;
+  // staged: TR already holds the rows (one round: row_hi - row_lo <= NTHR)
   for (int base = row_lo; base < row_hi; base += nthr) {
     const int nr = min(nthr, row_hi - base);
-    const int sh = stage_block<(NTHR + 2) / 2>(TR, SLT, F, ld, base, p0, nb, vt, nthr);
-    cp_wait_all();
+    const int sh = staged ? (base & 1) : stage_block<(NTHR + 2) / 2>(TR, SLT, F, ld, base, p0, nb, vt, nthr);
+    if (!staged) cp_wait_all();
     named_bar(bar, nthr);
     if (vt < nr) {
       double x[kWidePanel];
@@ -623,11 +626,103 @@ k_wide_panel(SnDev sd, FactorDev fd, const int4* __restrict__ tasks, int panel, 
   }
 }
 
+// C (shared memory, column stride SC, row shift shC) -= A diag(d) B^T for a
+// 32x32 tile over the 32 columns of the previous panel (A, B staged with
+// column stride kSL); 4 warps, warp gw rows gw*8..+8, on DMMA
+__device__ __forceinline__ void strip_mma(double* Cs, int SC, int shC, const double* A, int shA,
+                                          const double* Bs, int shB, const double* d, int gt) {
+  const int lane = gt & 31, gw = gt >> 5, g = lane >> 2, tq = lane & 3;
+  const int rr = gw * 8 + g;
+  double acc[4][2];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) acc[j][0] = acc[j][1] = 0.0;
+#pragma unroll
+  for (int kk = 0; kk < kWidePanel / 4; ++kk) {
+    const int q = kk * 4 + tq;
+    const double a = A[q * kSL + rr + shA];
+    const double dq = d[q];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) dmma_m8n8k4(acc[j][0], acc[j][1], a, Bs[q * kSL + j * 8 + g + shB] * dq);
+  }
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) Cs[(j * 8 + tq * 2 + e) * SC + rr + shC] -= acc[j][e];
+}
+
+// k_wide_panel with the lookahead strip folded in: for panel g >= 1 the CTA
+// first applies panel g-1's update to panel g's columns -- of the diagonal
+// rows (every CTA, like the diagonal block itself) and of its own rows --
+// straight into shared memory (DMMA), and factors / solves from there.  The
+// previous panel's L is final in the front (its kernel completed: this launch
+// follows it on the stream), and every earlier panel's update of these
+// columns is in (the host orders this launch after the rest update of panel
+// g-2).  The scaled L11 goes to the scratch slot `scr` (the rest-update
+// launch of this panel writes it into the front).
+__global__ void __launch_bounds__(kHugeRows)
+k_wide_panel_f(SnDev sd, FactorDev fd, const int4* __restrict__ tasks, int panel, double eps,
+               double* scr_base) {
+  __shared__ PanelSmem sm;
+  __shared__ __align__(16) double D[kWidePanel * kSL];
+  extern __shared__ __align__(16) double dyn_smem[];
+  double* TR = dyn_smem;                         // kWidePanel x kSLT
+  double* A = TR + kWidePanel * kSLT;            // 4 blocks of kWidePanel x kSL
+  double* dv = A + 4 * kWidePanel * kSL;         // previous panel's pivots
+  const int4 task = tasks[blockIdx.x];
+  const int s = task.x, rb = task.y;
+  const int c0 = sd.first[s], k = sd.first[s + 1] - c0, f = sd.f[s];
+  const size_t ld = wide_ld(f);
+  const int p0 = panel * kWidePanel, p1 = min(p0 + kWidePanel, k), nb = p1 - p0;
+  double* F = fd.lval + sd.l_off[s];
+  const int lo = p1 + rb * kPanelRows, hi = min(f, lo + kPanelRows);
+  const int nrow = max(0, hi - lo);
+  const int t = threadIdx.x;
+  if (t == 0) sm.prog = 0;
+  pdl_launch_dependents();
+  pdl_wait();  // the previous panel (programmatic launch)
+  if (panel > 0) {
+    const int q0 = p0 - kWidePanel;  // panel g-1: 32 columns (not a front's last panel)
+    stage_block<kNR2>(A, kSL, F, ld, p0, q0, kWidePanel, t, kHugeRows);
+    for (int j = 0; 32 * j < nrow; ++j)
+      stage_block<kNR2>(A + (j + 1) * kWidePanel * kSL, kSL, F, ld, lo + 32 * j, q0, kWidePanel, t,
+                        kHugeRows);
+    // the strip is the whole 32-column block: on a front's last (partial)
+    // panel its columns [p1, p0+32) are trailing entries, updated here and
+    // written back below (rows >= p1 are this CTA's rows: each entry once)
+    const int ncs = min(kWidePanel, f - p0);
+    stage_block<kNR2>(D, kSL, F, ld, p0, p0, nb, t, kHugeRows);
+    if (nrow > 0) stage_block<(kTrsRows + 2) / 2>(TR, kSLT, F, ld, lo, p0, ncs, t, kHugeRows);
+    if (t < kWidePanel) dv[t] = __ldcg(fd.d + c0 + q0 + t);
+    cp_wait_all();
+    __syncthreads();
+    const int sh = lo & 1;
+    strip_mma(D, kSL, 0, A, 0, A, 0, dv, t);
+    for (int j = 0; 32 * j < nrow; ++j)
+      strip_mma(TR + 32 * j, kSLT, sh, A + (j + 1) * kWidePanel * kSL, sh, A, 0, dv, t);
+    __syncthreads();
+    for (int c = nb; c < ncs; ++c)
+      for (int i = t; i < nrow; i += kHugeRows)
+        if (lo + i >= p0 + c) F[(lo + i) + static_cast<size_t>(p0 + c) * ld] = TR[c * kSLT + i + sh];
+  }
+  __syncthreads();
+  if (t < 32) {
+    diag_block(F, ld, p0, nb, eps, sm, D, rb == 0 ? fd.d + c0 + p0 : nullptr,
+               rb == 0 ? fd.stats : nullptr, &sm.prog, panel > 0);
+    if (rb == 0) {
+      double* scr = scr_base + static_cast<size_t>(task.z) * (kWidePanel * kWidePanel);
+      for (int i = t; i < kWidePanel * kWidePanel; i += 32) scr[i] = sm.Lsh[i / kWidePanel][i % kWidePanel];
+    }
+  } else {
+    trsm_rows<kTrsRows>(F, ld, p0, nb, lo, max(lo, hi), &sm.Us[0][0], sm.rinv, fd.stats, t - 32, TR,
+                        &sm.prog, 1, panel > 0);
+  }
+}
+
 // one 4-warp group (CTA) per 32x32 tile; block 0 also writes the panel's L11
 // blocks from the scratch slots of the nd fronts
 __global__ void __launch_bounds__(128)
 k_wide_update(SnDev sd, FactorDev fd, const int4* __restrict__ tiles, int count,
-              const int* __restrict__ fronts, int nd, int panel) {
+              const int* __restrict__ fronts, int nd, int panel, const double* scr_base) {
   __shared__ __align__(16) GroupSmem G;
   pdl_launch_dependents();
   pdl_wait();  // the panel kernel (programmatic launch on the main stream)
@@ -637,7 +732,7 @@ k_wide_update(SnDev sd, FactorDev fd, const int4* __restrict__ tiles, int count,
       const int c0 = sd.first[s], k = sd.first[s + 1] - c0, f = sd.f[s];
       const size_t ld = wide_ld(f);
       const int p0 = panel * kWidePanel, nb = min(p0 + kWidePanel, k) - p0;
-      const double* scr = fd.dscr + static_cast<size_t>(di) * (kWidePanel * kWidePanel);
+      const double* scr = scr_base + static_cast<size_t>(di) * (kWidePanel * kWidePanel);
       double* F = fd.lval + sd.l_off[s];
       for (int idx = threadIdx.x; idx < kWidePanel * kWidePanel; idx += blockDim.x) {
         const int i = idx / kWidePanel, p = idx % kWidePanel;
@@ -744,9 +839,21 @@ void launch_wide_panel(const SnDev& sd, const FactorDev& fd, const int4* tasks, 
 }
 
 void launch_wide_update(const SnDev& sd, const FactorDev& fd, const int4* tiles, int count,
-                        const int* fronts, int nd, int panel, cudaStream_t st, bool pdl) {
+                        const int* fronts, int nd, int panel, cudaStream_t st, bool pdl,
+                        const double* scr) {
   const int blocks = count > 0 ? count : (nd > 0 ? 1 : 0);
-  if (blocks) launch_pdl(k_wide_update, blocks, 128, 0, st, pdl, sd, fd, tiles, count, fronts, nd, panel);
+  if (blocks)
+    launch_pdl(k_wide_update, blocks, 128, 0, st, pdl, sd, fd, tiles, count, fronts, nd, panel,
+               scr ? scr : static_cast<const double*>(fd.dscr));
+}
+
+void launch_wide_panel_f(const SnDev& sd, const FactorDev& fd, const int4* tasks, int count, int panel,
+                         double eps, double* scr, cudaStream_t st) {
+  static PerDeviceOnce init;
+  constexpr int bytes = static_cast<int>(sizeof(double)) *
+                        (kWidePanel * kSLT + 4 * kWidePanel * kSL + kWidePanel);
+  init([] { cudaFuncSetAttribute(k_wide_panel_f, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes); });
+  if (count) launch_pdl(k_wide_panel_f, count, kHugeRows, bytes, st, true, sd, fd, tasks, panel, eps, scr);
 }
 
 // ---------------------------------------------------------------------------
