@@ -134,6 +134,7 @@ class LdlSystem {
 
   void factorize_direct(const double* kval, double eps) {
     CK(cudaMemsetAsync(ds_.p, 0, sizeof(int) * 4, st_));
+    if (huge_ctas_ > 0) CK(cudaMemsetAsync(hcnt_.p, 0, sizeof(int) * hcnt_.n, st_));
     FactorDev fd = factor_dev();
     if (sn_.path_ptr.size() > 1) {
       CK(cudaMemsetAsync(counter_.p, 0, sizeof(int), st_));
@@ -190,6 +191,39 @@ class LdlSystem {
       // overlaps it on st2_ (every tile still sees the panels in order: the
       // strip of g waits for the rest of g-1, the panel of g for the rest of g-2)
       const int g0 = T.lp_ptr[l], g1 = T.lp_ptr[l + 1];
+      if (huge_ctas_ > 0) {  // the level's panels as one persistent launch
+        HugeDev h{pn_tasks_.p, pn_ptr_.p, tiles_.p, tl_ptr_.p, dg_nodes_.p, dg_ptr_.p, g0, g1,
+                  hcnt_.p, hcnt_.p + T.lp_ptr.back(), dscr_.p, std::max(1, T.max_dg), 0, huge_ctas_,
+                  htrace_.p};
+        int mp = 1;
+        for (int g = g0; g < g1; ++g) mp = std::max(mp, T.pn_ptr[g + 1] - T.pn_ptr[g]);
+        h.npc = std::min(mp, huge_ctas_ / 2);
+        launch_huge_level(sd_, fd, h, eps, st_);
+        launches_ += 1;
+        if (htrace_.p && l == nlevels() - 1) {  // diagnostic: mean clocks per panel task phase, per level
+          std::vector<long long> hs(htrace_.n);
+          CK(cudaMemcpyAsync(hs.data(), htrace_.p, hs.size() * 8, cudaMemcpyDeviceToHost, st_));
+          CK(cudaStreamSynchronize(st_));
+          for (int l2 = 0; l2 < nlevels(); ++l2) {
+            double w = 0, a = 0, dg = 0, tr = 0;
+            int c = 0;
+            for (int g = T.lp_ptr[l2]; g < T.lp_ptr[l2 + 1]; ++g)
+              for (int q = T.pn_ptr[g]; q < T.pn_ptr[g + 1]; ++q) {
+                const long long* x = &hs[5 * q];
+                w += x[4] - x[0];
+                a += x[1] - x[4];
+                dg += x[2] - x[1];
+                tr += x[3] - x[2];
+                ++c;
+              }
+            if (c)
+              std::fprintf(stderr, "[ncl huge trace] level %d: %d panels, per task us: wait %.2f stage+strip %.2f "
+                           "diag %.2f trsm-tail %.2f\n", l2, T.lp_ptr[l2 + 1] - T.lp_ptr[l2], w / c / 1965.0,
+                           a / c / 1965.0, dg / c / 1965.0, tr / c / 1965.0);
+          }
+        }
+        continue;
+      }
       if (fused_panel_) {
         // the strip update of panel g-1 runs inside panel g's kernel; panel g
         // waits for the rest update of g-2, the rest update of g (stream 2,
@@ -659,6 +693,21 @@ class LdlSystem {
       lvl_cluster_[l] = c;
     }
     build_dag_segments(sms);
+    // opt-in (NCL_HUGE_LEVEL=1): measured slower than the per-panel launches
+    // on the 78k-bus mesh (3.28 vs 2.80 ms per factorization: a flag hop per
+    // panel instead of the programmatic launch, staging unchanged)
+    if (std::getenv("NCL_HUGE_LEVEL") && T.lp_ptr.back() > 0) {
+      huge_ctas_ = huge_level_ctas();
+      if (huge_ctas_ < 2) huge_ctas_ = 0;
+      pn_ptr_.upload(T.pn_ptr);
+      tl_ptr_.upload(T.tl_ptr);
+      dg_ptr_.upload(T.dg_ptr);
+      hcnt_.alloc(2 * static_cast<size_t>(T.lp_ptr.back()));
+      if (std::getenv("NCL_HUGE_TRACE")) {
+        htrace_.alloc(5 * T.pn_tasks.size());
+        htrace_.zero(st_);
+      }
+    }
     build_tree(sms);
     if (std::getenv("NCL_LEVEL_STATS")) {  // diagnostic: split fronts
       int ns = 0, nu = 0;
@@ -1086,6 +1135,10 @@ class LdlSystem {
   bool use_graph_ = std::getenv("NCL_NO_GRAPH") == nullptr;
   // huge levels: strip update folded into the panel kernel (NCL_NO_FUSED_PANEL=1: separate launch)
   bool fused_panel_ = std::getenv("NCL_NO_FUSED_PANEL") == nullptr;
+  // huge levels as one persistent launch (opt-in NCL_HUGE_LEVEL=1)
+  int huge_ctas_ = 0;
+  DBuf<int> hcnt_, pn_ptr_, tl_ptr_, dg_ptr_;
+  DBuf<long long> htrace_;
   int nfact_ = 0;
   cudaGraphExec_t graph_exec_ = nullptr;
   const double* g_kval_ = nullptr;

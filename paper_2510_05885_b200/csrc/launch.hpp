@@ -57,6 +57,26 @@ void launch_wide_panel(const SnDev& sd, const FactorDev& fd, const int4* tasks, 
 void launch_wide_update(const SnDev& sd, const FactorDev& fd, const int4* tiles, int count,
                         const int* fronts, int nd, int panel, cudaStream_t st, bool pdl,
                         const double* scr = nullptr);
+// a huge level's panels and trailing updates as one persistent launch
+// (wide_kernels.cu k_huge_level): global panels [g0, g1) of the schedule
+struct HugeDev {
+  const int4* pn;       // panel tasks, pn_ptr per global panel
+  const int* pn_ptr;
+  const int4* tiles;    // rest-update tiles, tl_ptr per global panel
+  const int* tl_ptr;
+  const int* dg;        // fronts of each panel, dg_ptr per global panel (L11 write-back)
+  const int* dg_ptr;
+  int g0, g1;
+  int* pc;              // per global panel: panel tasks done
+  int* rc;              // per global panel: rest items done (tiles + 1)
+  double* scr;          // L11 scratch, 2 x max_dg slots (panel parity)
+  int max_dg;
+  int npc;              // CTAs [0, npc) run panel tasks, the rest tiles
+  int ctas;             // grid (<= resident CTAs)
+  long long* trace;     // diagnostic: 5 SM-clock stamps per panel task
+};
+int huge_level_ctas();
+void launch_huge_level(const SnDev& sd, const FactorDev& fd, const HugeDev& h, double eps, cudaStream_t st);
 // k_wide_panel with the previous panel's strip update folded in (scr: this
 // panel's L11 scratch slots)
 void launch_wide_panel_f(const SnDev& sd, const FactorDev& fd, const int4* tasks, int count, int panel,

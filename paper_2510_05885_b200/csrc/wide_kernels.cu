@@ -659,16 +659,27 @@ __device__ __forceinline__ void strip_mma(double* Cs, int SC, int shC, const dou
 // columns is in (the host orders this launch after the rest update of panel
 // g-2).  The scaled L11 goes to the scratch slot `scr` (the rest-update
 // launch of this panel writes it into the front).
-__global__ void __launch_bounds__(kHugeRows)
-k_wide_panel_f(SnDev sd, FactorDev fd, const int4* __restrict__ tasks, int panel, double eps,
-               double* scr_base) {
-  __shared__ PanelSmem sm;
-  __shared__ __align__(16) double D[kWidePanel * kSL];
-  extern __shared__ __align__(16) double dyn_smem[];
-  double* TR = dyn_smem;                         // kWidePanel x kSLT
-  double* A = TR + kWidePanel * kSLT;            // 4 blocks of kWidePanel x kSL
-  double* dv = A + 4 * kWidePanel * kSL;         // previous panel's pivots
-  const int4 task = tasks[blockIdx.x];
+// one panel task (front s, row block rb below the panel; di: the front's
+// scratch slot): the body of k_wide_panel_f, shared with k_huge_level.  The
+// caller has completed the previous panel and every earlier update of this
+// panel's columns; returns after a CTA barrier.
+struct PanelTaskSmem {  // cp.async destinations 16-byte aligned
+  PanelSmem sm;
+  alignas(16) double D[kWidePanel * kSL];
+  alignas(16) double TR[kWidePanel * kSLT];
+  alignas(16) double A[4 * kWidePanel * kSL];
+  double dv[kWidePanel];
+};
+static_assert(offsetof(PanelTaskSmem, D) % 16 == 0 && offsetof(PanelTaskSmem, TR) % 16 == 0 &&
+                  offsetof(PanelTaskSmem, A) % 16 == 0, "PanelTaskSmem alignment");
+__device__ __forceinline__ void panel_task(const SnDev& sd, const FactorDev& fd, int4 task, int panel,
+                                           double eps, double* scr_base, PanelTaskSmem& P,
+                                           long long* stamp = nullptr) {
+  PanelSmem& sm = P.sm;
+  double* D = P.D;
+  double* TR = P.TR;
+  double* A = P.A;
+  double* dv = P.dv;
   const int s = task.x, rb = task.y;
   const int c0 = sd.first[s], k = sd.first[s + 1] - c0, f = sd.f[s];
   const size_t ld = wide_ld(f);
@@ -678,20 +689,18 @@ k_wide_panel_f(SnDev sd, FactorDev fd, const int4* __restrict__ tasks, int panel
   const int nrow = max(0, hi - lo);
   const int t = threadIdx.x;
   if (t == 0) sm.prog = 0;
-  pdl_launch_dependents();
-  pdl_wait();  // the previous panel (programmatic launch)
   if (panel > 0) {
     const int q0 = p0 - kWidePanel;  // panel g-1: 32 columns (not a front's last panel)
-    stage_block<kNR2>(A, kSL, F, ld, p0, q0, kWidePanel, t, kHugeRows);
-    for (int j = 0; 32 * j < nrow; ++j)
-      stage_block<kNR2>(A + (j + 1) * kWidePanel * kSL, kSL, F, ld, lo + 32 * j, q0, kWidePanel, t,
-                        kHugeRows);
     // the strip is the whole 32-column block: on a front's last (partial)
     // panel its columns [p1, p0+32) are trailing entries, updated here and
     // written back below (rows >= p1 are this CTA's rows: each entry once)
     const int ncs = min(kWidePanel, f - p0);
     stage_block<kNR2>(D, kSL, F, ld, p0, p0, nb, t, kHugeRows);
     if (nrow > 0) stage_block<(kTrsRows + 2) / 2>(TR, kSLT, F, ld, lo, p0, ncs, t, kHugeRows);
+    stage_block<kNR2>(A, kSL, F, ld, p0, q0, kWidePanel, t, kHugeRows);
+    for (int j = 0; 32 * j < nrow; ++j)
+      stage_block<kNR2>(A + (j + 1) * kWidePanel * kSL, kSL, F, ld, lo + 32 * j, q0, kWidePanel, t,
+                        kHugeRows);
     if (t < kWidePanel) dv[t] = __ldcg(fd.d + c0 + q0 + t);
     cp_wait_all();
     __syncthreads();
@@ -705,9 +714,11 @@ k_wide_panel_f(SnDev sd, FactorDev fd, const int4* __restrict__ tasks, int panel
         if (lo + i >= p0 + c) F[(lo + i) + static_cast<size_t>(p0 + c) * ld] = TR[c * kSLT + i + sh];
   }
   __syncthreads();
+  if (stamp && t == 0) stamp[1] = clock64();
   if (t < 32) {
     diag_block(F, ld, p0, nb, eps, sm, D, rb == 0 ? fd.d + c0 + p0 : nullptr,
                rb == 0 ? fd.stats : nullptr, &sm.prog, panel > 0);
+    if (stamp && t == 0) stamp[2] = clock64();
     if (rb == 0) {
       double* scr = scr_base + static_cast<size_t>(task.z) * (kWidePanel * kWidePanel);
       for (int i = t; i < kWidePanel * kWidePanel; i += 32) scr[i] = sm.Lsh[i / kWidePanel][i % kWidePanel];
@@ -715,6 +726,115 @@ k_wide_panel_f(SnDev sd, FactorDev fd, const int4* __restrict__ tasks, int panel
   } else {
     trsm_rows<kTrsRows>(F, ld, p0, nb, lo, max(lo, hi), &sm.Us[0][0], sm.rinv, fd.stats, t - 32, TR,
                         &sm.prog, 1, panel > 0);
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(kHugeRows)
+k_wide_panel_f(SnDev sd, FactorDev fd, const int4* __restrict__ tasks, int panel, double eps,
+               double* scr_base) {
+  extern __shared__ __align__(16) double dyn_smem[];
+  PanelTaskSmem& P = *reinterpret_cast<PanelTaskSmem*>(dyn_smem);
+  const int4 task = tasks[blockIdx.x];
+  pdl_launch_dependents();
+  pdl_wait();  // the previous panel (programmatic launch)
+  panel_task(sd, fd, task, panel, eps, scr_base, P);
+}
+
+// ---------------------------------------------------------------------------
+// A whole huge level as ONE persistent launch (the per-panel launches of
+// k_wide_panel_f / k_wide_update cost a launch gap each and start on SMs
+// whose instruction caches are cold for an 86 KB kernel).  CTAs [0, npc)
+// run the panel tasks of every panel in order (task j of panel g on CTA
+// j % npc); the others run the trailing-update tiles of panel g plus one
+// L11 write-back item.  Dependencies are the stream schedule's, through
+// per-panel completion counters (zeroed before the launch): panel g waits for
+// panel g-1 and the rest update of g-2; the rest update of g for panel g and
+// the rest update of g-1 (every tile still sees the panels in order).  Each
+// CTA runs its items in that order and waits only on earlier items, and the
+// grid is resident (HugeDev.ctas <= resident CTAs): no deadlock.
+__device__ __forceinline__ void huge_wait(const int* p, int v) {
+  if (ld_relaxed(p) < v) {
+    unsigned ns = 32;
+    while (ld_relaxed(p) < v) {
+      __nanosleep(ns);
+      if (ns < 256) ns <<= 1;
+    }
+  }
+  asm volatile("fence.acq_rel.gpu;" ::: "memory");
+}
+__device__ __forceinline__ void huge_done(int* p) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(p) : "memory");
+  }
+}
+
+__global__ void __launch_bounds__(kHugeRows)
+k_huge_level(SnDev sd, FactorDev fd, HugeDev h, double eps) {
+  extern __shared__ __align__(16) double dyn_smem[];
+  const int t = threadIdx.x;
+  pdl_launch_dependents();
+  pdl_wait();  // the level's assembly
+  const int ng = h.g1 - h.g0;
+  auto np = [&](int g) { return h.pn_ptr[g + 1] - h.pn_ptr[g]; };
+  auto nr = [&](int g) { return h.tl_ptr[g + 1] - h.tl_ptr[g] + 1; };  // tiles + the L11 item
+  if (static_cast<int>(blockIdx.x) < h.npc) {
+    PanelTaskSmem& P = *reinterpret_cast<PanelTaskSmem*>(dyn_smem);
+    for (int gi = 0; gi < ng; ++gi) {
+      const int g = h.g0 + gi;
+      double* scr = h.scr + static_cast<size_t>(gi & 1) * h.max_dg * (kWidePanel * kWidePanel);
+      for (int j = blockIdx.x; j < np(g); j += h.npc) {
+        if (t == 0) {
+          if (h.trace) h.trace[5 * static_cast<size_t>(h.pn_ptr[g] + j)] = clock64();
+          if (gi >= 1) huge_wait(h.pc + g - 1, np(g - 1));
+          if (gi >= 2) huge_wait(h.rc + g - 2, nr(g - 2));
+        }
+        __syncthreads();
+        long long* stamp = h.trace ? h.trace + 5 * static_cast<size_t>(h.pn_ptr[g] + j) : nullptr;
+        if (stamp && t == 0) stamp[4] = clock64();
+        panel_task(sd, fd, h.pn[h.pn_ptr[g] + j], gi, eps, scr, P, stamp);
+        if (stamp && t == 0) stamp[3] = clock64();
+        huge_done(h.pc + g);
+      }
+    }
+    return;
+  }
+  GroupSmem& G = *reinterpret_cast<GroupSmem*>(dyn_smem);
+  const int nrc = gridDim.x - h.npc, r = blockIdx.x - h.npc;
+  for (int gi = 0; gi < ng; ++gi) {
+    const int g = h.g0 + gi;
+    const double* scr = h.scr + static_cast<size_t>(gi & 1) * h.max_dg * (kWidePanel * kWidePanel);
+    const int ntl = nr(g) - 1;
+    for (int j = r; j < ntl + 1; j += nrc) {
+      if (t == 0) {
+        huge_wait(h.pc + g, np(g));
+        if (gi >= 1) huge_wait(h.rc + g - 1, nr(g - 1));
+      }
+      __syncthreads();
+      if (j < ntl) {
+        const int4 tl = h.tiles[h.tl_ptr[g] + j];
+        const int s = tl.x;
+        const int c0 = sd.first[s], k = sd.first[s + 1] - c0, f = sd.f[s];
+        const int p0 = tl.w * kWidePanel, p1 = min(p0 + kWidePanel, k);
+        group_tile(fd.lval + sd.l_off[s], wide_ld(f), f, fd.d + c0 + p0, p0, p1 - p0, tl.y, tl.z, G, t, 1);
+      } else {  // the panel's L11 blocks from the scratch slots
+        for (int di = 0; di < h.dg_ptr[g + 1] - h.dg_ptr[g]; ++di) {
+          const int s = h.dg[h.dg_ptr[g] + di];
+          const int c0 = sd.first[s], k = sd.first[s + 1] - c0, f = sd.f[s];
+          const size_t ld = wide_ld(f);
+          const int p0 = gi * kWidePanel, nb = min(p0 + kWidePanel, k) - p0;
+          const double* sc = scr + static_cast<size_t>(di) * (kWidePanel * kWidePanel);
+          double* F = fd.lval + sd.l_off[s];
+          for (int idx = t; idx < kWidePanel * kWidePanel; idx += kHugeRows) {
+            const int i = idx / kWidePanel, p = idx % kWidePanel;
+            if (i > p && i < nb) F[(p0 + i) + (p0 + p) * ld] = sc[idx];
+          }
+        }
+      }
+      huge_done(h.rc + g);
+    }
   }
 }
 
@@ -740,13 +860,14 @@ k_wide_update(SnDev sd, FactorDev fd, const int4* __restrict__ tiles, int count,
       }
     }
   }
-  if (static_cast<int>(blockIdx.x) >= count) return;
-  const int4 t = tiles[blockIdx.x];
-  const int s = t.x;
-  const int c0 = sd.first[s], k = sd.first[s + 1] - c0, f = sd.f[s];
-  const int p0 = t.w * kWidePanel, p1 = min(p0 + kWidePanel, k);
-  group_tile(fd.lval + sd.l_off[s], wide_ld(f), f, fd.d + c0 + p0, p0, p1 - p0, t.y, t.z, G,
-             threadIdx.x, 1);
+  if (static_cast<int>(blockIdx.x) < count) {
+    const int4 t = tiles[blockIdx.x];
+    const int s = t.x;
+    const int c0 = sd.first[s], k = sd.first[s + 1] - c0, f = sd.f[s];
+    const int p0 = t.w * kWidePanel, p1 = min(p0 + kWidePanel, k);
+    group_tile(fd.lval + sd.l_off[s], wide_ld(f), f, fd.d + c0 + p0, p0, p1 - p0, t.y, t.z, G,
+               threadIdx.x, 1);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -850,10 +971,31 @@ void launch_wide_update(const SnDev& sd, const FactorDev& fd, const int4* tiles,
 void launch_wide_panel_f(const SnDev& sd, const FactorDev& fd, const int4* tasks, int count, int panel,
                          double eps, double* scr, cudaStream_t st) {
   static PerDeviceOnce init;
-  constexpr int bytes = static_cast<int>(sizeof(double)) *
-                        (kWidePanel * kSLT + 4 * kWidePanel * kSL + kWidePanel);
+  constexpr int bytes = static_cast<int>(sizeof(PanelTaskSmem));
   init([] { cudaFuncSetAttribute(k_wide_panel_f, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes); });
   if (count) launch_pdl(k_wide_panel_f, count, kHugeRows, bytes, st, true, sd, fd, tasks, panel, eps, scr);
+}
+
+static constexpr int huge_smem() {
+  return static_cast<int>(sizeof(PanelTaskSmem) > sizeof(GroupSmem) ? sizeof(PanelTaskSmem) : sizeof(GroupSmem));
+}
+
+int huge_level_ctas() {  // resident CTAs of k_huge_level on this device
+  static PerDeviceOnce init;
+  init([] { cudaFuncSetAttribute(k_huge_level, cudaFuncAttributeMaxDynamicSharedMemorySize, huge_smem()); });
+  int per = 0, dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_huge_level, kHugeRows, huge_smem()) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return per * sms;
+}
+
+void launch_huge_level(const SnDev& sd, const FactorDev& fd, const HugeDev& h, double eps, cudaStream_t st) {
+  huge_level_ctas();  // the shared-memory opt-in on this device
+  launch_pdl(k_huge_level, h.ctas, kHugeRows, static_cast<size_t>(huge_smem()), st, true, sd, fd, h, eps);
 }
 
 // ---------------------------------------------------------------------------
