@@ -5,6 +5,7 @@ dram__bytes_write.sum]).
     python tools/launches.py gpurun_out/launches.csv <solves in the capture> [--json out.json]
 """
 import collections
+import re
 import csv
 import json
 import sys
@@ -22,7 +23,7 @@ def load(path):
             v = float(r[vi].replace(',', ''))
         except (ValueError, IndexError):
             continue
-        nm = r[ki].split('(')[0].replace('nclb::', '').replace('void ', '').strip()
+        nm = re.sub(r'^(void )?(nclb::)?(<unnamed>::|\(anonymous namespace\)::)?', '', r[ki]).split('(')[0].strip()
         d = launches.setdefault(r[idi], {"name": nm, "grid": r[gi]})
         d[r[mi]] = v
     return list(launches.values())
