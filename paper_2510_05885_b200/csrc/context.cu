@@ -164,6 +164,12 @@ class LdlSystem {
         launch_cc_partial(sd_, fd, s, T.f[s], T.split_ng[s], st_);
         launches_ += 1;
       }
+      if (mid_level(l)) {  // a 4-warp CTA per front, the front in shared memory
+        launch_mid_front(sd_, fd, kval, lvl_nodes_.p + T.lvl_ptr[l], T.lvl_ptr[l + 1] - T.lvl_ptr[l],
+                         lvl_fmax_[l], eps, st_);
+        launches_ += 1;
+        continue;
+      }
       if (lvl_fmax_[l] <= small_factor_limit()) {  // a warp per front
         launch_small_front(sd_, fd, kval, lvl_nodes_.p + T.lvl_ptr[l], T.lvl_ptr[l + 1] - T.lvl_ptr[l],
                            lvl_fmax_[l], eps, st_);
@@ -298,6 +304,17 @@ class LdlSystem {
   }
 
   int nlevels() const { return static_cast<int>(sn_.lvl_ptr.size()) - 1; }
+  // single-panel levels of fronts that fit in one CTA's shared memory, without
+  // Schur / split fronts (NCL_NO_MID=1: the small-front / cluster kernels)
+  bool use_mid_ = std::getenv("NCL_NO_MID") == nullptr;
+  bool mid_level(int l) const {
+    if (!use_mid_ || lvl_fmax_[l] > mid_front_limit() || lvl_kmax_[l] > kWidePanel) return false;
+    for (int q = sn_.lvl_ptr[l]; q < sn_.lvl_ptr[l + 1]; ++q) {
+      const int s = sn_.lvl_nodes[q];
+      if (s == sn_.schur || sn_.split_ng[s]) return false;
+    }
+    return true;
+  }
   // a warp per front for levels of many small fronts; a level of a few
   // fronts (the dense Schur system: one 118-row front) takes the cluster
   // solve, which spreads each front over up to 16 CTAs

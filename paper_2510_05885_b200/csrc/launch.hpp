@@ -88,6 +88,11 @@ void launch_bwd_warp(const SnDev& sd, const double* lval, const double* d,
                      const double* w, double* x, int* flags, int epoch,
                      const int8_t* wide, int* counter, int npaths, int grid, bool pipe,
                      cudaStream_t st);
+// wide_kernels.cu: levels of single-panel fronts (k <= 32) of at most
+// mid_front_limit() rows, one 4-warp CTA per front kept in shared memory
+int mid_front_limit();
+void launch_mid_front(const SnDev& sd, const FactorDev& fd, const double* kval, const int* nodes, int count,
+                      int fmax, double eps, cudaStream_t st);
 // small_front.cu: levels whose fronts all have <= small_*_limit() rows, one
 // warp per front (factorization; forward and backward solve)
 int small_factor_limit();

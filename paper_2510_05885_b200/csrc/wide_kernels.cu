@@ -871,6 +871,190 @@ k_wide_update(SnDev sd, FactorDev fd, const int4* __restrict__ tiles, int count,
 }
 
 // ---------------------------------------------------------------------------
+// Mid fronts: levels whose fronts all have at most kMidF rows and a single
+// panel (k <= 32) -- on the 78k-bus mesh the 3,100 fronts of levels 0-4.
+// k_wide_front gives such a front a 512-thread cluster CTA (one per SM) that
+// round-trips every phase through L2 (assembled columns, the staged diagonal
+// block and rows, three staged blocks per trailing tile) with a barrier
+// between phases.  Here one 4-warp CTA keeps the whole front in shared memory
+// (packed lower triangle: element (r, J) at S[cb[J] + r]) from the assembly
+// to the single write-back: zero + A entries + the children one by one (the
+// child's row map in shared memory, 16 of its entries per thread in flight),
+// the diagonal block (diag_block, warp 0) with the rows below in lock-step
+// (warps 1-3, trsm_steps), then the trailing update tile by tile on DMMA with
+// the fragment layout and masking of tile_mma_store -- every entry gets
+// bitwise the k_wide_front arithmetic.
+constexpr int kMidF = 216;
+
+struct MidSmem {
+  PanelSmem sm;
+  alignas(16) double D[kWidePanel * kSL];
+  double dv[kWidePanel];
+  int rel[kMidF];  // the current child's row map into the front
+  int cb[kMidF];   // column bases of the packed front
+};
+
+// the front's tile (rows r0.., columns q0..; nr x nc; lower part only when
+// `dg`) -= L(rows, 0:nb) diag(d) L(cols, 0:nb)^T, 4 warps, warp gw rows gw*8..+8
+__device__ __forceinline__ void mid_tile(double* S, const int* cb, int r0, int q0, const double* d,
+                                         int nb, int nr, int nc, bool dg, int gt) {
+  const int lane = gt & 31, gw = gt >> 5, g = lane >> 2, tq = lane & 3;
+  const int rr = gw * 8 + g;
+  double acc[4][2];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) acc[j][0] = acc[j][1] = 0.0;
+#pragma unroll
+  for (int kk = 0; kk < kWidePanel / 4; ++kk) {
+    const int q = kk * 4 + tq;
+    const bool qv = q < nb;
+    const int bq = qv ? cb[q] : 0;
+    const double a = (qv && rr < nr) ? S[bq + r0 + rr] : 0.0;
+    const double dq = qv ? d[q] : 0.0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int cc = j * 8 + g;
+      const double b = (qv && cc < nc) ? S[bq + q0 + cc] * dq : 0.0;
+      dmma_m8n8k4(acc[j][0], acc[j][1], a, b);
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int c = j * 8 + tq * 2 + e;
+      if (rr < nr && c < nc && (!dg || rr >= c)) {
+        double* x = S + cb[q0 + c] + r0 + rr;
+        *x = *x - acc[j][e];
+      }
+    }
+}
+
+// trsm_steps for one row r of the packed front: L(r, p) = x_p / d_p stored at
+// S[cb[p] + r]
+template <int W>
+__device__ __forceinline__ void mid_trsm_steps(int pb, int pe, double (&x)[kWidePanel], double* S,
+                                               const int* cb, int r, const double* us, const double* rinv,
+                                               const int* prog, bool& bad) {
+#pragma unroll 1
+  for (int p = pb; p < pe; ++p) {
+    while (ld_acquire_smem(prog) <= p) __nanosleep(64);
+    const double l = x[0] * rinv[p];
+    S[cb[p] + r] = l;
+    bad |= !isfinite(l);
+    const double2* up = reinterpret_cast<const double2*>(us + p * kWidePanel);
+#pragma unroll
+    for (int j = 0; j < W; j += 2) {
+      const double2 v = up[j >> 1];
+      x[j] = x[j + 1] - l * v.x;
+      x[j + 1] = (j + 2 < W ? x[j + 2] : 0.0) - l * v.y;
+    }
+  }
+}
+
+// NT threads: 128 (fronts up to 128 rows, several CTAs per SM) or 256 (two
+// 4-warp tile groups, wider assembly and row rounds for the bigger fronts)
+template <int NT>
+__global__ void __launch_bounds__(NT)
+k_mid_front(SnDev sd, FactorDev fd, const double* __restrict__ kval, const int* __restrict__ nodes,
+            double eps) {
+  extern __shared__ __align__(16) double dyn_smem[];
+  MidSmem& M = *reinterpret_cast<MidSmem*>(dyn_smem);
+  double* S = dyn_smem + (sizeof(MidSmem) + 7) / 8;  // the front, packed lower triangle
+  const int* cb = M.cb;
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+  const int s = nodes[blockIdx.x];
+  const int c0 = sd.first[s], k = sd.first[s + 1] - c0, f = sd.f[s];
+  const size_t ld = wide_ld(f);
+  double* F = fd.lval + sd.l_off[s];
+  pdl_launch_dependents();
+  // column J: rows J..f-1 after the columns before it
+  for (int J = t; J < f; J += NT) M.cb[J] = J * f - (J * (J - 1)) / 2 - J;
+  pdl_wait();  // the children (previous level)
+  // assembly: zero, the A entries, then the children in child order (per
+  // position the order of the column pass of assemble_col)
+  const int ntri = f * (f + 1) / 2;
+  for (int i = t; i < ntri; i += NT) S[i] = 0.0;
+  if (t == 0) M.sm.prog = 0;
+  __syncthreads();
+  for (int q = sd.asm_ptr[s] + t; q < sd.asm_ptr[s + 1]; q += NT) {
+    const int pos = sd.asm_pos[q];
+    S[cb[pos >> 16] + (pos & 0xffff)] += __ldg(kval + sd.asm_slot[q]);
+  }
+  __syncthreads();
+  // a child at a time: its row map into shared memory, then its entries
+  // (i, j), i >= j, in batches of 16 per thread with every load of a batch in
+  // flight (entries of one child land on distinct positions)
+  for (int cc = sd.ch_ptr[s]; cc < sd.ch_ptr[s + 1]; ++cc) {
+    const int c = sd.ch[cc];
+    const int fu = f_minus_k(sd, c);
+    const int uld = sd.u_ld[c];
+    const double* U = (sd.wide[c] ? fd.lval : fd.upd) + sd.u_off[c];
+    const int* rel = sd.rel + sd.rel_ptr[c];
+    for (int i = t; i < fu; i += NT) M.rel[i] = __ldg(rel + i);
+    __syncthreads();
+    const int n2 = fu * fu;
+    for (int e0 = 0; e0 < n2; e0 += NT * 16) {
+      double v[16];
+      int pos[16];
+#pragma unroll
+      for (int b = 0; b < 16; ++b) {
+        const int e = e0 + b * NT + t;
+        const int j = e / fu, i = e - j * fu;
+        const bool ok = e < n2 && i >= j;
+        pos[b] = ok ? cb[M.rel[j]] + M.rel[i] : -1;
+        v[b] = ok ? __ldcg(U + i + static_cast<size_t>(j) * uld) : 0.0;
+      }
+#pragma unroll
+      for (int b = 0; b < 16; ++b)
+        if (pos[b] >= 0) S[pos[b]] += v[b];
+    }
+    __syncthreads();
+  }
+  // the panel: diagonal block on warp 0 (staged copy), the rows below in
+  // lock-step on warps 1-3 (rounds of 96 rows; the first in lock-step)
+  for (int i = t; i < kWidePanel * kWidePanel; i += NT) {
+    const int q = i >> 5, r = i & 31;
+    M.D[q * kSL + r] = (q < k && r < k && r >= q) ? S[cb[q] + r] : 0.0;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    diag_block(nullptr, 0, 0, k, eps, M.sm, M.D, fd.d + c0, fd.stats, &M.sm.prog, true);
+    for (int i = lane; i < kWidePanel * kWidePanel; i += 32) {
+      const int r = i >> 5, q = i & 31;
+      if (r > q && r < k) S[cb[q] + r] = M.sm.Lsh[r][q];
+    }
+  } else {
+    bool bad = false;
+    for (int r = k + t - 32; r < f; r += NT - 32) {
+      double x[kWidePanel];
+#pragma unroll
+      for (int q = 0; q < kWidePanel; ++q) x[q] = q < k ? S[cb[q] + r] : 0.0;
+      const double* us = &M.sm.Us[0][0];
+      mid_trsm_steps<32>(0, min(k, 8), x, S, cb, r, us, M.sm.rinv, &M.sm.prog, bad);
+      mid_trsm_steps<24>(8, min(k, 16), x, S, cb, r, us, M.sm.rinv, &M.sm.prog, bad);
+      mid_trsm_steps<16>(16, min(k, 24), x, S, cb, r, us, M.sm.rinv, &M.sm.prog, bad);
+      mid_trsm_steps<8>(24, k, x, S, cb, r, us, M.sm.rinv, &M.sm.prog, bad);
+    }
+    if (bad) atomicOr(fd.stats + 3, 1);
+  }
+  __syncthreads();
+  if (t < kWidePanel) M.dv[t] = t < k ? __ldcg(fd.d + c0 + t) : 0.0;
+  __syncthreads();
+  // trailing update: tiles (ti >= tj) of rows / columns [k, f), in place; the
+  // operands (the L columns) and the tiles are disjoint
+  const int T = (f - k + kUpdTile - 1) / kUpdTile;
+  for (int tl = t >> 7; tl < T * (T + 1) / 2; tl += NT / 128) {  // a 4-warp group per tile
+    int ti, tj;
+    tri_decode(tl, ti, tj);
+    const int r0 = k + ti * kUpdTile, q0 = k + tj * kUpdTile;
+    mid_tile(S, cb, r0, q0, M.dv, k, min(kUpdTile, f - r0), min(kUpdTile, f - q0), ti == tj, t & 127);
+  }
+  __syncthreads();
+  for (int J = warp; J < f; J += NT / 32)
+    for (int r = J + lane; r < f; r += 32) F[r + J * ld] = S[cb[J] + r];
+}
+
+// ---------------------------------------------------------------------------
 thread_local const char* wide_last_error = "";
 
 static void wide_init() {
@@ -1151,6 +1335,27 @@ void launch_front_dag(const SnDev& sd, const FactorDev& fd, const double* kval, 
   dag_workers_per_sm();  // the smem opt-in on this device
   launch_pdl(k_front_dag, workers, 128, static_cast<size_t>(dag_smem_bytes()), st, true, sd, fd, kval, g,
              eps);
+}
+
+int mid_front_limit() { return kMidF; }
+
+void launch_mid_front(const SnDev& sd, const FactorDev& fd, const double* kval, const int* nodes, int count,
+                      int fmax, double eps, cudaStream_t st) {
+  static PerDeviceOnce init;
+  init([] {
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaFuncSetAttribute(k_mid_front<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
+    cudaFuncSetAttribute(k_mid_front<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
+  });
+  const int fm = fmax < 1 ? 1 : fmax;
+  const size_t smem = (sizeof(MidSmem) + 7) / 8 * 8 + sizeof(double) * (static_cast<size_t>(fm) * (fm + 1) / 2);
+  if (!count) return;
+  if (fm <= 128)
+    launch_pdl(k_mid_front<128>, count, 128, smem, st, true, sd, fd, kval, nodes, eps);
+  else
+    launch_pdl(k_mid_front<256>, count, 256, smem, st, true, sd, fd, kval, nodes, eps);
 }
 
 }  // namespace nclb

@@ -1,8 +1,9 @@
 """Parity of this round's wide-tier paths and of their switches, against the
 oracle: the tree-dataflow solves (tree_solve.cu; single-CTA and cluster
 launches), the panel kernel with the strip update folded in
-(k_wide_panel_f), the opt-in persistent huge-level kernel, and the kernels
-they replace.  Every configuration must reach the oracle's decisions and step
+(k_wide_panel_f), the opt-in persistent huge-level kernel, the mid-front
+kernel (single-panel fronts kept in shared memory), and the kernels they
+replace.  Every configuration must reach the oracle's decisions and step
 (same bars as test_gpu_kkt.py) and be bitwise reproducible from one call to
 the next (the second call replays the CUDA graphs).
 
@@ -26,8 +27,9 @@ CONFIGS = {
     "tree-single-cta": {"NCL_TREE_C": "1"},
     "separate-strip": {"NCL_NO_FUSED_PANEL": "1"},
     "persistent-huge": {"NCL_HUGE_LEVEL": "1"},
+    "no-mid-fronts": {"NCL_NO_MID": "1"},
 }
-SWITCHES = ("NCL_NO_TREE", "NCL_TREE_C", "NCL_NO_FUSED_PANEL", "NCL_HUGE_LEVEL")
+SWITCHES = ("NCL_NO_TREE", "NCL_TREE_C", "NCL_NO_FUSED_PANEL", "NCL_HUGE_LEVEL", "NCL_NO_MID")
 
 _cache = {}
 
