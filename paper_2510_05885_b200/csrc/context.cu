@@ -705,8 +705,11 @@ class LdlSystem {
         solve_cluster_[l] = c;
       }
       if (level_is_huge(fmax, nf)) continue;  // multi-kernel path
+      // one wave: k_wide_front holds one CTA per SM (its staging shared
+      // memory), so a level's clusters should fit the SMs at once
+      // (mesh levels 5-6: 276 -> 250 us against sizing for two CTAs per SM)
       int c = 16;
-      while (c > 1 && nf * c > 2 * sms) c >>= 1;
+      while (c > 1 && nf * c > sms) c >>= 1;
       lvl_cluster_[l] = c;
     }
     build_dag_segments(sms);

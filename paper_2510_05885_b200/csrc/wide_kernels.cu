@@ -275,10 +275,8 @@ __device__ __forceinline__ void diag_steps(int pb, int pe, int nb, double eps, d
   int p = pb;
 #pragma unroll 1
   for (; p + 4 <= pe; p += 4) {
-    diag_pivot<W>(p, nb, eps, a, dnext, myd, pf, bad, lane, sm);
-    diag_pivot<W>(p + 1, nb, eps, a, dnext, myd, pf, bad, lane, sm);
-    diag_pivot<W>(p + 2, nb, eps, a, dnext, myd, pf, bad, lane, sm);
-    diag_pivot<W>(p + 3, nb, eps, a, dnext, myd, pf, bad, lane, sm);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) diag_pivot<W>(p + u, nb, eps, a, dnext, myd, pf, bad, lane, sm);
     if (prog && lane == 0) st_release_smem(prog, p + 4);
   }
 #pragma unroll 1
@@ -314,10 +312,11 @@ __device__ __noinline__ void diag_block(const double* F, size_t ld, int p0, int 
   double myd = 0.0;  // lane p keeps d_p
   int pf = 0, bad = 0;
   double dnext = __shfl_sync(kFull, a[0], 0);
-  diag_steps<32>(0, min(nb, 8), nb, eps, a, dnext, myd, pf, bad, lane, sm, prog);
-  diag_steps<24>(8, min(nb, 16), nb, eps, a, dnext, myd, pf, bad, lane, sm, prog);
-  diag_steps<16>(16, min(nb, 24), nb, eps, a, dnext, myd, pf, bad, lane, sm, prog);
-  diag_steps<8>(24, nb, nb, eps, a, dnext, myd, pf, bad, lane, sm, prog);
+  // two rotation widths: fewer code bodies (instruction fetch) than four
+  // narrowing ones outweigh the extra zero updates (tools/ubench_diag.cu:
+  // ~16 % fewer cycles per block)
+  diag_steps<32>(0, min(nb, 16), nb, eps, a, dnext, myd, pf, bad, lane, sm, prog);
+  diag_steps<16>(16, nb, nb, eps, a, dnext, myd, pf, bad, lane, sm, prog);
   __syncwarp();
   if (dout && lane < nb) dout[lane] = myd;
   if (stats) {
@@ -954,7 +953,7 @@ __device__ __forceinline__ void mid_trsm_steps(int pb, int pe, double (&x)[kWide
 // NT threads: 128 (fronts up to 128 rows, several CTAs per SM) or 256 (two
 // 4-warp tile groups, wider assembly and row rounds for the bigger fronts)
 template <int NT>
-__global__ void __launch_bounds__(NT)
+__global__ void __launch_bounds__(NT, NT == 128 ? 4 : 1)
 k_mid_front(SnDev sd, FactorDev fd, const double* __restrict__ kval, const int* __restrict__ nodes,
             double eps) {
   extern __shared__ __align__(16) double dyn_smem[];
