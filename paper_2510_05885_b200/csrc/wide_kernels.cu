@@ -199,19 +199,29 @@ __device__ __noinline__ void assemble_col(const SnDev& sd, const FactorDev& fd,
           mc = max(mc, cnt[t]);
         }
       }
-      for (int i = lane; i < mc; i += 32) {
-        double v[G];
-        int r[G];
+      // four 32-row chunks per batch: every load of the batch is issued
+      // before the first add (the adds go through a pointer the compiler
+      // cannot tell apart from the loads, so it would not hoist them), the
+      // adds in the (chunk, child) order of a chunk-by-chunk pass
+      constexpr int B = 4;
+      for (int i0 = lane; i0 < mc; i0 += 32 * B) {
+        double v[B][G];
+        int r[B][G];
 #pragma unroll
-        for (int t = 0; t < G; ++t) {
-          v[t] = i < cnt[t] ? __ldcg(U[t] + i) : 0.0;
-          r[t] = i < cnt[t] ? rel[t][i] : -1;
-        }
+        for (int b = 0; b < B; ++b)
 #pragma unroll
-        for (int t = 0; t < G; ++t) {
-          if (r[t] >= 0) a[r[t]] += v[t];
-          __syncwarp(__activemask());
-        }
+          for (int t = 0; t < G; ++t) {
+            const int i = i0 + 32 * b;
+            v[b][t] = i < cnt[t] ? __ldcg(U[t] + i) : 0.0;
+            r[b][t] = i < cnt[t] ? rel[t][i] : -1;
+          }
+#pragma unroll
+        for (int b = 0; b < B; ++b)
+#pragma unroll
+          for (int t = 0; t < G; ++t) {
+            if (r[b][t] >= 0) a[r[b][t]] += v[b][t];
+            __syncwarp(__activemask());
+          }
       }
       __syncwarp();
     }
