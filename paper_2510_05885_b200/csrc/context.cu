@@ -190,7 +190,7 @@ class LdlSystem {
         continue;
       }
       const int na = T.asm_task_ptr[l + 1] - T.asm_task_ptr[l];
-      launch_wide_assemble(sd_, fd, kval, asm_task_.p + T.asm_task_ptr[l], na, st_);
+      launch_wide_assemble(sd_, fd, kval, asm_task_.p + T.asm_task_ptr[l], na, lvl_fmax_[l], st_);
       launches_ += na > 0;
       // one panel of lookahead across two streams: the panel kernel of g+1
       // runs as soon as the strip update of g is in, the rest of g's update
@@ -904,7 +904,7 @@ class LdlSystem {
   // NCL_TREE_C=1 runs every tree level one CTA per front.
   struct TreePart {
     int l0 = 0, l1 = 0, C = 1, teams = 0, fmax = 0, pmax = 0;
-    DBuf<int> list, wptr, wait, par, gbase, grow, gsrc;
+    DBuf<int> list, wptr, wait, par;
     std::vector<int> lvl;  // per list position: level (trace)
     TreeDev td{};
     bool on() const { return l1 > l0; }
@@ -928,38 +928,24 @@ class LdlSystem {
     }
     const int teams = tree_teams(C, fmax, pmax);
     if (teams < 1) return false;
-    std::vector<int> wptr{0}, wait, par, gbase, grow, gsrc;
-    std::vector<std::vector<int>> bucket;
+    std::vector<int> wptr{0}, wait, par;
     for (int s : list) {
       for (int q = T.ch_ptr[s]; q < T.ch_ptr[s + 1]; ++q)
         if (pos[T.ch[q]] >= 0) wait.push_back(T.ch[q]);
       wptr.push_back(static_cast<int>(wait.size()));
       const int p = T.sparent[s];
       par.push_back(p >= 0 && pos[p] >= 0 ? p : -1);
-      // gather rows: the children's update-vector entries landing on each
-      // front row, in child order (the order k_fwd_front adds them)
-      bucket.assign(static_cast<size_t>(T.f[s]), {});
-      for (int q = T.ch_ptr[s]; q < T.ch_ptr[s + 1]; ++q) {
-        const int c = T.ch[q], fu = T.f[c] - (T.first[c + 1] - T.first[c]), rp = T.rel_ptr[c];
-        for (int i = 0; i < fu; ++i) bucket[T.rel[rp + i]].push_back(rp + i);
-      }
-      gbase.push_back(static_cast<int>(grow.size()));
-      for (int r = 0; r < T.f[s]; ++r) {
-        grow.push_back(static_cast<int>(gsrc.size()));
-        gsrc.insert(gsrc.end(), bucket[r].begin(), bucket[r].end());
-      }
-      grow.push_back(static_cast<int>(gsrc.size()));
     }
     P.list.upload(list);
     P.wptr.upload(wptr);
     P.wait.upload(wait.empty() ? std::vector<int>{0} : wait);
     P.par.upload(par);
-    P.gbase.upload(gbase);
-    P.grow.upload(grow);
-    P.gsrc.upload(gsrc.empty() ? std::vector<int>{0} : gsrc);
-    if (trmode) tr_trace_[idx].alloc(8 * list.size());
+    if (trmode) {
+      tr_trace_[idx].alloc(16 * static_cast<size_t>(std::max<int>(static_cast<int>(list.size()), teams * C)));
+      tr_trace_[idx].zero(st_);
+    }
     P.td = TreeDev{P.list.p, static_cast<int>(list.size()), P.wptr.p, P.wait.p, P.par.p,
-                   P.gbase.p, P.grow.p, P.gsrc.p, tr_flags_.p, trmode == 3 ? nullptr : tr_trace_[idx].p};
+                   tr_flags_.p, trmode == 3 ? nullptr : tr_trace_[idx].p};
     P.lvl.assign(list.size(), 0);
     for (int l = l0; l < l1; ++l)
       for (int q = T.lvl_ptr[l]; q < T.lvl_ptr[l + 1]; ++q) P.lvl[pos[T.lvl_nodes[q]]] = l;
@@ -970,8 +956,8 @@ class LdlSystem {
     P.fmax = fmax;
     P.pmax = pmax;
     if (std::getenv("NCL_LEVEL_STATS"))
-      std::fprintf(stderr, "[ncl tree] levels %d-%d: %zu fronts on %d teams of %d CTAs (fmax %d, %zu gather entries)\n",
-                   l0, l1 - 1, list.size(), P.teams, C, fmax, gsrc.size());
+      std::fprintf(stderr, "[ncl tree] levels %d-%d: %zu fronts on %d teams of %d CTAs (fmax %d)\n",
+                   l0, l1 - 1, list.size(), P.teams, C, fmax);
     return true;
   }
   void build_tree(int /*sms*/) {
@@ -1017,35 +1003,28 @@ class LdlSystem {
     tr_l0_ = l0;
     tr_l1_ = l1;
   }
-  // diagnostic (NCL_TREE_TRACE=1, NCL_NO_GRAPH=1): per level, mean wait /
-  // gather / solve per front and the longest solve, per direction
+  // diagnostic (NCL_TREE_TRACE=1): per launch and direction, the mean SM
+  // clocks (us at 1.965 GHz) per front of each phase, from each team's rank 0:
+  // wait (reset, cluster barrier, children / parent flags), gather, solve,
+  // write-out + publish
   void dump_tree_trace() {
     for (int pi = 0; pi < 2; ++pi) {
       const TreePart& P = tp_[pi];
       if (!P.on() || !tr_trace_[pi].p) continue;
-      const size_t n = P.lvl.size();
-      std::vector<unsigned long long> h(8 * n);
+      std::vector<unsigned long long> h(tr_trace_[pi].n);
       CK(cudaMemcpyAsync(h.data(), tr_trace_[pi].p, h.size() * 8, cudaMemcpyDeviceToHost, st_));
       CK(cudaStreamSynchronize(st_));
-      constexpr double us = 1.0 / 1965.0;  // SM clock stamps
+      const int grid = P.teams * P.C;
       for (int dir = 0; dir < 2; ++dir) {
-        std::fprintf(stderr, "[ncl tree trace] C=%d %s (mean us per front: wait / gather / solve, max solve):",
-                     P.C, dir ? "bwd" : "fwd");
-        for (int l = P.l0; l < P.l1; ++l) {
-          double wt = 0, ga = 0, so = 0, mx = 0;
-          int c = 0;
-          for (size_t i = 0; i < n; ++i) {
-            if (P.lvl[i] != l) continue;
-            const unsigned long long* t = &h[4 * (dir * n + i)];
-            wt += (t[1] - t[0]) * us;
-            ga += (t[2] - t[1]) * us;
-            so += (t[3] - t[2]) * us;
-            mx = std::max(mx, (t[3] - t[2]) * us);
-            ++c;
-          }
-          std::fprintf(stderr, " L%d[w%.1f g%.1f s%.1f m%.1f]", l, wt / c, ga / c, so / c, mx);
+        double sum[4] = {0, 0, 0, 0}, cnt = 0;
+        for (int b = 0; b < grid; ++b) {
+          const unsigned long long* x = &h[8 * static_cast<size_t>(dir * grid + b)];
+          for (int i = 0; i < 4; ++i) sum[i] += static_cast<double>(x[i]);
+          cnt += static_cast<double>(x[4]);
         }
-        std::fprintf(stderr, "\n");
+        const double us = 1.0 / 1965.0 / std::max(1.0, cnt);
+        std::fprintf(stderr, "[ncl tree trace] C=%d %s: %.0f fronts, per front us: wait %.2f gather %.2f solve %.2f "
+                     "out %.2f\n", P.C, dir ? "bwd" : "fwd", cnt, sum[0] * us, sum[1] * us, sum[2] * us, sum[3] * us);
       }
     }
   }

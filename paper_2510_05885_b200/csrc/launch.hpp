@@ -49,8 +49,9 @@ struct DagDev {
 int dag_workers_per_sm();
 void launch_front_dag(const SnDev& sd, const FactorDev& fd, const double* kval, const DagDev& g,
                       int workers, double eps, cudaStream_t st);
+// max_f: the level's largest front (per-warp shared accumulators)
 void launch_wide_assemble(const SnDev& sd, const FactorDev& fd, const double* kval,
-                          const int4* tasks, int count, cudaStream_t st);
+                          const int4* tasks, int count, int max_f, cudaStream_t st);
 void launch_wide_panel(const SnDev& sd, const FactorDev& fd, const int4* tasks, int count,
                        int panel, double eps, cudaStream_t st);
 // scr: the scaled L11 blocks of the nd fronts (nullptr: fd.dscr)
@@ -120,11 +121,8 @@ struct TreeDev {
   const int* wait_ptr;  // forward: per list position, its children in the list
   const int* wait;
   const int* par;       // backward: per list position, the parent if in the list, else -1
-  const int* g_base;    // per list position: offset of its f+1 gather row pointers in g_row
-  const int* g_row;
-  const int* g_src;     // update-vector offsets, child order within a row
   int* flags;           // per supernode: 1 forward done, 2 backward done
-  unsigned long long* trace;  // diagnostic (NCL_TREE_TRACE): 4 stamps per front and direction
+  unsigned long long* trace;  // diagnostic (NCL_TREE_TRACE): phase clocks per team and direction
 };
 constexpr int kTreeMaxF = 2048;
 constexpr int kTreeCluster = 8;  // CTAs per front in the cluster launch (top levels)

@@ -321,6 +321,7 @@ k_fwd_tree(SnDev sd, TreeDev td, const double* __restrict__ lval, double* w, dou
   const int team = C > 1 ? blockIdx.x / C : blockIdx.x, nteams = C > 1 ? gridDim.x / C : gridDim.x;
   const double* T0 = C > 1 ? cl.map_shared_rank(T, 0) : T;
   const int* xd0 = C > 1 ? cl.map_shared_rank(&sm.xdone, 0) : &sm.xdone;
+  unsigned long long ph[5] = {0, 0, 0, 0, 0};  // trace: SM clocks per phase, summed over the fronts
   for (int li = team; li < td.n; li += nteams) {
     FrontGeo g = front_geo(sd, lval, __ldg(td.list + li));
     int row_lo = 0, row_hi = g.f;  // the front rows this CTA gathers and writes
@@ -337,8 +338,8 @@ k_fwd_tree(SnDev sd, TreeDev td, const double* __restrict__ lval, double* w, dou
         row_hi = min(g.f, g.k + 32 * j1);
       }
     }
-    unsigned long long* tr = td.trace ? td.trace + 4 * static_cast<size_t>(li) : nullptr;
-    if (tr && tid == 0 && rank == 0) tr[0] = gtime();
+    const bool tr = td.trace && tid == 0 && rank == 0;
+    unsigned long long t0 = tr ? gtime() : 0, t1 = 0, t2 = 0, t3 = 0;
     if (warp == 0 && rank == 0)  // the chain's first L blocks do not depend on anything
       for (int b = 0; b < kStages; ++b) fwd_stage(sm.head[b], g, b, lane);
     for (int i = tid; i < kMaxRB; i += kThr) sm.cnt[i] = 0;
@@ -350,19 +351,23 @@ k_fwd_tree(SnDev sd, TreeDev td, const double* __restrict__ lval, double* w, dou
       for (int e = e0 + lane; e < e1; e += 32) gwait_ge(td.flags + __ldg(td.wait + e), 1);
     }
     __syncthreads();
-    if (tr && tid == 0 && rank == 0) tr[1] = gtime();
-    // gather: T_r = w_r (pivot rows) + the children's entries, child order
-    {
-      const int* gp = td.g_row + __ldg(td.g_base + li);
-      for (int r = row_lo + tid; r < row_hi; r += kThr) {
-        double v = r < g.k ? __ldcg(w + g.c0 + r) : 0.0;
-        const int e0 = __ldg(gp + r), e1 = __ldg(gp + r + 1);
-        for (int e = e0; e < e1; ++e) v += __ldcg(uvec + __ldg(td.g_src + e));
-        T[r] = v;
-      }
-    }
+    if (tr) t1 = gtime();
+    // gather: T_r = w_r (pivot rows) + the children's entries in child order
+    // -- child by child, every entry of a child (landing in this CTA's rows)
+    // loaded at once, a CTA barrier between children
+    for (int r = row_lo + tid; r < row_hi; r += kThr) T[r] = r < g.k ? __ldcg(w + g.c0 + r) : 0.0;
     __syncthreads();
-    if (tr && tid == 0 && rank == 0) tr[2] = gtime();
+    for (int cc = __ldg(sd.ch_ptr + g.s); cc < __ldg(sd.ch_ptr + g.s + 1); ++cc) {
+      const int c = __ldg(sd.ch + cc);
+      const int rp = __ldg(sd.rel_ptr + c), fu = __ldg(sd.rel_ptr + c + 1) - rp;
+      for (int i = tid; i < fu; i += kThr) {
+        const int dr = __ldg(sd.rel + rp + i);
+        const double u = __ldcg(uvec + rp + i);
+        if (dr >= row_lo && dr < row_hi) T[dr] += u;
+      }
+      __syncthreads();
+    }
+    if (tr) t2 = gtime();
     if (rank == 0) {
       if (warp == 0)
         fwd_chain(g, T, sm);
@@ -372,6 +377,7 @@ k_fwd_tree(SnDev sd, TreeDev td, const double* __restrict__ lval, double* w, dou
       fwd_bulk<true>(g, warp - 1, T, T0, xd0, sm.cnt);
     }
     __syncthreads();
+    if (tr) t3 = gtime();
     double* u = uvec + __ldg(sd.rel_ptr + g.s);
     for (int r = row_lo + tid; r < row_hi; r += kThr) {
       if (r < g.k)
@@ -387,9 +393,18 @@ k_fwd_tree(SnDev sd, TreeDev td, const double* __restrict__ lval, double* w, dou
     if (tid == 0 && rank == 0) {
       __threadfence();
       st_release(td.flags + g.s, 1);
-      if (tr) tr[3] = gtime();
+    }
+    if (tr) {  // per phase: wait, gather, solve, write-out + publish
+      const unsigned long long t4 = gtime();
+      ph[0] += t1 - t0;
+      ph[1] += t2 - t1;
+      ph[2] += t3 - t2;
+      ph[3] += t4 - t3;
+      ph[4] += 1;
     }
   }
+  if (td.trace && tid == 0 && rank == 0)
+    for (int i = 0; i < 5; ++i) td.trace[8 * static_cast<size_t>(blockIdx.x) + i] = ph[i];
 }
 
 // ---------------------------------------------------------------------------
@@ -611,6 +626,7 @@ k_bwd_tree(SnDev sd, TreeDev td, const double* __restrict__ lval, const double* 
     rm.pstride = pmax;
     rm.rank = rank;
   }
+  unsigned long long ph[5] = {0, 0, 0, 0, 0};  // trace: SM clocks per phase, summed over the fronts
   for (int li0 = team; li0 < td.n; li0 += nteams) {
     const int li = td.n - 1 - li0;
     FrontGeo g = front_geo(sd, lval, __ldg(td.list + li));
@@ -634,8 +650,8 @@ k_bwd_tree(SnDev sd, TreeDev td, const double* __restrict__ lval, const double* 
       g.rlo = g.P;
       g.rhi = g.NR;
     }
-    unsigned long long* tr = td.trace ? td.trace + 4 * static_cast<size_t>(td.n + li) : nullptr;
-    if (tr && tid == 0 && rank == 0) tr[0] = gtime();
+    const bool tr = td.trace && tid == 0 && rank == 0;
+    unsigned long long t0 = tr ? gtime() : 0, t1 = 0, t2 = 0, t3 = 0;
     if (warp == 0 && rank == 0)
       for (int o = 0; o < kStages; ++o) bwd_stage(sm.head[o], g, g.P - 1 - o, lane);
     for (int i = tid; i < kMaxRB; i += kThr) sm.cnt[i] = 0;
@@ -650,14 +666,14 @@ k_bwd_tree(SnDev sd, TreeDev td, const double* __restrict__ lval, const double* 
     const int par = __ldg(td.par + li);
     if (tid == 0 && par >= 0 && g.rhi > g.rlo) gwait_ge(td.flags + par, 2);
     __syncthreads();
-    if (tr && tid == 0 && rank == 0) tr[1] = gtime();
+    if (tr) t1 = gtime();
     if (g.rhi > g.rlo) {
       const int* rows = sd.rows + __ldg(sd.rows_ptr + g.s);
       const int r1 = min(g.f, rb_start(g.k, g.P, g.rhi - 1) + 32);
       for (int r = rb_start(g.k, g.P, g.rlo) + tid; r < r1; r += kThr) X[r] = __ldcg(x + __ldg(rows + r));
     }
     __syncthreads();
-    if (tr && tid == 0 && rank == 0) tr[2] = gtime();
+    if (tr) t2 = gtime();
     if (rank == 0) {
       if (warp == 0)
         bwd_chain(g, X, acc, C > 1 ? C : kBulk, pmax, C > 1 ? nrem : 0, x, sm);
@@ -666,6 +682,7 @@ k_bwd_tree(SnDev sd, TreeDev td, const double* __restrict__ lval, const double* 
     } else if (warp > 0) {
       bwd_bulk<true>(g, warp - 1, X, acc + (warp - 1) * 32 * pmax, sm, false, rm);
     }
+    if (tr) t3 = gtime();
     if (C > 1) {
       cl.sync();  // rank 0 is done with its slots; every rank's x rows are out
     } else {
@@ -674,9 +691,18 @@ k_bwd_tree(SnDev sd, TreeDev td, const double* __restrict__ lval, const double* 
     if (tid == 0 && rank == 0) {
       __threadfence();
       st_release(td.flags + g.s, 2);
-      if (tr) tr[3] = gtime();
+    }
+    if (tr) {
+      const unsigned long long t4 = gtime();
+      ph[0] += t1 - t0;
+      ph[1] += t2 - t1;
+      ph[2] += t3 - t2;
+      ph[3] += t4 - t3;
+      ph[4] += 1;
     }
   }
+  if (td.trace && tid == 0 && rank == 0)
+    for (int i = 0; i < 5; ++i) td.trace[8 * static_cast<size_t>(gridDim.x + blockIdx.x) + i] = ph[i];
 }
 
 }  // namespace

@@ -587,16 +587,22 @@ k_wide_front(SnDev sd, FactorDev fd, const double* __restrict__ kval,
 
 // ---------------------------------------------------------------------------
 // multi-kernel path for levels with huge fronts
+// a warp per front column, accumulated in the warp's shared-memory column
+// (acc_f doubles) and written to the front once: in place in global memory
+// the zero fill, the A entries and every child's adds were L2
+// read-modify-write round trips on the critical path of each huge level
 __global__ void __launch_bounds__(256)
 k_wide_assemble(SnDev sd, FactorDev fd, const double* __restrict__ kval,
-                const int4* __restrict__ tasks) {
+                const int4* __restrict__ tasks, int acc_f) {
+  extern __shared__ __align__(16) double asm_acc[];
   const int4 t = tasks[blockIdx.x];
   const int s = t.x, J = t.y + (threadIdx.x >> 5);
   pdl_launch_dependents();
   pdl_wait();  // the previous level (programmatic launch)
   const int c0 = sd.first[s], f = sd.f[s], k = sd.first[s + 1] - c0;
   if (J < min(f, t.y + kAsmCols))
-    assemble_col(sd, fd, kval, s, c0, k, f, fd.lval + sd.l_off[s], wide_ld(f), J, nullptr);
+    assemble_col(sd, fd, kval, s, c0, k, f, fd.lval + sd.l_off[s], wide_ld(f), J,
+                 asm_acc + static_cast<size_t>(threadIdx.x >> 5) * acc_f);
 }
 
 // one CTA per (front, 128-row block below the panel): warp 0 factors the
@@ -1140,8 +1146,17 @@ static void launch_pdl(Kern kern, int grid, int block, size_t smem, cudaStream_t
 }
 
 void launch_wide_assemble(const SnDev& sd, const FactorDev& fd, const double* kval,
-                          const int4* tasks, int count, cudaStream_t st) {
-  if (count) launch_pdl(k_wide_assemble, count, 256, 0, st, true, sd, fd, kval, tasks);
+                          const int4* tasks, int count, int max_f, cudaStream_t st) {
+  static PerDeviceOnce init;
+  init([] {
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaFuncSetAttribute(k_wide_assemble, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
+  });
+  const int acc_f = max_f < 1 ? 1 : max_f;
+  const size_t smem = sizeof(double) * kAsmCols * static_cast<size_t>(acc_f);
+  if (count) launch_pdl(k_wide_assemble, count, 256, smem, st, true, sd, fd, kval, tasks, acc_f);
 }
 
 void launch_wide_panel(const SnDev& sd, const FactorDev& fd, const int4* tasks, int count,
