@@ -13,7 +13,9 @@ import subprocess
 import numpy as np
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libncl_b200.so")
+# NCL_B200_LIB: another build of the same library (same-box A/B timing of two
+# builds, tools/ab_lib.sh); unset, the in-tree build
+LIB_PATH = os.environ.get("NCL_B200_LIB") or os.path.join(PKG, "libncl_b200.so")
 CSRC = os.path.join(PKG, "csrc")
 
 _i, _d, _p, _ll = C.c_int, C.c_double, C.c_void_p, C.c_longlong

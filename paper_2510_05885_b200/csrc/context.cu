@@ -83,6 +83,7 @@ class LdlSystem {
   cudaStream_t stream() const { return st_; }
 
   ~LdlSystem() {
+    if (ptrace_.p) dump_panel_trace();
     if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
     if (solve_exec_) cudaGraphExecDestroy(solve_exec_);
     for (auto e : evs_) cudaEventDestroy(e);
@@ -231,6 +232,8 @@ class LdlSystem {
         continue;
       }
       if (fused_panel_) {
+        const bool ptr = ptrace_.p != nullptr;  // diagnostic: NCL_PANEL_TRACE
+        if (ptr && l == first_huge_) CK(cudaMemsetAsync(ptrace_.p, 0, ptrace_.n * 8, st_));
         // the strip update of panel g-1 runs inside panel g's kernel; panel g
         // waits for the rest update of g-2, the rest update of g (stream 2,
         // also writing panel g's L11) for panel g; L11 scratch by parity
@@ -240,11 +243,11 @@ class LdlSystem {
           const int nt = T.tl_ptr[g + 1] - T.tl_ptr[g];
           double* scr = dscr_.p + static_cast<size_t>((g - g0) & 1) * std::max(1, T.max_dg) * (kWidePanel * kWidePanel);
           if (g - 2 >= g0) CK(cudaStreamWaitEvent(st_, ev_rest(g - 2), 0));
-          launch_wide_panel_f(sd_, fd, pn_tasks_.p + T.pn_ptr[g], np, g - g0, eps, scr, st_);
+          launch_wide_panel_f(sd_, fd, pn_tasks_.p + T.pn_ptr[g], np, g - g0, eps, scr, st_, ptr ? g : -1);
           CK(cudaEventRecord(ev_panel(g), st_));
           CK(cudaStreamWaitEvent(st2_, ev_panel(g), 0));
           launch_wide_update(sd_, fd, tiles_.p + T.tl_ptr[g], nt, dg_nodes_.p + T.dg_ptr[g], nd, g - g0,
-                             st2_, false, scr);
+                             st2_, false, scr, ptr ? g : -1);
           CK(cudaEventRecord(ev_rest(g), st2_));
           launches_ += (np > 0) + (nt > 0 || nd > 0);
         }
@@ -284,6 +287,49 @@ class LdlSystem {
     CK(cudaGetLastError());
   }
 
+  // diagnostic (NCL_PANEL_TRACE=1, library built with make EXTRA=-DNCL_PANEL_TRACE):
+  // per huge level of the last factorization,
+  // printed when the context is destroyed, the mean per panel of: launch gap
+  // (previous panel's end -> this panel past its programmatic wait), staging,
+  // strip, diagonal block, TRSM tail; and how often the rest update of g-2
+  // ended after panel g-1 (it gated panel g)
+  DBuf<unsigned long long> ptrace_;
+  int first_huge_ = -1;
+  void dump_panel_trace() {
+    std::vector<unsigned long long> h(ptrace_.n);
+    CK(cudaStreamSynchronize(st_));
+    CK(cudaStreamSynchronize(st2_));
+    CK(cudaMemcpy(h.data(), ptrace_.p, h.size() * 8, cudaMemcpyDeviceToHost));
+    const auto& T = sn_;
+    double tot[6] = {0, 0, 0, 0, 0, 0};
+    for (int l = 0; l < nlevels(); ++l) {
+      const int g0 = T.lp_ptr[l], g1 = T.lp_ptr[l + 1];
+      if (g1 <= g0) continue;
+      double a[6] = {0, 0, 0, 0, 0, 0};
+      int late = 0;
+      for (int g = g0; g < g1; ++g) {
+        const unsigned long long* x = &h[8 * static_cast<size_t>(g)];
+        const double prev_end = g > g0 ? static_cast<double>(h[8 * static_cast<size_t>(g - 1) + 5]) : static_cast<double>(x[0]);
+        a[0] += (static_cast<double>(x[1]) - prev_end) * 1e-3;
+        a[1] += (static_cast<double>(x[2]) - static_cast<double>(x[1])) * 1e-3;
+        a[2] += (static_cast<double>(x[3]) - static_cast<double>(x[2])) * 1e-3;
+        a[3] += (static_cast<double>(x[4]) - static_cast<double>(x[3])) * 1e-3;
+        a[4] += (static_cast<double>(x[5]) - static_cast<double>(x[4])) * 1e-3;
+        a[5] += (static_cast<double>(x[5]) - static_cast<double>(x[1])) * 1e-3;
+        if (g - 2 >= g0 && h[8 * static_cast<size_t>(g - 2) + 7] > h[8 * static_cast<size_t>(g - 1) + 5]) ++late;
+      }
+      const int n = g1 - g0;
+      for (int i = 0; i < 6; ++i) tot[i] += a[i];
+      std::fprintf(stderr, "[ncl panel trace] level %d: %d panels, per panel us: gap %.2f stage %.2f strip %.2f "
+                   "diag %.2f tail %.2f (body %.2f); rest g-2 late %d; level span %.1f\n", l, n, a[0] / n, a[1] / n,
+                   a[2] / n, a[3] / n, a[4] / n, a[5] / n, late,
+                   (static_cast<double>(h[8 * static_cast<size_t>(g1 - 1) + 7]) - static_cast<double>(h[8 * static_cast<size_t>(g0)])) * 1e-3);
+    }
+    std::fprintf(stderr, "[ncl panel trace] total us: gap %.1f stage %.1f strip %.1f diag %.1f tail %.1f\n", tot[0],
+                 tot[1], tot[2], tot[3], tot[4]);
+    set_panel_trace(nullptr);
+    std::fflush(stderr);
+  }
   // diagnostic: NCL_WIDE_TRACE=<level> prints per-phase timestamps of the
   // first front of that wide level (cluster rank 0, %globaltimer) to stderr
   void dump_trace(int l) {
@@ -727,6 +773,15 @@ class LdlSystem {
         htrace_.alloc(5 * T.pn_tasks.size());
         htrace_.zero(st_);
       }
+    }
+    if (std::getenv("NCL_PANEL_TRACE") && T.lp_ptr.back() > 0) {
+      ptrace_.alloc(8 * static_cast<size_t>(T.lp_ptr.back()));
+      if (!set_panel_trace(ptrace_.p)) {
+        std::fprintf(stderr, "[ncl] NCL_PANEL_TRACE: library built without -DNCL_PANEL_TRACE\n");
+        ptrace_.alloc(0);
+      }
+      for (int l = 0; l < nlevels() && first_huge_ < 0; ++l)
+        if (T.lp_ptr[l + 1] > T.lp_ptr[l]) first_huge_ = l;
     }
     build_tree(sms);
     if (std::getenv("NCL_LEVEL_STATS")) {  // diagnostic: split fronts

@@ -57,7 +57,7 @@ void launch_wide_panel(const SnDev& sd, const FactorDev& fd, const int4* tasks, 
 // scr: the scaled L11 blocks of the nd fronts (nullptr: fd.dscr)
 void launch_wide_update(const SnDev& sd, const FactorDev& fd, const int4* tiles, int count,
                         const int* fronts, int nd, int panel, cudaStream_t st, bool pdl,
-                        const double* scr = nullptr);
+                        const double* scr = nullptr, int gtr = -1);
 // a huge level's panels and trailing updates as one persistent launch
 // (wide_kernels.cu k_huge_level): global panels [g0, g1) of the schedule
 struct HugeDev {
@@ -81,7 +81,11 @@ void launch_huge_level(const SnDev& sd, const FactorDev& fd, const HugeDev& h, d
 // k_wide_panel with the previous panel's strip update folded in (scr: this
 // panel's L11 scratch slots)
 void launch_wide_panel_f(const SnDev& sd, const FactorDev& fd, const int4* tasks, int count, int panel,
-                         double eps, double* scr, cudaStream_t st);
+                         double eps, double* scr, cudaStream_t st, int gtr = -1);
+// diagnostic: device buffer of 8 stamps per huge-path panel (nullptr: off);
+// gtr above is the panel's global index in it
+// false: the library was built without -DNCL_PANEL_TRACE
+bool set_panel_trace(unsigned long long* p);
 void launch_fwd_warp(const SnDev& sd, const double* lval, double* w, double* uvec,
                      int* flags, int epoch, int* counter, int npaths, int grid, bool pipe,
                      cudaStream_t st);

@@ -97,11 +97,29 @@ __device__ __forceinline__ unsigned long long globaltimer() {
   return t;
 }
 
+// diagnostic (NCL_PANEL_TRACE): per huge-path panel g, 8 %globaltimer stamps
+// (latest over the CTAs) -- panel entry, after the programmatic wait, staged, strip applied,
+// diagonal block done, panel end (last CTA), rest update start, rest end
+// Compiled in only with -DNCL_PANEL_TRACE (make EXTRA=-DNCL_PANEL_TRACE): even
+// never taken, the stamps cost the panel kernel 16 registers and ~0.9 us per
+// launch (ncu launch list, same box).
+#ifdef NCL_PANEL_TRACE
+__device__ unsigned long long* g_ptrace = nullptr;
+__device__ __forceinline__ void ptrace_max(int g, int i) {
+  if (g >= 0 && g_ptrace) atomicMax(g_ptrace + 8 * g + i, globaltimer());
+}
+#else
+__device__ __forceinline__ void ptrace_max(int, int) {}
+#endif
+
 __device__ __forceinline__ void cp16(void* dst, const void* src) {
   const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
 }
 __device__ __forceinline__ void cp_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait_group() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 __device__ __forceinline__ void named_bar(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
@@ -665,9 +683,44 @@ __device__ __forceinline__ void strip_mma(double* Cs, int SC, int shC, const dou
     for (int e = 0; e < 2; ++e) Cs[(j * 8 + tq * 2 + e) * SC + rr + shC] -= acc[j][e];
 }
 
+// strip_mma for a whole 32x32 tile on ONE warp (lane layout as above): 16
+// independent 8x8 accumulators, so the DMMA latency overlaps; per element
+// the same k order as strip_mma (bitwise the same result)
+__device__ __forceinline__ void strip_mma_warp(double* Cs, int SC, int shC, const double* A, int shA,
+                                               const double* Bs, int shB, const double* d, int lane) {
+  const int g = lane >> 2, tq = lane & 3;
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+#pragma unroll
+  for (int kk = 0; kk < kWidePanel / 4; ++kk) {
+    const int q = kk * 4 + tq;
+    const double dq = d[q];
+    double a[4], b[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) a[i] = A[q * kSL + i * 8 + g + shA];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) b[j] = Bs[q * kSL + j * 8 + g + shB] * dq;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) dmma_m8n8k4(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) Cs[(j * 8 + tq * 2 + e) * SC + i * 8 + g + shC] -= acc[i][j][e];
+}
+
 // k_wide_panel with the lookahead strip folded in: for panel g >= 1 the CTA
 // first applies panel g-1's update to panel g's columns -- of the diagonal
-// rows (every CTA, like the diagonal block itself) and of its own rows --
+// rows (every CTA, like the diagonal block itself; all four warps) and of its
+// own rows (each TRSM warp its 32 rows, while warp 0 factors the diagonal
+// block: factor 2.41 -> 2.34 ms on the mesh against all strips first) --
 // straight into shared memory (DMMA), and factors / solves from there.  The
 // previous panel's L is final in the front (its kernel completed: this launch
 // follows it on the stream), and every earlier panel's update of these
@@ -689,7 +742,7 @@ static_assert(offsetof(PanelTaskSmem, D) % 16 == 0 && offsetof(PanelTaskSmem, TR
                   offsetof(PanelTaskSmem, A) % 16 == 0, "PanelTaskSmem alignment");
 __device__ __forceinline__ void panel_task(const SnDev& sd, const FactorDev& fd, int4 task, int panel,
                                            double eps, double* scr_base, PanelTaskSmem& P,
-                                           long long* stamp = nullptr) {
+                                           long long* stamp = nullptr, int gtr = -1) {
   PanelSmem& sm = P.sm;
   double* D = P.D;
   double* TR = P.TR;
@@ -704,41 +757,63 @@ __device__ __forceinline__ void panel_task(const SnDev& sd, const FactorDev& fd,
   const int nrow = max(0, hi - lo);
   const int t = threadIdx.x;
   if (t == 0) sm.prog = 0;
+  // the strip is the whole 32-column block: on a front's last (partial)
+  // panel its columns [p1, p0+32) are trailing entries, updated here and
+  // written back by the TRSM warps (rows >= p1 are this CTA's rows: each
+  // entry once)
+  const int q0 = p0 - kWidePanel;  // panel g-1: 32 columns (not a front's last panel)
+  const int ncs = min(kWidePanel, f - p0);
   if (panel > 0) {
-    const int q0 = p0 - kWidePanel;  // panel g-1: 32 columns (not a front's last panel)
-    // the strip is the whole 32-column block: on a front's last (partial)
-    // panel its columns [p1, p0+32) are trailing entries, updated here and
-    // written back below (rows >= p1 are this CTA's rows: each entry once)
-    const int ncs = min(kWidePanel, f - p0);
+    // only the diagonal rows' strip is on the critical path: cp.async group 0
+    // (every thread) stages them, group 1 (the TRSM warps) this CTA's rows,
+    // whose strip the TRSM warps apply while warp 0 factors the diagonal block
     stage_block<kNR2>(D, kSL, F, ld, p0, p0, nb, t, kHugeRows);
-    if (nrow > 0) stage_block<(kTrsRows + 2) / 2>(TR, kSLT, F, ld, lo, p0, ncs, t, kHugeRows);
     stage_block<kNR2>(A, kSL, F, ld, p0, q0, kWidePanel, t, kHugeRows);
-    for (int j = 0; 32 * j < nrow; ++j)
-      stage_block<kNR2>(A + (j + 1) * kWidePanel * kSL, kSL, F, ld, lo + 32 * j, q0, kWidePanel, t,
-                        kHugeRows);
+    cp_commit();
+    if (t >= 32) {
+      if (nrow > 0) stage_block<(kTrsRows + 2) / 2>(TR, kSLT, F, ld, lo, p0, ncs, t - 32, kTrsRows);
+      for (int j = 0; 32 * j < nrow; ++j)
+        stage_block<kNR2>(A + (j + 1) * kWidePanel * kSL, kSL, F, ld, lo + 32 * j, q0, kWidePanel, t - 32,
+                          kTrsRows);
+      cp_commit();
+    }
     if (t < kWidePanel) dv[t] = __ldcg(fd.d + c0 + q0 + t);
-    cp_wait_all();
+    if (t < 32)
+      cp_wait_all();
+    else
+      cp_wait_group<1>();
     __syncthreads();
-    const int sh = lo & 1;
+    if (t == 0) ptrace_max(gtr, 2);
     strip_mma(D, kSL, 0, A, 0, A, 0, dv, t);
-    for (int j = 0; 32 * j < nrow; ++j)
-      strip_mma(TR + 32 * j, kSLT, sh, A + (j + 1) * kWidePanel * kSL, sh, A, 0, dv, t);
-    __syncthreads();
-    for (int c = nb; c < ncs; ++c)
-      for (int i = t; i < nrow; i += kHugeRows)
-        if (lo + i >= p0 + c) F[(lo + i) + static_cast<size_t>(p0 + c) * ld] = TR[c * kSLT + i + sh];
   }
   __syncthreads();
   if (stamp && t == 0) stamp[1] = clock64();
+  if (t == 0) {
+    if (panel == 0) ptrace_max(gtr, 2);
+    ptrace_max(gtr, 3);
+  }
   if (t < 32) {
     diag_block(F, ld, p0, nb, eps, sm, D, rb == 0 ? fd.d + c0 + p0 : nullptr,
                rb == 0 ? fd.stats : nullptr, &sm.prog, panel > 0);
     if (stamp && t == 0) stamp[2] = clock64();
+    if (t == 0) ptrace_max(gtr, 4);
     if (rb == 0) {
       double* scr = scr_base + static_cast<size_t>(task.z) * (kWidePanel * kWidePanel);
       for (int i = t; i < kWidePanel * kWidePanel; i += 32) scr[i] = sm.Lsh[i / kWidePanel][i % kWidePanel];
     }
   } else {
+    if (panel > 0) {
+      cp_wait_all();
+      named_bar(1, kTrsRows);
+      const int w = (t >> 5) - 1, lane = t & 31, sh = lo & 1;  // warp w: rows [32w, 32w+32)
+      if (32 * w < nrow) {
+        strip_mma_warp(TR + 32 * w, kSLT, sh, A + (w + 1) * kWidePanel * kSL, sh, A, 0, dv, lane);
+        __syncwarp();
+        for (int c = nb; c < ncs; ++c)
+          for (int i = 32 * w + lane; i < min(nrow, 32 * w + 32); i += 32)
+            if (lo + i >= p0 + c) F[(lo + i) + static_cast<size_t>(p0 + c) * ld] = TR[c * kSLT + i + sh];
+      }
+    }
     trsm_rows<kTrsRows>(F, ld, p0, nb, lo, max(lo, hi), &sm.Us[0][0], sm.rinv, fd.stats, t - 32, TR,
                         &sm.prog, 1, panel > 0);
   }
@@ -747,13 +822,16 @@ __device__ __forceinline__ void panel_task(const SnDev& sd, const FactorDev& fd,
 
 __global__ void __launch_bounds__(kHugeRows)
 k_wide_panel_f(SnDev sd, FactorDev fd, const int4* __restrict__ tasks, int panel, double eps,
-               double* scr_base) {
+               double* scr_base, int gtr) {
   extern __shared__ __align__(16) double dyn_smem[];
   PanelTaskSmem& P = *reinterpret_cast<PanelTaskSmem*>(dyn_smem);
   const int4 task = tasks[blockIdx.x];
+  if (threadIdx.x == 0) ptrace_max(gtr, 0);
   pdl_launch_dependents();
   pdl_wait();  // the previous panel (programmatic launch)
-  panel_task(sd, fd, task, panel, eps, scr_base, P);
+  if (threadIdx.x == 0) ptrace_max(gtr, 1);
+  panel_task(sd, fd, task, panel, eps, scr_base, P, nullptr, gtr);
+  if (threadIdx.x == 0) ptrace_max(gtr, 5);
 }
 
 // ---------------------------------------------------------------------------
@@ -857,10 +935,11 @@ k_huge_level(SnDev sd, FactorDev fd, HugeDev h, double eps) {
 // blocks from the scratch slots of the nd fronts
 __global__ void __launch_bounds__(128)
 k_wide_update(SnDev sd, FactorDev fd, const int4* __restrict__ tiles, int count,
-              const int* __restrict__ fronts, int nd, int panel, const double* scr_base) {
+              const int* __restrict__ fronts, int nd, int panel, const double* scr_base, int gtr) {
   __shared__ __align__(16) GroupSmem G;
   pdl_launch_dependents();
   pdl_wait();  // the panel kernel (programmatic launch on the main stream)
+  if (threadIdx.x == 0) ptrace_max(gtr, 6);
   if (blockIdx.x == 0) {
     for (int di = 0; di < nd; ++di) {
       const int s = fronts[di];
@@ -883,6 +962,12 @@ k_wide_update(SnDev sd, FactorDev fd, const int4* __restrict__ tiles, int count,
     group_tile(fd.lval + sd.l_off[s], wide_ld(f), f, fd.d + c0 + p0, p0, p1 - p0, t.y, t.z, G,
                threadIdx.x, 1);
   }
+#ifdef NCL_PANEL_TRACE
+  if (gtr >= 0) {
+    __syncthreads();
+    if (threadIdx.x == 0) ptrace_max(gtr, 7);
+  }
+#endif
 }
 
 // ---------------------------------------------------------------------------
@@ -1169,19 +1254,29 @@ void launch_wide_panel(const SnDev& sd, const FactorDev& fd, const int4* tasks, 
 
 void launch_wide_update(const SnDev& sd, const FactorDev& fd, const int4* tiles, int count,
                         const int* fronts, int nd, int panel, cudaStream_t st, bool pdl,
-                        const double* scr) {
+                        const double* scr, int gtr) {
   const int blocks = count > 0 ? count : (nd > 0 ? 1 : 0);
   if (blocks)
     launch_pdl(k_wide_update, blocks, 128, 0, st, pdl, sd, fd, tiles, count, fronts, nd, panel,
-               scr ? scr : static_cast<const double*>(fd.dscr));
+               scr ? scr : static_cast<const double*>(fd.dscr), gtr);
 }
 
 void launch_wide_panel_f(const SnDev& sd, const FactorDev& fd, const int4* tasks, int count, int panel,
-                         double eps, double* scr, cudaStream_t st) {
+                         double eps, double* scr, cudaStream_t st, int gtr) {
   static PerDeviceOnce init;
   constexpr int bytes = static_cast<int>(sizeof(PanelTaskSmem));
   init([] { cudaFuncSetAttribute(k_wide_panel_f, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes); });
-  if (count) launch_pdl(k_wide_panel_f, count, kHugeRows, bytes, st, true, sd, fd, tasks, panel, eps, scr);
+  if (count) launch_pdl(k_wide_panel_f, count, kHugeRows, bytes, st, true, sd, fd, tasks, panel, eps, scr, gtr);
+}
+
+bool set_panel_trace(unsigned long long* p) {
+#ifdef NCL_PANEL_TRACE
+  cudaMemcpyToSymbol(g_ptrace, &p, sizeof(p));
+  return true;
+#else
+  (void)p;
+  return false;
+#endif
 }
 
 static constexpr int huge_smem() {
