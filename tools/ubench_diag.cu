@@ -7,6 +7,7 @@
 //        -I paper_2510_05885_b200/csrc -DWK='"<path>/wide_kernels.cu"' tools/ubench_diag.cu -o tools/ubench_diag
 #include WK
 #include <cstdio>
+#include <string>
 #include <vector>
 
 namespace nclb {
@@ -73,7 +74,7 @@ __global__ void k_ub_lsh(const double* A, double* dout, double eps) {
 }
 }  // namespace nclb
 
-int main() {
+int main(int argc, char** argv) {
   using namespace nclb;
   std::vector<double> h(32 * 32);
   unsigned s = 12345;
@@ -104,6 +105,23 @@ int main() {
   }
   std::printf("diag_block 32 pivots, cycles per block: plain %lld  +progress flag %lld  +stats %lld  (%.1f / pivot)\n",
               c[0], c[1], c[2], c[0] / 32.0);
+  if (argc > 1) {  // dump 1/d and L of the block (bitwise comparison of two builds)
+    double* o;
+    cudaMalloc(&o, 8 * (64 + 1024));
+    std::vector<double> r(64 + 1024);
+    for (int m = 0; m < 2; ++m) {  // m = 1: a block with a tiny pivot (static perturbation)
+      if (m == 1) {
+        std::vector<double> h2 = h;
+        h2[5 * 32 + 5] = 1e-14;
+        cudaMemcpy(A, h2.data(), 8 * 1024, cudaMemcpyHostToDevice);
+      }
+      k_ub_lsh<0><<<1, 32>>>(A, o, 1e-10);
+      cudaMemcpy(r.data(), o, r.size() * 8, cudaMemcpyDeviceToHost);
+      FILE* f = std::fopen((std::string(argv[1]) + (m ? ".tiny" : "")).c_str(), "wb");
+      std::fwrite(r.data(), 8, r.size(), f);
+      std::fclose(f);
+    }
+  }
 #ifdef HAVE_DIAG2
   double* o2;
   cudaMalloc(&o2, 8 * (64 + 1024));
