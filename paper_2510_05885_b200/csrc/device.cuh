@@ -72,12 +72,11 @@ __device__ __forceinline__ int ld_acquire(const int* p) {
 // ld.acquire.gpu costs: CCTL.IVALL after every poll, and with it the L1 hits
 // of all static index data).  Ordering: the producer's lanes store their data,
 // meet at a warp barrier and lane 0 releases the flag (st.release.gpu,
-// ldl_kernels.cu publish).  The consumer polls relaxed and, once per node
-// after its last poll, completes the acquire pattern with fence.acq_rel.gpu
-// (flag_wait_done: "a strong read followed by fence.acq_rel" is an acquire in
-// the PTX memory model), so the producer's release synchronizes-with it and
-// the __syncwarp that follows carries the edge to every lane.  Its loads of
-// the produced data are L2 loads (ld.global.cg) issued after that.
+// ldl_kernels.cu publish).  The consumer polls relaxed and, once per flag
+// after its last poll, reads the flag with ld.acquire.gpu (flag_acquire), so
+// the producer's release synchronizes-with it and the __syncwarp that follows
+// carries the edge to every lane.  Its loads of the produced data are L2
+// loads (ld.global.cg) issued after that.
 __device__ __forceinline__ int ld_relaxed(const int* p) {
   int v;
   asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -130,10 +129,14 @@ __device__ __forceinline__ void pdl_launch_dependents() {
 }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
-__device__ __forceinline__ void flag_wait_done() {
-  asm volatile("fence.acq_rel.gpu;" ::: "memory");
-  __syncwarp();
-}
+// The acquire half of a flag wait, per flag: the lane that observed `flag` at
+// its epoch (relaxed polls) reads it once more with ld.acquire.gpu (LDG.STRONG
+// + L1 invalidation) -- the producer's st.release synchronizes-with that read,
+// and a __syncwarp after carries the edge to the other lanes.  Cheaper than
+// fence.acq_rel.gpu (MEMBAR.ALL.GPU + ERRBAR: waits for every outstanding
+// access of the warp; 10 % of the warp-tier factorization's stall samples),
+// and nodes without a flag to wait for pay nothing.
+__device__ __forceinline__ void flag_acquire(const int* flag) { (void)ld_acquire(flag); }
 
 __device__ __forceinline__ void st_release(int* p, int v) {
   asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");

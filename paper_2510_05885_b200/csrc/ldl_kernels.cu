@@ -249,14 +249,18 @@ k_factor_warp(SnDev sd, FactorDev fd, const double* __restrict__ kval,
         for (int t = 0; t < kLtA; ++t) av[t] = X.ap[t] >= 0 ? ldg_pin(kval + X.as[t]) : 0.0;
       }
       WT(0);
-      if (X.chid >= 0 && X.chid != heavy && fl != epoch)
-        wait_flag(flags + X.chid, epoch);
+      if (X.chid >= 0 && X.chid != heavy) {
+        if (fl != epoch) wait_flag(flags + X.chid, epoch);
+        flag_acquire(flags + X.chid);
+      }
       for (int c = R.chb + 32 + lane; c < R.che; c += 32) {
         const int ch = sd.ch[c];
-        if (ch != heavy)
+        if (ch != heavy) {
           wait_flag(flags + ch, epoch);
+          flag_acquire(flags + ch);
+        }
       }
-      flag_wait_done();
+      __syncwarp();
       WT(1);
       double lv[kLtR];
 #pragma unroll
@@ -463,13 +467,18 @@ k_fwd_warp(SnDev sd, const double* __restrict__ lval, double* w, double* uvec,
         load_idx(R);
         fl = (chid >= 0 && chid != heavy) ? ld_relaxed(flags + chid) : epoch;
       }
-      if (chid >= 0 && chid != heavy && fl != epoch) wait_flag(flags + chid, epoch);
+      if (chid >= 0 && chid != heavy) {
+        if (fl != epoch) wait_flag(flags + chid, epoch);
+        flag_acquire(flags + chid);
+      }
       for (int c = R.chb + 32 + lane; c < R.che; c += 32) {
         const int ch = sd.ch[c];
-        if (ch != heavy)
+        if (ch != heavy) {
           wait_flag(flags + ch, epoch);
+          flag_acquire(flags + ch);
+        }
       }
-      flag_wait_done();
+      __syncwarp();
       WT(0);
       double uv[kLsR];
 #pragma unroll
@@ -563,9 +572,11 @@ k_bwd_warp(SnDev sd, const double* __restrict__ lval, const double* __restrict__
     {
       const int par = R.spar;
       const int row = (lane >= R.k && lane < R.f) ? __ldg(sd.rows + R.rowsp + lane) : 0;
-      if (par >= 0 && !wide[par] && lane == 0)
+      if (par >= 0 && !wide[par] && lane == 0) {
         wait_flag(flags + par, epoch);
-      flag_wait_done();
+        flag_acquire(flags + par);
+      }
+      __syncwarp();
       xr = (lane >= R.k && lane < R.f) ? __ldcg(x + row) : 0.0;
     }
     for (int q = pe - 1; q >= pb; --q) {

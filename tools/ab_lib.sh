@@ -19,6 +19,6 @@ mkdir -p gpurun_out/ab
 for r in $(seq $rounds); do
   for lib in "" tools/ab/lib_*.so; do
     NCL_B200_LIB=$lib timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu-baseline "$@" > gpurun_out/ab/b.json 2>/dev/null
-    python -c "import json; d=json.load(open('gpurun_out/ab/b.json')); print('${lib:-tree}'.ljust(28), d['value'], d['e2e']['value'], d['roofline'].get('phase_ms'))"
+    python -c "import json; d=json.load(open('gpurun_out/ab/b.json')); print('${lib:-tree}'.ljust(28), d['value'], d['e2e']['value'], (d.get('roofline') or {}).get('phase_ms'))"
   done
 done
