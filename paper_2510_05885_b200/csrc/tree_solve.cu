@@ -8,8 +8,8 @@
 // positions i, i+G, i+2G, ... (forward: children before parents; backward:
 // the reversed list) -- and a front waits only for the fronts it reads:
 // its children's update vectors (forward) or its parent's solution rows
-// (backward), through one flag per front (st.release.gpu / relaxed polls +
-// fence.acq_rel.gpu).  Every CTA runs its positions in list order, so a
+// (backward), through one flag per front (a CTA or cluster barrier, then
+// st.release.gpu by one thread / relaxed polls + one ld.acquire.gpu).  Every CTA runs its positions in list order, so a
 // front is only ever waited on by CTAs holding later positions: no deadlock
 // while all CTAs are resident (grid <= resident CTAs).
 //
@@ -116,7 +116,9 @@ __device__ __forceinline__ void wait_ge_cl(const int* p, int v) {
 __device__ __forceinline__ void wait_ge(const int* p, int v) {
   while (ld_acq_cta(p) < v) __nanosleep(16);
 }
-// a flag of another CTA (gpu scope): relaxed polls, then one acquire fence
+// a flag of another CTA (gpu scope): relaxed polls, then one acquire read of
+// it (device.cuh flag_acquire; the caller's barrier carries the edge to the
+// other threads)
 __device__ __forceinline__ void gwait_ge(const int* p, int v) {
   if (ld_relaxed(p) < v) {
     unsigned ns = 32;
@@ -125,7 +127,7 @@ __device__ __forceinline__ void gwait_ge(const int* p, int v) {
       if (ns < 256) ns <<= 1;
     }
   }
-  asm volatile("fence.acq_rel.gpu;" ::: "memory");
+  flag_acquire(p);
 }
 
 // row blocks of a front: pivot blocks [32R, min(32R+32, k)), then update
@@ -390,10 +392,8 @@ k_fwd_tree(SnDev sd, TreeDev td, const double* __restrict__ lval, double* w, dou
     } else {
       __syncthreads();
     }
-    if (tid == 0 && rank == 0) {
-      __threadfence();
+    if (tid == 0 && rank == 0)  // the barrier above orders every thread's (rank's) writes before it
       st_release(td.flags + g.s, 1);
-    }
     if (tr) {  // per phase: wait, gather, solve, write-out + publish
       const unsigned long long t4 = gtime();
       ph[0] += t1 - t0;
@@ -688,10 +688,7 @@ k_bwd_tree(SnDev sd, TreeDev td, const double* __restrict__ lval, const double* 
     } else {
       __syncthreads();
     }
-    if (tid == 0 && rank == 0) {
-      __threadfence();
-      st_release(td.flags + g.s, 2);
-    }
+    if (tid == 0 && rank == 0) st_release(td.flags + g.s, 2);
     if (tr) {
       const unsigned long long t4 = gtime();
       ph[0] += t1 - t0;
