@@ -1010,9 +1010,19 @@ class LdlSystem {
     P.teams = std::min(static_cast<int>(list.size()), teams);
     P.fmax = fmax;
     P.pmax = pmax;
-    if (std::getenv("NCL_LEVEL_STATS"))
-      std::fprintf(stderr, "[ncl tree] levels %d-%d: %zu fronts on %d teams of %d CTAs (fmax %d)\n",
-                   l0, l1 - 1, list.size(), P.teams, C, fmax);
+    if (std::getenv("NCL_LEVEL_STATS")) {
+      long long nch = 0, nent = 0;
+      int mch = 0;
+      for (int s : list) {
+        const int c = T.ch_ptr[s + 1] - T.ch_ptr[s];
+        nch += c;
+        mch = std::max(mch, c);
+        for (int q = T.ch_ptr[s]; q < T.ch_ptr[s + 1]; ++q) nent += T.rel_ptr[T.ch[q] + 1] - T.rel_ptr[T.ch[q]];
+      }
+      std::fprintf(stderr, "[ncl tree] levels %d-%d: %zu fronts on %d teams of %d CTAs (fmax %d); children per "
+                   "front mean %.1f max %d, update entries per front %.0f\n", l0, l1 - 1, list.size(), P.teams, C,
+                   fmax, static_cast<double>(nch) / list.size(), mch, static_cast<double>(nent) / list.size());
+    }
     return true;
   }
   void build_tree(int /*sms*/) {

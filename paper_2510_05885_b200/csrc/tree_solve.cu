@@ -74,6 +74,9 @@ __device__ __forceinline__ unsigned sptr(const void* p) {
 __device__ __forceinline__ void cp16(void* dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sptr(dst)), "l"(src) : "memory");
 }
+__device__ __forceinline__ void cp4(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sptr(dst)), "l"(src) : "memory");
+}
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_wait() {
@@ -169,8 +172,11 @@ __device__ __forceinline__ FrontGeo front_geo(const SnDev& sd, const double* lva
 
 // ---------------------------------------------------------------------------
 // forward
+constexpr int kGMax = 2048;  // children's update entries staged for a front's gather
 struct FwdSmem {
   double head[kStages][32 * kHeadSL];  // rows [32b, 32b+64) x the 32 columns of block b
+  int grel[kGMax];                     // gather: the children's entries in child order --
+  int gsrc[kGMax];                     //   destination row, update-vector offset
   int xdone;                           // pivot blocks solved
   int cnt[kMaxRB];                     // per row block: panels applied by the bulk warps
 };
@@ -346,6 +352,27 @@ k_fwd_tree(SnDev sd, TreeDev td, const double* __restrict__ lval, double* w, dou
       for (int b = 0; b < kStages; ++b) fwd_stage(sm.head[b], g, b, lane);
     for (int i = tid; i < kMaxRB; i += kThr) sm.cnt[i] = 0;
     if (tid == 0) sm.xdone = 0;
+    // gather: T_r = w_r (pivot rows) + the children's entries in child order.
+    // Its static part before the children are awaited (off the critical
+    // path; cold index loads after the step's L2 flush): this CTA's pivot
+    // rows of w (final before the launch) and every child's destination rows
+    for (int r = row_lo + tid; r < row_hi; r += kThr) T[r] = r < g.k ? __ldcg(w + g.c0 + r) : 0.0;
+    const int ch0 = __ldg(sd.ch_ptr + g.s), ch1 = __ldg(sd.ch_ptr + g.s + 1);
+    int gtot = 0;  // entries staged (-1: more than kGMax, gathered directly)
+    for (int cc = ch0; cc < ch1; ++cc) {
+      const int c = __ldg(sd.ch + cc);
+      const int rp = __ldg(sd.rel_ptr + c), fu = __ldg(sd.rel_ptr + c + 1) - rp;
+      if (gtot + fu > kGMax) {
+        gtot = -1;
+        break;
+      }
+      for (int i = tid; i < fu; i += kThr) {
+        cp4(&sm.grel[gtot + i], sd.rel + rp + i);
+        sm.gsrc[gtot + i] = rp + i;
+      }
+      gtot += fu;
+    }
+    cp_commit();
     if (C > 1) cl.sync();  // rank 0's progress is reset before any rank reads it
     // children's update vectors: wide children in the list publish flags
     if (warp == 1) {
@@ -354,20 +381,43 @@ k_fwd_tree(SnDev sd, TreeDev td, const double* __restrict__ lval, double* w, dou
     }
     __syncthreads();
     if (tr) t1 = gtime();
-    // gather: T_r = w_r (pivot rows) + the children's entries in child order
-    // -- child by child, every entry of a child (landing in this CTA's rows)
-    // loaded at once, a CTA barrier between children
-    for (int r = row_lo + tid; r < row_hi; r += kThr) T[r] = r < g.k ? __ldcg(w + g.c0 + r) : 0.0;
-    __syncthreads();
-    for (int cc = __ldg(sd.ch_ptr + g.s); cc < __ldg(sd.ch_ptr + g.s + 1); ++cc) {
-      const int c = __ldg(sd.ch + cc);
-      const int rp = __ldg(sd.rel_ptr + c), fu = __ldg(sd.rel_ptr + c + 1) - rp;
-      for (int i = tid; i < fu; i += kThr) {
-        const int dr = __ldg(sd.rel + rp + i);
-        const double u = __ldcg(uvec + rp + i);
-        if (dr >= row_lo && dr < row_hi) T[dr] += u;
+    if (gtot >= 0) {  // every child's update entries in one round trip, then child by child
+      cp_wait<0>();
+      __syncthreads();  // grel / gsrc staged
+      constexpr int kJ = kGMax / kThr;
+      double v[kJ];
+#pragma unroll
+      for (int j = 0; j < kJ; ++j) {
+        const int e = tid + j * kThr;
+        v[j] = e < gtot ? __ldcg(uvec + sm.gsrc[e]) : 0.0;
       }
+      for (int cc = ch0, o = 0; cc < ch1; ++cc) {
+        const int c = __ldg(sd.ch + cc);
+        const int o1 = o + __ldg(sd.rel_ptr + c + 1) - __ldg(sd.rel_ptr + c);
+#pragma unroll
+        for (int j = 0; j < kJ; ++j) {
+          const int e = tid + j * kThr;
+          if (e >= o && e < o1) {
+            const int dr = sm.grel[e];
+            if (dr >= row_lo && dr < row_hi) T[dr] += v[j];
+          }
+        }
+        o = o1;
+        __syncthreads();
+      }
+    } else {  // child by child, a CTA barrier between children
+      cp_wait<0>();
       __syncthreads();
+      for (int cc = ch0; cc < ch1; ++cc) {
+        const int c = __ldg(sd.ch + cc);
+        const int rp = __ldg(sd.rel_ptr + c), fu = __ldg(sd.rel_ptr + c + 1) - rp;
+        for (int i = tid; i < fu; i += kThr) {
+          const int dr = __ldg(sd.rel + rp + i);
+          const double u = __ldcg(uvec + rp + i);
+          if (dr >= row_lo && dr < row_hi) T[dr] += u;
+        }
+        __syncthreads();
+      }
     }
     if (tr) t2 = gtime();
     if (rank == 0) {
