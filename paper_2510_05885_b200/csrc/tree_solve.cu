@@ -464,6 +464,7 @@ struct BwdSmem {
   // 16-byte chunk c at chunk index q*32 + (c ^ (q & 7)) (lane = column reads)
   double head[kStages][32 * 64];
   double Ts[kBulk][32 * kTsSL];  // per bulk warp: one 32x32 block, row-major
+  int grow[kTreeMaxF];           // x positions of this CTA's update rows (staged)
   int xdone;                     // pivot blocks solved, counted from the last
   int cnt[kMaxRB];               // per column block: contributions applied
 };
@@ -711,17 +712,23 @@ k_bwd_tree(SnDev sd, TreeDev td, const double* __restrict__ lval, const double* 
     // z_q = w_q / d_q for the pivots (the forward result, final)
     if (rank == 0)
       for (int q = tid; q < g.k; q += kThr) X[q] = __ldg(w + g.c0 + q) / __ldg(d + g.c0 + q);
+    // the x positions of this CTA's update rows: static, staged before the
+    // parent is awaited (cold index loads off the critical path)
+    const int ur0 = g.rhi > g.rlo ? rb_start(g.k, g.P, g.rlo) : 0;
+    const int ur1 = g.rhi > g.rlo ? min(g.f, rb_start(g.k, g.P, g.rhi - 1) + 32) : 0;
+    {
+      const int* rows = sd.rows + __ldg(sd.rows_ptr + g.s);
+      for (int r = ur0 + tid; r < ur1; r += kThr) cp4(&sm.grow[r], rows + r);
+      cp_commit();
+    }
     if (C > 1) cl.sync();  // rank 0's slots and counters are reset before any rank adds to them
     // the parent's solution rows (the CTAs that own update rows)
     const int par = __ldg(td.par + li);
     if (tid == 0 && par >= 0 && g.rhi > g.rlo) gwait_ge(td.flags + par, 2);
+    cp_wait<0>();
     __syncthreads();
     if (tr) t1 = gtime();
-    if (g.rhi > g.rlo) {
-      const int* rows = sd.rows + __ldg(sd.rows_ptr + g.s);
-      const int r1 = min(g.f, rb_start(g.k, g.P, g.rhi - 1) + 32);
-      for (int r = rb_start(g.k, g.P, g.rlo) + tid; r < r1; r += kThr) X[r] = __ldcg(x + __ldg(rows + r));
-    }
+    for (int r = ur0 + tid; r < ur1; r += kThr) X[r] = __ldcg(x + sm.grow[r]);
     __syncthreads();
     if (tr) t2 = gtime();
     if (rank == 0) {
