@@ -116,6 +116,10 @@ __device__ __forceinline__ void cp16(void* dst, const void* src) {
   const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
 }
+__device__ __forceinline__ void cp4(void* dst, const void* src) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(src) : "memory");
+}
 __device__ __forceinline__ void cp_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
@@ -991,12 +995,17 @@ k_wide_update(SnDev sd, FactorDev fd, const int4* __restrict__ tiles, int count,
 // bitwise the k_wide_front arithmetic.
 constexpr int kMidF = 216;
 
+constexpr int kMidCh = 16;    // children whose row maps are staged before the wait
+constexpr int kMidRel = 1024;  // staged row-map entries (all children)
 struct MidSmem {
   PanelSmem sm;
   alignas(16) double D[kWidePanel * kSL];
   double dv[kWidePanel];
-  int rel[kMidF];  // the current child's row map into the front
-  int cb[kMidF];   // column bases of the packed front
+  const double* chU[kMidCh];  // per child: its update block, rows, leading dimension
+  int chfu[kMidCh], chld[kMidCh], chrp[kMidCh];
+  int relall[kMidRel];  // the children's row maps into the front, child order
+  int rel[kMidF];       // one child's row map (more than kMidCh children / kMidRel entries)
+  int cb[kMidF];        // column bases of the packed front
 };
 
 // the front's tile (rows r0.., columns q0..; nr x nc; lower part only when
@@ -1074,39 +1083,87 @@ k_mid_front(SnDev sd, FactorDev fd, const double* __restrict__ kval, const int* 
   pdl_launch_dependents();
   // column J: rows J..f-1 after the columns before it
   for (int J = t; J < f; J += NT) M.cb[J] = J * f - (J * (J - 1)) / 2 - J;
-  pdl_wait();  // the children (previous level)
   // assembly: zero, the A entries, then the children in child order (per
-  // position the order of the column pass of assemble_col)
+  // position the order of the column pass of assemble_col).  Everything but
+  // the children's update values is static (kval is complete before the
+  // level launches), so it is done before the programmatic wait: the first
+  // wave overlaps the previous level and no CTA waits on index loads after it
   const int ntri = f * (f + 1) / 2;
   for (int i = t; i < ntri; i += NT) S[i] = 0.0;
   if (t == 0) M.sm.prog = 0;
+  const int ch0 = sd.ch_ptr[s], nch = sd.ch_ptr[s + 1] - ch0;
+  const bool chpre = nch <= kMidCh;
+  if (chpre && t < nch) {
+    const int c = sd.ch[ch0 + t];
+    M.chfu[t] = f_minus_k(sd, c);
+    M.chld[t] = sd.u_ld[c];
+    M.chrp[t] = sd.rel_ptr[c];
+    M.chU[t] = (sd.wide[c] ? fd.lval : fd.upd) + sd.u_off[c];
+  }
   __syncthreads();
   for (int q = sd.asm_ptr[s] + t; q < sd.asm_ptr[s + 1]; q += NT) {
     const int pos = sd.asm_pos[q];
     S[cb[pos >> 16] + (pos & 0xffff)] += __ldg(kval + sd.asm_slot[q]);
   }
+  int nrel = 0;  // row-map entries staged (-1: too many, staged per child)
+  if (chpre) {
+    for (int ci = 0; ci < nch; ++ci) {
+      const int fu = M.chfu[ci];
+      if (nrel + fu > kMidRel) {
+        nrel = -1;
+        break;
+      }
+      for (int i = t; i < fu; i += NT) cp4(&M.relall[nrel + i], sd.rel + M.chrp[ci] + i);
+      nrel += fu;
+    }
+  } else {
+    nrel = -1;
+  }
+  cp_commit();
+  cp_wait_all();
+  pdl_wait();  // the children (previous level)
   __syncthreads();
-  // a child at a time: its row map into shared memory, then its entries
-  // (i, j), i >= j, in batches of 16 per thread with every load of a batch in
-  // flight (entries of one child land on distinct positions)
-  for (int cc = sd.ch_ptr[s]; cc < sd.ch_ptr[s + 1]; ++cc) {
-    const int c = sd.ch[cc];
-    const int fu = f_minus_k(sd, c);
-    const int uld = sd.u_ld[c];
-    const double* U = (sd.wide[c] ? fd.lval : fd.upd) + sd.u_off[c];
-    const int* rel = sd.rel + sd.rel_ptr[c];
-    for (int i = t; i < fu; i += NT) M.rel[i] = __ldg(rel + i);
-    __syncthreads();
+  // a child at a time: its entries (i, j), i >= j, in batches of 16 per thread
+  // with every load of a batch in flight (entries of one child land on
+  // distinct positions)
+  for (int ci = 0, ro = 0; ci < nch; ++ci) {
+    int fu, uld;
+    const double* U;
+    const int* rel;
+    if (nrel >= 0) {
+      fu = M.chfu[ci];
+      uld = M.chld[ci];
+      U = M.chU[ci];
+      rel = M.relall + ro;
+      ro += fu;
+    } else {
+      const int c = sd.ch[ch0 + ci];
+      fu = f_minus_k(sd, c);
+      uld = sd.u_ld[c];
+      U = (sd.wide[c] ? fd.lval : fd.upd) + sd.u_off[c];
+      const int* grel = sd.rel + sd.rel_ptr[c];
+      for (int i = t; i < fu; i += NT) M.rel[i] = __ldg(grel + i);
+      __syncthreads();
+      rel = M.rel;
+    }
     const int n2 = fu * fu;
+    const float rfu = 1.0f / static_cast<float>(fu);
     for (int e0 = 0; e0 < n2; e0 += NT * 16) {
       double v[16];
       int pos[16];
 #pragma unroll
       for (int b = 0; b < 16; ++b) {
         const int e = e0 + b * NT + t;
-        const int j = e / fu, i = e - j * fu;
+        int j = __float2int_rz((static_cast<float>(e) + 0.5f) * rfu), i = e - j * fu;  // e = j fu + i
+        if (i < 0) {
+          --j;
+          i += fu;
+        } else if (i >= fu) {
+          ++j;
+          i -= fu;
+        }
         const bool ok = e < n2 && i >= j;
-        pos[b] = ok ? cb[M.rel[j]] + M.rel[i] : -1;
+        pos[b] = ok ? cb[rel[j]] + rel[i] : -1;
         v[b] = ok ? __ldcg(U + i + static_cast<size_t>(j) * uld) : 0.0;
       }
 #pragma unroll
