@@ -173,18 +173,40 @@ __device__ __forceinline__ void tri_decode(int t, int& i, int& j) {
 // ---------------------------------------------------------------------------
 // assembly of front column J (one warp).  acc: f doubles of shared memory
 // private to this warp, or nullptr to accumulate in place (huge fronts).
-__device__ __noinline__ void assemble_col(const SnDev& sd, const FactorDev& fd,
-                                          const double* __restrict__ kval, int s, int c0, int k,
-                                          int f, double* F, size_t ld, int J, double* acc) {
+// Index words are static: ColMeta (the column's contribution and A-entry
+// ranges) can be loaded a column ahead (assemble_cols), and the first A chunk
+// and children group are issued before the zero fill.
+struct ColMeta {
+  int e0, e1, a0, a1;
+};
+__device__ __forceinline__ ColMeta col_meta(const SnDev& sd, int s, int c0, int k, int J) {
+  const int cb = sd.cc_off[s] + J;
+  return ColMeta{ldg_pin(sd.cc_ptr + cb), ldg_pin(sd.cc_ptr + cb + 1), J < k ? ldg_pin(sd.asm_cp + c0 + J) : 0,
+                 J < k ? ldg_pin(sd.asm_cp + c0 + J + 1) : 0};
+}
+__device__ __forceinline__ void assemble_col_m(const SnDev& sd, const FactorDev& fd,
+                                               const double* __restrict__ kval, int s, int f, double* F,
+                                               size_t ld, int J, double* acc, const ColMeta& m) {
+  constexpr int G = 4;
   const int lane = threadIdx.x & 31;
   double* col = F + J * ld;
   double* a = acc ? acc : col;
-  const int cb = sd.cc_off[s] + J;
-  const int e0 = sd.cc_ptr[cb], e1 = sd.cc_ptr[cb + 1];
-  const int a0 = J < k ? sd.asm_cp[c0 + J] : 0, a1 = J < k ? sd.asm_cp[c0 + J + 1] : 0;
+  const int e0 = m.e0, e1 = m.e1, a0 = m.a0, a1 = m.a1;
+  const int qa = a0 + lane;
+  const int ap0 = qa < a1 ? ldg_pin(sd.asm_pos + qa) : 0, as0 = qa < a1 ? ldg_pin(sd.asm_slot + qa) : 0;
+  int cw0[G], rb0[G];
+  long long ub0[G];
+#pragma unroll
+  for (int t = 0; t < G; ++t) {
+    const bool in = e0 + t < e1;
+    cw0[t] = in ? ldg_pin(sd.cc_cnt + e0 + t) : 0;
+    ub0[t] = in ? ldg_pin(sd.cc_ubase + e0 + t) : 0;
+    rb0[t] = in ? ldg_pin(sd.cc_rbase + e0 + t) : 0;
+  }
   for (int r = J + lane; r < f; r += 32) a[r] = 0.0;
   __syncwarp();
-  for (int q = a0 + lane; q < a1; q += 32) a[sd.asm_pos[q] & 0xffff] += __ldg(kval + sd.asm_slot[q]);
+  if (qa < a1) a[ap0 & 0xffff] += __ldg(kval + as0);
+  for (int q = qa + 32; q < a1; q += 32) a[sd.asm_pos[q] & 0xffff] += __ldg(kval + sd.asm_slot[q]);
   __syncwarp();
   const int ng = sd.split_ng[s];
   if (ng) {  // group sums of the contributions (split.cu), in group order
@@ -202,7 +224,6 @@ __device__ __noinline__ void assemble_col(const SnDev& sd, const FactorDev& fd,
     // barrier each); per position the order is fixed by (32-row chunk, child),
     // so sums are deterministic, though not child by child for columns
     // taller than 32 rows
-    constexpr int G = 4;
     for (int eg = e0; eg < e1; eg += G) {
       const double* U[G];
       const int* rel[G];
@@ -214,10 +235,10 @@ __device__ __noinline__ void assemble_col(const SnDev& sd, const FactorDev& fd,
         U[t] = nullptr;
         rel[t] = nullptr;
         if (e < e1) {
-          const int cw = sd.cc_cnt[e];
+          const int cw = eg == e0 ? cw0[t] : sd.cc_cnt[e];
           cnt[t] = cw & ((1 << 30) - 1);
-          U[t] = ((cw >> 30) ? fd.lval : fd.upd) + sd.cc_ubase[e];
-          rel[t] = sd.rel + sd.cc_rbase[e];
+          U[t] = ((cw >> 30) ? fd.lval : fd.upd) + (eg == e0 ? ub0[t] : sd.cc_ubase[e]);
+          rel[t] = sd.rel + (eg == e0 ? rb0[t] : sd.cc_rbase[e]);
           mc = max(mc, cnt[t]);
         }
       }
@@ -250,6 +271,28 @@ __device__ __noinline__ void assemble_col(const SnDev& sd, const FactorDev& fd,
   }
   if (acc)
     for (int r = J + lane; r < f; r += 32) col[r] = a[r];
+}
+__device__ __noinline__ void assemble_col(const SnDev& sd, const FactorDev& fd,
+                                          const double* __restrict__ kval, int s, int c0, int k,
+                                          int f, double* F, size_t ld, int J, double* acc) {
+  assemble_col_m(sd, fd, kval, s, f, F, ld, J, acc, col_meta(sd, s, c0, k, J));
+}
+// columns J, J + Js, ... of the front on one warp, the next column's ColMeta
+// in flight while a column is assembled
+__device__ __noinline__ void assemble_cols(const SnDev& sd, const FactorDev& fd,
+                                           const double* __restrict__ kval, int s, int c0, int k,
+                                           int f, double* F, size_t ld, int J, int Js, double* acc) {
+  if (J >= f) return;
+  ColMeta m = col_meta(sd, s, c0, k, J);
+  for (;;) {
+    const int Jn = J + Js;
+    ColMeta mn{0, 0, 0, 0};
+    if (Jn < f) mn = col_meta(sd, s, c0, k, Jn);
+    assemble_col_m(sd, fd, kval, s, f, F, ld, J, acc, m);
+    if (Jn >= f) break;
+    J = Jn;
+    m = mn;
+  }
 }
 
 // 1/d without the branchy slow path of __drcp_rn (which splits the pivot loop
@@ -534,8 +577,7 @@ k_wide_front(SnDev sd, FactorDev fd, const double* __restrict__ kval,
   if (tr) trace[fi * 128 + ti++] = globaltimer();
   {
     double* acc = dyn_smem + static_cast<size_t>(warp) * acc_f;
-    for (int J = rank * kWarps + warp; J < f; J += C * kWarps)
-      assemble_col(sd, fd, kval, s, c0, k, f, F, ld, J, acc);
+    assemble_cols(sd, fd, kval, s, c0, k, f, F, ld, rank * kWarps + warp, C * kWarps, acc);
   }
   cl.sync();
   if (tr) trace[fi * 128 + ti++] = globaltimer();
