@@ -184,30 +184,42 @@ __device__ __forceinline__ ColMeta col_meta(const SnDev& sd, int s, int c0, int 
   return ColMeta{ldg_pin(sd.cc_ptr + cb), ldg_pin(sd.cc_ptr + cb + 1), J < k ? ldg_pin(sd.asm_cp + c0 + J) : 0,
                  J < k ? ldg_pin(sd.asm_cp + c0 + J + 1) : 0};
 }
-__device__ __forceinline__ void assemble_col_m(const SnDev& sd, const FactorDev& fd,
-                                               const double* __restrict__ kval, int s, int f, double* F,
-                                               size_t ld, int J, double* acc, const ColMeta& m) {
-  constexpr int G = 4;
+constexpr int kColG = 4;  // children per contribution group
+struct ColPre {  // the first children group's index words
+  int cw0[kColG], rb0[kColG];
+  long long ub0[kColG];
+};
+// the column's static part: zero fill and A entries (kval is an input)
+__device__ __forceinline__ void col_static(const SnDev& sd, const double* __restrict__ kval, int f, int J,
+                                           double* a, const ColMeta& m, ColPre& p) {
   const int lane = threadIdx.x & 31;
-  double* col = F + J * ld;
-  double* a = acc ? acc : col;
-  const int e0 = m.e0, e1 = m.e1, a0 = m.a0, a1 = m.a1;
-  const int qa = a0 + lane;
-  const int ap0 = qa < a1 ? ldg_pin(sd.asm_pos + qa) : 0, as0 = qa < a1 ? ldg_pin(sd.asm_slot + qa) : 0;
-  int cw0[G], rb0[G];
-  long long ub0[G];
+  const int qa = m.a0 + lane;
+  const int ap0 = qa < m.a1 ? ldg_pin(sd.asm_pos + qa) : 0, as0 = qa < m.a1 ? ldg_pin(sd.asm_slot + qa) : 0;
 #pragma unroll
-  for (int t = 0; t < G; ++t) {
-    const bool in = e0 + t < e1;
-    cw0[t] = in ? ldg_pin(sd.cc_cnt + e0 + t) : 0;
-    ub0[t] = in ? ldg_pin(sd.cc_ubase + e0 + t) : 0;
-    rb0[t] = in ? ldg_pin(sd.cc_rbase + e0 + t) : 0;
+  for (int t = 0; t < kColG; ++t) {
+    const bool in = m.e0 + t < m.e1;
+    p.cw0[t] = in ? ldg_pin(sd.cc_cnt + m.e0 + t) : 0;
+    p.ub0[t] = in ? ldg_pin(sd.cc_ubase + m.e0 + t) : 0;
+    p.rb0[t] = in ? ldg_pin(sd.cc_rbase + m.e0 + t) : 0;
   }
   for (int r = J + lane; r < f; r += 32) a[r] = 0.0;
   __syncwarp();
-  if (qa < a1) a[ap0 & 0xffff] += __ldg(kval + as0);
-  for (int q = qa + 32; q < a1; q += 32) a[sd.asm_pos[q] & 0xffff] += __ldg(kval + sd.asm_slot[q]);
+  if (qa < m.a1) a[ap0 & 0xffff] += __ldg(kval + as0);
+  for (int q = qa + 32; q < m.a1; q += 32) a[sd.asm_pos[q] & 0xffff] += __ldg(kval + sd.asm_slot[q]);
   __syncwarp();
+}
+// the children's contributions (the previous level's update blocks), then
+// the column out of acc
+__device__ __forceinline__ void col_children(const SnDev& sd, const FactorDev& fd, int s, int f, double* F,
+                                             size_t ld, int J, double* acc, const ColMeta& m, const ColPre& p) {
+  constexpr int G = kColG;
+  const int lane = threadIdx.x & 31;
+  double* col = F + J * ld;
+  double* a = acc ? acc : col;
+  const int e0 = m.e0, e1 = m.e1;
+  const int* cw0 = p.cw0;
+  const int* rb0 = p.rb0;
+  const long long* ub0 = p.ub0;
   const int ng = sd.split_ng[s];
   if (ng) {  // group sums of the contributions (split.cu), in group order
     const double* P = fd.ccpart + sd.split_off[s] + static_cast<size_t>(J) * ng * f;
@@ -271,6 +283,13 @@ __device__ __forceinline__ void assemble_col_m(const SnDev& sd, const FactorDev&
   }
   if (acc)
     for (int r = J + lane; r < f; r += 32) col[r] = a[r];
+}
+__device__ __forceinline__ void assemble_col_m(const SnDev& sd, const FactorDev& fd,
+                                               const double* __restrict__ kval, int s, int f, double* F,
+                                               size_t ld, int J, double* acc, const ColMeta& m) {
+  ColPre p;
+  col_static(sd, kval, f, J, acc ? acc : F + J * ld, m, p);
+  col_children(sd, fd, s, f, F, ld, J, acc, m, p);
 }
 __device__ __noinline__ void assemble_col(const SnDev& sd, const FactorDev& fd,
                                           const double* __restrict__ kval, int s, int c0, int k,
@@ -667,11 +686,18 @@ k_wide_assemble(SnDev sd, FactorDev fd, const double* __restrict__ kval,
   const int4 t = tasks[blockIdx.x];
   const int s = t.x, J = t.y + (threadIdx.x >> 5);
   pdl_launch_dependents();
-  pdl_wait();  // the previous level (programmatic launch)
   const int c0 = sd.first[s], f = sd.f[s], k = sd.first[s + 1] - c0;
-  if (J < min(f, t.y + kAsmCols))
-    assemble_col(sd, fd, kval, s, c0, k, f, fd.lval + sd.l_off[s], wide_ld(f), J,
-                 asm_acc + static_cast<size_t>(threadIdx.x >> 5) * acc_f);
+  const bool mine = J < min(f, t.y + kAsmCols);
+  double* acc = asm_acc + static_cast<size_t>(threadIdx.x >> 5) * acc_f;
+  ColMeta m{0, 0, 0, 0};
+  ColPre p;
+  // the static part (index words, zero fill, A entries) before the wait
+  if (mine) {
+    m = col_meta(sd, s, c0, k, J);
+    col_static(sd, kval, f, J, acc, m, p);
+  }
+  pdl_wait();  // the previous level (programmatic launch)
+  if (mine) col_children(sd, fd, s, f, fd.lval + sd.l_off[s], wide_ld(f), J, acc, m, p);
 }
 
 // one CTA per (front, 128-row block below the panel): warp 0 factors the
