@@ -760,7 +760,8 @@ class LdlSystem {
     }
     build_dag_segments(sms);
     // opt-in (NCL_HUGE_LEVEL=1): measured slower than the per-panel launches
-    // on the 78k-bus mesh (3.28 vs 2.80 ms per factorization: a flag hop per
+    // on the 78k-bus mesh (2.43 vs 2.15 ms per factorization with the acquire
+    // reads of this round; 3.28 vs 2.80 ms with fence.acq_rel: a flag hop per
     // panel instead of the programmatic launch, staging unchanged)
     if (std::getenv("NCL_HUGE_LEVEL") && T.lp_ptr.back() > 0) {
       huge_ctas_ = huge_level_ctas();

@@ -931,14 +931,11 @@ __device__ __forceinline__ void huge_wait(const int* p, int v) {
       if (ns < 256) ns <<= 1;
     }
   }
-  asm volatile("fence.acq_rel.gpu;" ::: "memory");
+  flag_acquire(p);  // the caller's CTA barrier carries it to the other threads
 }
 __device__ __forceinline__ void huge_done(int* p) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(p) : "memory");
-  }
+  __syncthreads();  // every thread's writes before thread 0's release
+  if (threadIdx.x == 0) asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(p) : "memory");
 }
 
 __global__ void __launch_bounds__(kHugeRows)
