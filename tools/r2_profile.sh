@@ -1,7 +1,8 @@
 #!/bin/bash
 # Round-2 profile capture (gpurun from the repo root): bench lines of every
-# workload with the reference CPU arm, the mesh launch list (time + DRAM bytes
-# per launch) and ncu --set full captures of the top kernels.
+# workload with the reference CPU arm, the mesh launch lists (time + DRAM bytes
+# per launch; caches flushed per kernel by ncu's default, and not flushed) and
+# ncu --set full captures of the top kernels.
 O=gpurun_out/r2p
 mkdir -p $O
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > $O/gpu.txt
@@ -14,13 +15,13 @@ timeout 900 python bench.py --steps 5 --warmup 3 --workload elec:1000:1 --form k
 timeout 900 python bench.py --steps 5 --warmup 3 --workload bearing:1000:1000 --form k2r > $O/bench_bearing1000_k2r.json 2> $O/bearing.err
 timeout 500 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
   -c 3000 --csv --log-file $O/launches_mesh280_k1s.csv python bench.py --steps 1 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
-timeout 400 ncu --set full --clock-control none --import-source on -k regex:k_wide_panel_f -s 40 -c 1 \
-  -o $O/prof_wide_panel_f python bench.py --steps 1 --warmup 1 --no-cpu-baseline > /dev/null 2>&1
-timeout 400 ncu --set full --clock-control none --import-source on -k regex:k_fwd_tree -s 2 -c 1 \
-  -o $O/prof_fwd_tree python bench.py --steps 1 --warmup 1 --no-cpu-baseline > /dev/null 2>&1
-timeout 400 ncu --set full --clock-control none --import-source on -k regex:k_bwd_tree -s 2 -c 1 \
-  -o $O/prof_bwd_tree python bench.py --steps 1 --warmup 1 --no-cpu-baseline > /dev/null 2>&1
-timeout 400 ncu --set full --clock-control none --import-source on -k regex:k_wide_front -s 6 -c 1 \
-  -o $O/prof_wide_front python bench.py --steps 1 --warmup 1 --no-cpu-baseline > /dev/null 2>&1
+timeout 500 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
+  --cache-control none -c 3000 --csv --log-file $O/launches_mesh280_k1s_nocacheflush.csv python bench.py --steps 1 --warmup 3 \
+  --no-cpu-baseline > /dev/null 2>&1
+for k in k_wide_panel_f:40 k_wide_update:40 k_fwd_tree:2 k_bwd_tree:2 k_wide_front:6 k_mid_front:5 k_factor_warp:3 k_wide_assemble:10; do
+  n=${k%%:*}; s=${k##*:}
+  timeout 400 ncu --set full --clock-control none --import-source on -k regex:$n -s $s -c 1 \
+    -o $O/prof_$n python bench.py --steps 1 --warmup 1 --no-cpu-baseline > /dev/null 2>&1
+done
 for f in $O/*.json; do echo $f; python -c "import json; d=json.load(open('$f')); print(d.get('value'), (d.get('e2e') or {}).get('value'), (d.get('cpu_baseline') or {}).get('value'), (d.get('roofline') or {}).get('phase_ms'))"; done
 ls -la $O
