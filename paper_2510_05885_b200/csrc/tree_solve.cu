@@ -678,6 +678,13 @@ k_bwd_tree(SnDev sd, TreeDev td, const double* __restrict__ lval, const double* 
     rm.rank = rank;
   }
   unsigned long long ph[5] = {0, 0, 0, 0, 0};  // trace: SM clocks per phase, summed over the fronts
+  for (int i = tid; i < kMaxRB; i += kThr) sm.cnt[i] = 0;
+  for (int i = tid; i < kSlots * 32 * pmax; i += kThr) acc[i] = 0.0;
+  if (tid == 0) sm.xdone = 0;
+  if (C > 1)
+    cl.sync();  // every rank's slots are zero before any rank adds to rank 0's
+  else
+    __syncthreads();
   for (int li0 = team; li0 < td.n; li0 += nteams) {
     const int li = td.n - 1 - li0;
     FrontGeo g = front_geo(sd, lval, __ldg(td.list + li));
@@ -705,10 +712,9 @@ k_bwd_tree(SnDev sd, TreeDev td, const double* __restrict__ lval, const double* 
     unsigned long long t0 = tr ? gtime() : 0, t1 = 0, t2 = 0, t3 = 0;
     if (warp == 0 && rank == 0)
       for (int o = 0; o < kStages; ++o) bwd_stage(sm.head[o], g, g.P - 1 - o, lane);
-    for (int i = tid; i < kMaxRB; i += kThr) sm.cnt[i] = 0;
-    for (int sl = 0; sl < kSlots; ++sl)
-      for (int i = tid; i < 32 * g.P; i += kThr) acc[sl * 32 * pmax + i] = 0.0;
-    if (tid == 0) sm.xdone = 0;
+    // the slots and counters are zero here: zeroed before the loop and after
+    // every front (before its closing barrier), so no cluster barrier is
+    // needed before the other ranks add to rank 0's
     // z_q = w_q / d_q for the pivots (the forward result, final)
     if (rank == 0)
       for (int q = tid; q < g.k; q += kThr) X[q] = __ldg(w + g.c0 + q) / __ldg(d + g.c0 + q);
@@ -721,7 +727,6 @@ k_bwd_tree(SnDev sd, TreeDev td, const double* __restrict__ lval, const double* 
       for (int r = ur0 + tid; r < ur1; r += kThr) cp4(&sm.grow[r], rows + r);
       cp_commit();
     }
-    if (C > 1) cl.sync();  // rank 0's slots and counters are reset before any rank adds to them
     // the parent's solution rows (the CTAs that own update rows)
     const int par = __ldg(td.par + li);
     if (tid == 0 && par >= 0 && g.rhi > g.rlo) gwait_ge(td.flags + par, 2);
@@ -740,8 +745,13 @@ k_bwd_tree(SnDev sd, TreeDev td, const double* __restrict__ lval, const double* 
       bwd_bulk<true>(g, warp - 1, X, acc + (warp - 1) * 32 * pmax, sm, false, rm);
     }
     if (tr) t3 = gtime();
+    __syncthreads();  // this CTA is done with its slots and counters (rank 0: every partial consumed)
+    for (int i = tid; i < kMaxRB; i += kThr) sm.cnt[i] = 0;
+    for (int sl = 0; sl < kSlots; ++sl)
+      for (int i = tid; i < 32 * g.P; i += kThr) acc[sl * 32 * pmax + i] = 0.0;
+    if (tid == 0) sm.xdone = 0;
     if (C > 1) {
-      cl.sync();  // rank 0 is done with its slots; every rank's x rows are out
+      cl.sync();  // every rank's x rows are out and slots reset
     } else {
       __syncthreads();
     }
