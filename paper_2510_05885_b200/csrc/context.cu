@@ -167,7 +167,7 @@ class LdlSystem {
       }
       if (mid_level(l)) {  // a 4-warp CTA per front, the front in shared memory
         launch_mid_front(sd_, fd, kval, lvl_nodes_.p + T.lvl_ptr[l], T.lvl_ptr[l + 1] - T.lvl_ptr[l],
-                         lvl_fmax_[l], eps, st_);
+                         lvl_fmax_[l], eps, st_, stage_gather_);
         launches_ += 1;
         continue;
       }
@@ -1001,7 +1001,7 @@ class LdlSystem {
       tr_trace_[idx].zero(st_);
     }
     P.td = TreeDev{P.list.p, static_cast<int>(list.size()), P.wptr.p, P.wait.p, P.par.p,
-                   tr_flags_.p, trmode == 3 ? nullptr : tr_trace_[idx].p};
+                   tr_flags_.p, trmode == 3 ? nullptr : tr_trace_[idx].p, stage_gather_ ? 1 : 0};
     P.lvl.assign(list.size(), 0);
     for (int l = l0; l < l1; ++l)
       for (int q = T.lvl_ptr[l]; q < T.lvl_ptr[l + 1]; ++q) P.lvl[pos[T.lvl_nodes[q]]] = l;
@@ -1200,6 +1200,10 @@ class LdlSystem {
   bool use_graph_ = std::getenv("NCL_NO_GRAPH") == nullptr;
   // huge levels: strip update folded into the panel kernel (NCL_NO_FUSED_PANEL=1: separate launch)
   bool fused_panel_ = std::getenv("NCL_NO_FUSED_PANEL") == nullptr;
+  // NCL_NO_STAGED_GATHER=1 (tests): the mid-front assembly and the tree forward
+  // gather take their unstaged fallback paths (more children / entries than
+  // the staging buffers hold)
+  bool stage_gather_ = std::getenv("NCL_NO_STAGED_GATHER") == nullptr;
   // huge levels as one persistent launch (opt-in NCL_HUGE_LEVEL=1)
   int huge_ctas_ = 0;
   DBuf<int> hcnt_, pn_ptr_, tl_ptr_, dg_ptr_;

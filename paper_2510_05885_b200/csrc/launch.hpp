@@ -97,7 +97,7 @@ void launch_bwd_warp(const SnDev& sd, const double* lval, const double* d,
 // mid_front_limit() rows, one 4-warp CTA per front kept in shared memory
 int mid_front_limit();
 void launch_mid_front(const SnDev& sd, const FactorDev& fd, const double* kval, const int* nodes, int count,
-                      int fmax, double eps, cudaStream_t st);
+                      int fmax, double eps, cudaStream_t st, bool stage = true);
 // small_front.cu: levels whose fronts all have <= small_*_limit() rows, one
 // warp per front (factorization; forward and backward solve)
 int small_factor_limit();
@@ -127,6 +127,7 @@ struct TreeDev {
   const int* par;       // backward: per list position, the parent if in the list, else -1
   int* flags;           // per supernode: 1 forward done, 2 backward done
   unsigned long long* trace;  // diagnostic (NCL_TREE_TRACE): phase clocks per team and direction
+  int stage;            // 0: the forward gather's direct loop only (NCL_NO_STAGED_GATHER, tests)
 };
 constexpr int kTreeMaxF = 2048;
 constexpr int kTreeCluster = 8;  // CTAs per front in the cluster launch (top levels)

@@ -358,8 +358,8 @@ k_fwd_tree(SnDev sd, TreeDev td, const double* __restrict__ lval, double* w, dou
     // rows of w (final before the launch) and every child's destination rows
     for (int r = row_lo + tid; r < row_hi; r += kThr) T[r] = r < g.k ? __ldcg(w + g.c0 + r) : 0.0;
     const int ch0 = __ldg(sd.ch_ptr + g.s), ch1 = __ldg(sd.ch_ptr + g.s + 1);
-    int gtot = 0;  // entries staged (-1: more than kGMax, gathered directly)
-    for (int cc = ch0; cc < ch1; ++cc) {
+    int gtot = td.stage ? 0 : -1;  // entries staged (-1: more than kGMax, gathered directly)
+    for (int cc = ch0; cc < ch1 && gtot >= 0; ++cc) {
       const int c = __ldg(sd.ch + cc);
       const int rp = __ldg(sd.rel_ptr + c), fu = __ldg(sd.rel_ptr + c + 1) - rp;
       if (gtot + fu > kGMax) {

@@ -1135,7 +1135,7 @@ __device__ __forceinline__ void mid_trsm_steps(int pb, int pe, double (&x)[kWide
 template <int NT>
 __global__ void __launch_bounds__(NT, NT == 128 ? 4 : 1)
 k_mid_front(SnDev sd, FactorDev fd, const double* __restrict__ kval, const int* __restrict__ nodes,
-            double eps) {
+            double eps, int stage) {
   extern __shared__ __align__(16) double dyn_smem[];
   MidSmem& M = *reinterpret_cast<MidSmem*>(dyn_smem);
   double* S = dyn_smem + (sizeof(MidSmem) + 7) / 8;  // the front, packed lower triangle
@@ -1157,7 +1157,7 @@ k_mid_front(SnDev sd, FactorDev fd, const double* __restrict__ kval, const int* 
   for (int i = t; i < ntri; i += NT) S[i] = 0.0;
   if (t == 0) M.sm.prog = 0;
   const int ch0 = sd.ch_ptr[s], nch = sd.ch_ptr[s + 1] - ch0;
-  const bool chpre = nch <= kMidCh;
+  const bool chpre = stage && nch <= kMidCh;  // stage = 0: the per-child path (tests)
   if (chpre && t < nch) {
     const int c = sd.ch[ch0 + t];
     M.chfu[t] = f_minus_k(sd, c);
@@ -1586,7 +1586,7 @@ void launch_front_dag(const SnDev& sd, const FactorDev& fd, const double* kval, 
 int mid_front_limit() { return kMidF; }
 
 void launch_mid_front(const SnDev& sd, const FactorDev& fd, const double* kval, const int* nodes, int count,
-                      int fmax, double eps, cudaStream_t st) {
+                      int fmax, double eps, cudaStream_t st, bool stage) {
   static PerDeviceOnce init;
   init([] {
     int dev = 0, optin = 0;
@@ -1599,9 +1599,9 @@ void launch_mid_front(const SnDev& sd, const FactorDev& fd, const double* kval, 
   const size_t smem = (sizeof(MidSmem) + 7) / 8 * 8 + sizeof(double) * (static_cast<size_t>(fm) * (fm + 1) / 2);
   if (!count) return;
   if (fm <= 128)
-    launch_pdl(k_mid_front<128>, count, 128, smem, st, true, sd, fd, kval, nodes, eps);
+    launch_pdl(k_mid_front<128>, count, 128, smem, st, true, sd, fd, kval, nodes, eps, stage ? 1 : 0);
   else
-    launch_pdl(k_mid_front<256>, count, 256, smem, st, true, sd, fd, kval, nodes, eps);
+    launch_pdl(k_mid_front<256>, count, 256, smem, st, true, sd, fd, kval, nodes, eps, stage ? 1 : 0);
 }
 
 }  // namespace nclb

@@ -2,8 +2,8 @@
 oracle: the tree-dataflow solves (tree_solve.cu; single-CTA and cluster
 launches), the panel kernel with the strip update folded in
 (k_wide_panel_f), the opt-in persistent huge-level kernel, the mid-front
-kernel (single-panel fronts kept in shared memory), and the kernels they
-replace.  Every configuration must reach the oracle's decisions and step
+kernel (single-panel fronts kept in shared memory), the unstaged fallbacks of
+the staged gathers, and the kernels they replace.  Every configuration must reach the oracle's decisions and step
 (same bars as test_gpu_kkt.py) and be bitwise reproducible from one call to
 the next (the second call replays the CUDA graphs).
 
@@ -28,8 +28,12 @@ CONFIGS = {
     "separate-strip": {"NCL_NO_FUSED_PANEL": "1"},
     "persistent-huge": {"NCL_HUGE_LEVEL": "1"},
     "no-mid-fronts": {"NCL_NO_MID": "1"},
+    # the mid-front assembly and the tree forward gather without their staged
+    # row maps (the paths fronts with more children / entries than the staging
+    # buffers hold take)
+    "unstaged-gathers": {"NCL_NO_STAGED_GATHER": "1"},
 }
-SWITCHES = ("NCL_NO_TREE", "NCL_TREE_C", "NCL_NO_FUSED_PANEL", "NCL_HUGE_LEVEL", "NCL_NO_MID")
+SWITCHES = ("NCL_NO_TREE", "NCL_TREE_C", "NCL_NO_FUSED_PANEL", "NCL_HUGE_LEVEL", "NCL_NO_MID", "NCL_NO_STAGED_GATHER")
 
 _cache = {}
 
