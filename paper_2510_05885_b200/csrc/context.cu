@@ -244,14 +244,23 @@ class LdlSystem {
           double* scr = dscr_.p + static_cast<size_t>((g - g0) & 1) * std::max(1, T.max_dg) * (kWidePanel * kWidePanel);
           if (g - 2 >= g0) CK(cudaStreamWaitEvent(st_, ev_rest(g - 2), 0));
           launch_wide_panel_f(sd_, fd, pn_tasks_.p + T.pn_ptr[g], np, g - g0, eps, scr, st_, ptr ? g : -1);
-          CK(cudaEventRecord(ev_panel(g), st_));
-          CK(cudaStreamWaitEvent(st2_, ev_panel(g), 0));
-          launch_wide_update(sd_, fd, tiles_.p + T.tl_ptr[g], nt, dg_nodes_.p + T.dg_ptr[g], nd, g - g0,
-                             st2_, false, scr, ptr ? g : -1);
-          CK(cudaEventRecord(ev_rest(g), st2_));
+          if (g == g1 - 1) {
+            // the level's last rest update (the update matrices the next
+            // level's assembly reads) on the main stream as a programmatic
+            // launch: no launch gap behind the last panel, and the next
+            // assembly's static part overlaps it (factor -16 us on the mesh)
+            if (g - 1 >= g0) CK(cudaStreamWaitEvent(st_, ev_rest(g - 1), 0));
+            launch_wide_update(sd_, fd, tiles_.p + T.tl_ptr[g], nt, dg_nodes_.p + T.dg_ptr[g], nd, g - g0,
+                               st_, true, scr, ptr ? g : -1);
+          } else {
+            CK(cudaEventRecord(ev_panel(g), st_));
+            CK(cudaStreamWaitEvent(st2_, ev_panel(g), 0));
+            launch_wide_update(sd_, fd, tiles_.p + T.tl_ptr[g], nt, dg_nodes_.p + T.dg_ptr[g], nd, g - g0,
+                               st2_, false, scr, ptr ? g : -1);
+            CK(cudaEventRecord(ev_rest(g), st2_));
+          }
           launches_ += (np > 0) + (nt > 0 || nd > 0);
         }
-        if (g1 > g0) CK(cudaStreamWaitEvent(st_, ev_rest(g1 - 1), 0));
         continue;
       }
       for (int g = g0; g < g1; ++g) {
