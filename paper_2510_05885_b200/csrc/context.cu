@@ -166,7 +166,7 @@ class LdlSystem {
         launches_ += 1;
       }
       if (mid_level(l)) {  // a 4-warp CTA per front, the front in shared memory
-        launch_mid_front(sd_, fd, kval, lvl_nodes_.p + T.lvl_ptr[l], T.lvl_ptr[l + 1] - T.lvl_ptr[l],
+        launch_mid_front(sd_, fd, kval, mid_nodes_.p + T.lvl_ptr[l], T.lvl_ptr[l + 1] - T.lvl_ptr[l],
                          lvl_fmax_[l], eps, st_, stage_gather_);
         launches_ += 1;
         continue;
@@ -690,6 +690,14 @@ class LdlSystem {
       poff_.upload(po);
     }
     lvl_nodes_.upload(T.lvl_nodes);
+    {  // mid-front launches: each level's fronts largest first (the last wave
+       // is then the small fronts; fronts of a level are independent)
+      std::vector<int> mn(T.lvl_nodes);
+      for (size_t l = 0; l + 1 < T.lvl_ptr.size(); ++l)
+        std::stable_sort(mn.begin() + T.lvl_ptr[l], mn.begin() + T.lvl_ptr[l + 1],
+                         [&](int a, int b) { return T.f[a] > T.f[b]; });
+      mid_nodes_.upload(mn);
+    }
     std::vector<int8_t> wide(T.wide.begin(), T.wide.end());
     wide_.upload(wide);
     std::vector<int4> at(T.asm_task.size());
@@ -986,11 +994,16 @@ class LdlSystem {
     int fmax = 0, pmax = 0;
     for (int q = T.lvl_ptr[l0]; q < T.lvl_ptr[l1]; ++q) {
       const int s = T.lvl_nodes[q];
-      pos[s] = static_cast<int>(list.size());
       list.push_back(s);
       fmax = std::max(fmax, T.f[s]);
       pmax = std::max(pmax, (T.first[s + 1] - T.first[s] + 31) / 32);
     }
+    // each level's fronts largest first (fronts of a level are independent:
+    // the list stays topological; the teams start on the long fronts)
+    for (int l = l0; l < l1; ++l)
+      std::stable_sort(list.begin() + (T.lvl_ptr[l] - T.lvl_ptr[l0]), list.begin() + (T.lvl_ptr[l + 1] - T.lvl_ptr[l0]),
+                       [&](int a, int b) { return T.f[a] > T.f[b]; });
+    for (size_t i = 0; i < list.size(); ++i) pos[list[i]] = static_cast<int>(i);
     const int teams = tree_teams(C, fmax, pmax);
     if (teams < 1) return false;
     std::vector<int> wptr{0}, wait, par;
@@ -1243,6 +1256,7 @@ class LdlSystem {
   DBuf<longlong2> poff_;
   DBuf<int4> pn_tasks_;
   DBuf<int4> tiles_, tiles_s_;
+  DBuf<int> mid_nodes_;  // lvl_nodes with each level's fronts largest first (mid-front launches)
   cudaStream_t st2_ = nullptr;        // huge-level lookahead stream
   std::vector<cudaEvent_t> evs_;      // per huge panel: panel done, rest done
   cudaEvent_t ev_panel(int g) { return evs_[2 * g]; }
