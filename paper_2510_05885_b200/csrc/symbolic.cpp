@@ -1002,6 +1002,9 @@ Supernodal build_supernodal(const LowerCsc& A, const Symbolic& S, int schur_n0) 
       for (int cb = 0; cb < f; cb += kAsmCols) T.asm_task.push_back({s, cb, 0, 0});
       maxp = std::max(maxp, (k + kWidePanel - 1) / kWidePanel);
     }
+    // the tallest fronts' columns first (more rows per task; tasks are independent)
+    std::stable_sort(T.asm_task.begin() + T.asm_task_ptr.back(), T.asm_task.end(),
+                     [&](const std::array<int, 4>& a, const std::array<int, 4>& b) { return T.f[a[0]] > T.f[b[0]]; });
     T.asm_task_ptr.push_back(static_cast<int>(T.asm_task.size()));
     for (int p = 0; p < maxp; ++p) {
       for (int q = T.lvl_ptr[l]; q < T.lvl_ptr[l + 1]; ++q) {
