@@ -74,6 +74,9 @@ __device__ __forceinline__ unsigned sptr(const void* p) {
 __device__ __forceinline__ void cp16(void* dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sptr(dst)), "l"(src) : "memory");
 }
+__device__ __forceinline__ void cp8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sptr(dst)), "l"(src) : "memory");
+}
 __device__ __forceinline__ void cp4(void* dst, const void* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sptr(dst)), "l"(src) : "memory");
 }
@@ -582,6 +585,22 @@ __device__ __forceinline__ void bwd_load(double (&v)[32], const FrontGeo& g, int
 #pragma unroll
   for (int q = 0; q < 32; ++q) v[q] = (ok && q < nq) ? __ldg(src + q * g.ld) : 0.0;
 }
+// bwd_load's block straight into the warp's transpose buffer Ts (row lane,
+// column q at Ts[lane * kTsSL + q]) by cp.async: no registers held
+__device__ __forceinline__ void bwd_stage_ts(double* Ts, const FrontGeo& g, int R, int b, int lane) {
+  const int r0 = rb_start(g.k, g.P, R), nr = rb_size(g.k, g.f, g.P, R);
+  const int q0 = 32 * b, nq = min(32, g.k - q0);
+  const double* src = g.L + r0 + lane + static_cast<size_t>(q0) * g.ld;
+  const bool ok = lane < nr;
+#pragma unroll 8
+  for (int q = 0; q < 32; ++q) {
+    if (ok && q < nq)
+      cp8(Ts + lane * kTsSL + q, src + q * g.ld);
+    else
+      Ts[lane * kTsSL + q] = 0.0;
+  }
+  cp_commit();
+}
 __device__ __forceinline__ void red_rel_cta(int* p, int v) {
   asm volatile("red.release.cta.shared::cta.add.s32 [%0], %1;" ::"r"(sptr(p)), "r"(v) : "memory");
 }
@@ -603,6 +622,7 @@ __device__ __forceinline__ void bwd_apply(const double (&v)[32], const FrontGeo&
                                           const BwdRemote& rm, int lane) {
   if (R < g.P) wait_ge(&sm.xdone, g.P - R);
   const int r0 = rb_start(g.k, g.P, R), nr = rb_size(g.k, g.f, g.P, R);
+  __syncwarp();  // every lane's reads of the previous item's Ts are done
 #pragma unroll
   for (int q = 0; q < 32; ++q) Ts[lane * kTsSL + q] = v[q];
   __syncwarp();
@@ -628,6 +648,8 @@ __device__ __forceinline__ void bwd_apply(const double (&v)[32], const FrontGeo&
   if (lane == 0) red_rel_cl(rm.cnt0 + b, 1);
 }
 
+// the warp's first item was staged into Ts before the parent was awaited
+// (k_bwd_tree: L is static); the later ones go through registers, one ahead
 template <bool REMOTE>
 __device__ __forceinline__ void bwd_bulk(const FrontGeo& g, int wb, const double* X, double* accw,
                                          BwdSmem& sm, bool ph2, const BwdRemote& rm) {
@@ -637,7 +659,10 @@ __device__ __forceinline__ void bwd_bulk(const FrontGeo& g, int wb, const double
   if (!bwd_first(g, wb, it, ph2)) return;
   double* Ts = sm.Ts[wb];
   double A[32], B[32];
-  bwd_load(A, g, it.R, it.b, lane);
+  cp_wait<0>();  // the first item's block, staged into Ts before the parent was awaited
+  __syncwarp();
+#pragma unroll
+  for (int q = 0; q < 32; ++q) A[q] = Ts[lane * kTsSL + q];
   for (;;) {
     BwdIt nx = it;
     const bool hb = bwd_next(g, wb, nx, ph2);
@@ -718,6 +743,13 @@ k_bwd_tree(SnDev sd, TreeDev td, const double* __restrict__ lval, const double* 
     // z_q = w_q / d_q for the pivots (the forward result, final)
     if (rank == 0)
       for (int q = tid; q < g.k; q += kThr) X[q] = __ldg(w + g.c0 + q) / __ldg(d + g.c0 + q);
+    // the bulk warps' first item (static L) into their transpose buffers
+    // before the parent is awaited: the other ranks' first partials are what
+    // rank 0's chain waits for at every front
+    if (warp > 0) {
+      BwdIt it0;
+      if (bwd_first(g, warp - 1, it0, rank == 0)) bwd_stage_ts(sm.Ts[warp - 1], g, it0.R, it0.b, lane);
+    }
     // the x positions of this CTA's update rows: static, staged before the
     // parent is awaited (cold index loads off the critical path)
     const int ur0 = g.rhi > g.rlo ? rb_start(g.k, g.P, g.rlo) : 0;
