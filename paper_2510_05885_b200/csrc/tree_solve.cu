@@ -178,6 +178,7 @@ __device__ __forceinline__ FrontGeo front_geo(const SnDev& sd, const double* lva
 constexpr int kGMax = 2048;  // children's update entries staged for a front's gather
 struct FwdSmem {
   double head[kStages][32 * kHeadSL];  // rows [32b, 32b+64) x the 32 columns of block b
+  double first[kBulk][32 * 33];        // per bulk warp: its first item's L block, row-major (staged)
   int grel[kGMax];                     // gather: the children's entries in child order --
   int gsrc[kGMax];                     //   destination row, update-vector offset
   int xdone;                           // pivot blocks solved
@@ -291,16 +292,42 @@ __device__ __forceinline__ void fwd_apply(const double (&v)[32], const FrontGeo&
   if (!REMOTE && lane == 0 && R < g.P) st_rel_cta(&cnt[R], c + 1);
 }
 
+// the first item of bulk warp wb: (c, R) and whether there is one
+__device__ __forceinline__ bool fwd_first(const FrontGeo& g, int wb, int& c, int& R) {
+  c = 0;
+  R = g.rlo + wb;
+  if (R >= g.rhi || g.P == 0) return false;
+  return fwd_valid(g, c, R) || fwd_next(g, wb, c, R);
+}
+// fwd_load's block into a row-major staging block (row lane at S[lane * 33])
+// by cp.async: issued before the children are awaited (L is static)
+__device__ __forceinline__ void fwd_stage_first(double* S, const FrontGeo& g, int c, int R, int lane) {
+  const int r0 = rb_start(g.k, g.P, R), nr = rb_size(g.k, g.f, g.P, R);
+  const int q0 = 32 * c, nq = min(32, g.k - q0);
+  const double* src = g.L + r0 + lane + static_cast<size_t>(q0) * g.ld;
+  const bool ok = lane < nr;
+#pragma unroll 8
+  for (int q = 0; q < 32; ++q) {
+    if (ok && q < nq)
+      cp8(S + lane * 33 + q, src + q * g.ld);
+    else
+      S[lane * 33 + q] = 0.0;
+  }
+  cp_commit();
+}
+
 template <bool REMOTE>
 __device__ __forceinline__ void fwd_bulk(const FrontGeo& g, int wb, double* T, const double* X0,
-                                         const int* xd0, int* cnt) {
+                                         const int* xd0, int* cnt, const double* first) {
   const int lane = threadIdx.x & 31;
   __syncwarp();  // the warp enters converged (the CTA's tid-0 branches)
-  int c = 0, R = g.rlo + wb;
-  if (R >= g.rhi || g.P == 0) return;
-  if (!fwd_valid(g, c, R) && !fwd_next(g, wb, c, R)) return;
+  int c, R;
+  if (!fwd_first(g, wb, c, R)) return;
   double A[32], B[32];
-  fwd_load(A, g, c, R, lane);
+  cp_wait<0>();  // the first item's block, staged before the children were awaited
+  __syncwarp();
+#pragma unroll
+  for (int q = 0; q < 32; ++q) A[q] = first[lane * 33 + q];
   for (;;) {
     int cb = c, Rb = R;
     const bool hb = fwd_next(g, wb, cb, Rb);
@@ -376,6 +403,10 @@ k_fwd_tree(SnDev sd, TreeDev td, const double* __restrict__ lval, double* w, dou
       gtot += fu;
     }
     cp_commit();
+    if (warp > 0) {  // the bulk warps' first L blocks (static), before the children are awaited
+      int c1, R1;
+      if (fwd_first(g, warp - 1, c1, R1)) fwd_stage_first(sm.first[warp - 1], g, c1, R1, lane);
+    }
     if (C > 1) cl.sync();  // rank 0's progress is reset before any rank reads it
     // children's update vectors: wide children in the list publish flags
     if (warp == 1) {
@@ -427,9 +458,9 @@ k_fwd_tree(SnDev sd, TreeDev td, const double* __restrict__ lval, double* w, dou
       if (warp == 0)
         fwd_chain(g, T, sm);
       else
-        fwd_bulk<false>(g, warp - 1, T, T, &sm.xdone, sm.cnt);
+        fwd_bulk<false>(g, warp - 1, T, T, &sm.xdone, sm.cnt, sm.first[warp - 1]);
     } else if (warp > 0) {
-      fwd_bulk<true>(g, warp - 1, T, T0, xd0, sm.cnt);
+      fwd_bulk<true>(g, warp - 1, T, T0, xd0, sm.cnt, sm.first[warp - 1]);
     }
     __syncthreads();
     if (tr) t3 = gtime();
