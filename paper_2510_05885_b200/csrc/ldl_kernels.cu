@@ -125,6 +125,10 @@ __device__ __forceinline__ void warp_pivots(double (&fr)[kWF + 1], double* F, do
     const double u = fr[0];
     double* cbp = cb + (p & 1) * kCB;
     if (lane >= p) cbp[lane - p] = u;
+    // row p+1's entry in column p+1, shuffled while 1/d is formed: with
+    // u(p+1) from the broadcast column every lane forms the next pivot itself
+    // (row p+1's own operations: the same value) -- no shuffle on the chain
+    const double a11 = __shfl_sync(0xffffffffu, fr[1], (p + 1) & 31);
     const double r = rcp_nr(dp);
     const double l = mine ? u * r : 0.0;
     if (mine) F[p * kFLD + lane] = l;
@@ -137,9 +141,10 @@ __device__ __forceinline__ void warp_pivots(double (&fr)[kWF + 1], double* F, do
       double2 v[B / 2];  // issued before the dependent chain of the batch
 #pragma unroll
       for (int j = 0; j < B; j += 2) v[j / 2] = *reinterpret_cast<const double2*>(cbp + j0 + j);
-      if (j0 == 0) {  // the next pivot's column first, then its diagonal out
+      if (j0 == 0) {  // the next pivot's column first
         fr[0] = fr[1] - l * v[0].y;
-        dnext = __shfl_sync(0xffffffffu, fr[0], (p + 1) & 31);
+        const double u1 = v[0].y;  // u of row p+1 (0 past the front)
+        dnext = (p + 1 < f) ? a11 - ((u1 * r) * u1) : fr[0];
       }
 #pragma unroll
       for (int j = (j0 == 0 ? 2 : 0); j < B; j += 2) {
