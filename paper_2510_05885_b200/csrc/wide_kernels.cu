@@ -817,19 +817,29 @@ struct PanelTaskSmem {  // cp.async destinations 16-byte aligned
 };
 static_assert(offsetof(PanelTaskSmem, D) % 16 == 0 && offsetof(PanelTaskSmem, TR) % 16 == 0 &&
                   offsetof(PanelTaskSmem, A) % 16 == 0, "PanelTaskSmem alignment");
+// a front's static geometry (loaded before the programmatic wait: after it
+// the panel's first loads are the staging of its blocks, one round trip)
+struct PanelGeo {
+  int c0, k, f;
+  long long loff;
+};
+__device__ __forceinline__ PanelGeo panel_geo(const SnDev& sd, int s) {
+  const int c0 = sd.first[s];
+  return PanelGeo{c0, sd.first[s + 1] - c0, sd.f[s], sd.l_off[s]};
+}
 __device__ __forceinline__ void panel_task(const SnDev& sd, const FactorDev& fd, int4 task, int panel,
-                                           double eps, double* scr_base, PanelTaskSmem& P,
+                                           double eps, double* scr_base, PanelTaskSmem& P, const PanelGeo& geo,
                                            long long* stamp = nullptr, int gtr = -1) {
   PanelSmem& sm = P.sm;
   double* D = P.D;
   double* TR = P.TR;
   double* A = P.A;
   double* dv = P.dv;
-  const int s = task.x, rb = task.y;
-  const int c0 = sd.first[s], k = sd.first[s + 1] - c0, f = sd.f[s];
+  const int rb = task.y;
+  const int c0 = geo.c0, k = geo.k, f = geo.f;
   const size_t ld = wide_ld(f);
   const int p0 = panel * kWidePanel, p1 = min(p0 + kWidePanel, k), nb = p1 - p0;
-  double* F = fd.lval + sd.l_off[s];
+  double* F = fd.lval + geo.loff;
   const int lo = p1 + rb * kPanelRows, hi = min(f, lo + kPanelRows);
   const int nrow = max(0, hi - lo);
   const int t = threadIdx.x;
@@ -903,11 +913,12 @@ k_wide_panel_f(SnDev sd, FactorDev fd, const int4* __restrict__ tasks, int panel
   extern __shared__ __align__(16) double dyn_smem[];
   PanelTaskSmem& P = *reinterpret_cast<PanelTaskSmem*>(dyn_smem);
   const int4 task = tasks[blockIdx.x];
+  const PanelGeo geo = panel_geo(sd, task.x);  // static: before the wait
   if (threadIdx.x == 0) ptrace_max(gtr, 0);
   pdl_launch_dependents();
   pdl_wait();  // the previous panel (programmatic launch)
   if (threadIdx.x == 0) ptrace_max(gtr, 1);
-  panel_task(sd, fd, task, panel, eps, scr_base, P, nullptr, gtr);
+  panel_task(sd, fd, task, panel, eps, scr_base, P, geo, nullptr, gtr);
   if (threadIdx.x == 0) ptrace_max(gtr, 5);
 }
 
@@ -961,7 +972,8 @@ k_huge_level(SnDev sd, FactorDev fd, HugeDev h, double eps) {
         __syncthreads();
         long long* stamp = h.trace ? h.trace + 5 * static_cast<size_t>(h.pn_ptr[g] + j) : nullptr;
         if (stamp && t == 0) stamp[4] = clock64();
-        panel_task(sd, fd, h.pn[h.pn_ptr[g] + j], gi, eps, scr, P, stamp);
+        const int4 task = h.pn[h.pn_ptr[g] + j];
+        panel_task(sd, fd, task, gi, eps, scr, P, panel_geo(sd, task.x), stamp);
         if (stamp && t == 0) stamp[3] = clock64();
         huge_done(h.pc + g);
       }
