@@ -1381,12 +1381,12 @@ class KktSystem {
     std::fill(std::begin(ms_), std::end(ms_) - 1, 0.0);
     Scalars* ds = ldl_->dev_scalars();
     Scalars* hs = ldl_->host_scalars();
-    CK(cudaMemsetAsync(&ds->hmax, 0, sizeof(double), st_));
-    launch_absmax2(static_cast<int>(hval_.n), hv, P_.n, sg, &ds->hmax, st_);
+    // max(|H|, |sigma|) is only read for the first delta after a rejected
+    // unregularised attempt without a warm start (kkt.cpp:273-313): computed
+    // then, not on every call
     double delta = 0.0;
     bool first = true;
     const int* tgt = P_.inertia_target;
-    launches_ += 1;
     for (;;) {
       st->factor_attempts++;
       const int e0 = tick();
@@ -1443,7 +1443,16 @@ class KktSystem {
         }
       }
       if (first) {
-        delta = warm > 0.0 ? std::max(1e-20, warm / 3.0) : 1e-8 * std::max(1.0, hs->hmax);
+        if (warm > 0.0) {
+          delta = std::max(1e-20, warm / 3.0);
+        } else {
+          CK(cudaMemsetAsync(&ds->hmax, 0, sizeof(double), st_));
+          launch_absmax2(static_cast<int>(hval_.n), hv, P_.n, sg, &ds->hmax, st_);
+          launches_ += 1;
+          CK(cudaMemcpyAsync(&hs->hmax, &ds->hmax, sizeof(double), cudaMemcpyDeviceToHost, st_));
+          CK(cudaStreamSynchronize(st_));
+          delta = 1e-8 * std::max(1.0, hs->hmax);
+        }
         first = false;
       } else {
         delta *= 8.0;
