@@ -1428,10 +1428,8 @@ class KktSystem {
           launch_recover(P_, jp_ptr_.p, jp_idx_.p, jv, sol_.p, v_.p, rs_.p, pk_.p, r2, rho,
                          delta, dx, dr, dy, st_);
           CK(cudaMemsetAsync(&ds->nonfinite, 0, sizeof(int), st_));
-          launch_nonfinite(P_.n, dx, &ds->nonfinite, st_);
-          launch_nonfinite(P_.m, dr, &ds->nonfinite, st_);
-          launch_nonfinite(P_.m, dy, &ds->nonfinite, st_);
-          launches_ += 4;
+          launch_nonfinite3(P_.n, dx, P_.m, dr, dy, &ds->nonfinite, st_);
+          launches_ += 2;
           CK(cudaMemcpyAsync(&hs->nonfinite, &ds->nonfinite, sizeof(int),
                              cudaMemcpyDeviceToHost, st_));
           const int e6 = tick();

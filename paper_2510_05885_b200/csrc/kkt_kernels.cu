@@ -263,6 +263,17 @@ __global__ void k_nonfinite(int n, const double* __restrict__ a, int* flag) {
       return;
     }
 }
+// the step's three outputs (dx[n], dr[m], dy[m]) in one pass
+__global__ void k_nonfinite3(int n, const double* __restrict__ a, int m, const double* __restrict__ b,
+                             const double* __restrict__ c, int* flag) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n + 2 * m; i += gridDim.x * blockDim.x) {
+    const double v = i < n ? a[i] : (i < n + m ? b[i - n] : c[i - n - m]);
+    if (!isfinite(v)) {
+      atomicOr(flag, 1);
+      return;
+    }
+  }
+}
 
 // ---- refinement pieces --------------------------------------------------------
 // r = b - A x over the full symmetric row pattern; norm = max |r_i| (NaN
@@ -401,6 +412,14 @@ void launch_nonfinite(int n, const double* a, int* flag, cudaStream_t st) {
   int g = nb(n);
   if (g > 1184) g = 1184;
   k_nonfinite<<<g, 256, 0, st>>>(n, a, flag);
+}
+
+void launch_nonfinite3(int n, const double* a, int m, const double* b, const double* c, int* flag,
+                       cudaStream_t st) {
+  if (n + 2 * m <= 0) return;
+  int g = nb(n + 2 * m);
+  if (g > 1184) g = 1184;
+  k_nonfinite3<<<g, 256, 0, st>>>(n, a, m, b, c, flag);
 }
 
 void launch_residual(int N, const int* fr_ptr, const int* fr_col, const int* fr_slot,

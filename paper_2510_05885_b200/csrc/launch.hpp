@@ -163,6 +163,9 @@ void launch_recover(const KktPlan& P, const int* jp_ptr, const int* jp_idx,
                     const double* rs, const double* pk, const double* r2, double rho,
                     double delta, double* dx, double* dr, double* dy, cudaStream_t st);
 void launch_nonfinite(int n, const double* a, int* flag, cudaStream_t st);
+// dx[n], dr[m], dy[m] in one pass
+void launch_nonfinite3(int n, const double* a, int m, const double* b, const double* c, int* flag,
+                       cudaStream_t st);
 void launch_residual(int N, const int* fr_ptr, const int* fr_col, const int* fr_slot,
                      const double* kval, const double* x, const double* b, double* r,
                      double* norm, const int* long_rows, int nlong_rows, cudaStream_t st);
