@@ -240,7 +240,20 @@ class LdlSystem {
         for (int g = g0; g < g1; ++g) {
           const int nd = T.dg_ptr[g + 1] - T.dg_ptr[g];
           const int np = T.pn_ptr[g + 1] - T.pn_ptr[g];
-          const int nt = T.tl_ptr[g + 1] - T.tl_ptr[g];
+          // 64x64 tiles where the update is latency-bound (about one wave of
+          // 32x32 tile CTAs or less: the mesh, -12 us); the 32x32 kernel's
+          // parallelism where it is throughput-bound (elec's 3000-row front:
+          // 64x64 tiles were 0.8 ms slower per Newton step)
+          const bool t64 = use_t64_ && T.tl_ptr[g + 1] - T.tl_ptr[g] <= kT64MaxTiles;
+          const int nt = t64 ? T.tl64_ptr[g + 1] - T.tl64_ptr[g] : T.tl_ptr[g + 1] - T.tl_ptr[g];
+          auto rest = [&](cudaStream_t s2, bool pdl, double* sc) {
+            if (t64)
+              launch_wide_update64(sd_, fd, tiles64_.p + T.tl64_ptr[g], nt, dg_nodes_.p + T.dg_ptr[g], nd, g - g0,
+                                   s2, pdl, sc);
+            else
+              launch_wide_update(sd_, fd, tiles_.p + T.tl_ptr[g], nt, dg_nodes_.p + T.dg_ptr[g], nd, g - g0, s2,
+                                 pdl, sc, ptrace_.p ? g : -1);
+          };
           double* scr = dscr_.p + static_cast<size_t>((g - g0) & 1) * std::max(1, T.max_dg) * (kWidePanel * kWidePanel);
           if (g - 2 >= g0) CK(cudaStreamWaitEvent(st_, ev_rest(g - 2), 0));
           launch_wide_panel_f(sd_, fd, pn_tasks_.p + T.pn_ptr[g], np, g - g0, eps, scr, st_, ptr ? g : -1);
@@ -250,13 +263,11 @@ class LdlSystem {
             // launch: no launch gap behind the last panel, and the next
             // assembly's static part overlaps it (factor -16 us on the mesh)
             if (g - 1 >= g0) CK(cudaStreamWaitEvent(st_, ev_rest(g - 1), 0));
-            launch_wide_update(sd_, fd, tiles_.p + T.tl_ptr[g], nt, dg_nodes_.p + T.dg_ptr[g], nd, g - g0,
-                               st_, true, scr, ptr ? g : -1);
+            rest(st_, true, scr);
           } else {
             CK(cudaEventRecord(ev_panel(g), st_));
             CK(cudaStreamWaitEvent(st2_, ev_panel(g), 0));
-            launch_wide_update(sd_, fd, tiles_.p + T.tl_ptr[g], nt, dg_nodes_.p + T.dg_ptr[g], nd, g - g0,
-                               st2_, false, scr, ptr ? g : -1);
+            rest(st2_, false, scr);
             CK(cudaEventRecord(ev_rest(g), st2_));
           }
           launches_ += (np > 0) + (nt > 0 || nd > 0);
@@ -736,6 +747,12 @@ class LdlSystem {
     for (size_t i = 0; i < tl.size(); ++i)
       tl[i] = make_int4(T.tiles[i][0], T.tiles[i][1], T.tiles[i][2], T.tiles[i][3]);
     tiles_.upload(tl);
+    {
+      std::vector<int4> t64(T.tiles64.size());
+      for (size_t i = 0; i < t64.size(); ++i)
+        t64[i] = make_int4(T.tiles64[i][0], T.tiles64[i][1], T.tiles64[i][2], T.tiles64[i][3]);
+      tiles64_.upload(t64);
+    }
     // per level: cluster size of the fused launch, or 0 = huge-front path
     int sms = 148;
     {
@@ -1222,6 +1239,9 @@ class LdlSystem {
   bool use_graph_ = std::getenv("NCL_NO_GRAPH") == nullptr;
   // huge levels: strip update folded into the panel kernel (NCL_NO_FUSED_PANEL=1: separate launch)
   bool fused_panel_ = std::getenv("NCL_NO_FUSED_PANEL") == nullptr;
+  // the fused path's rest updates as 64x64 tiles (NCL_UPD32=1: 32x32, k_wide_update)
+  bool use_t64_ = std::getenv("NCL_UPD32") == nullptr;
+  static constexpr int kT64MaxTiles = 1036;  // 32x32 tiles: 7 CTAs per SM x 148
   // NCL_NO_STAGED_GATHER=1 (tests): the mid-front assembly and the tree forward
   // gather take their unstaged fallback paths (more children / entries than
   // the staging buffers hold)
@@ -1256,6 +1276,7 @@ class LdlSystem {
   DBuf<longlong2> poff_;
   DBuf<int4> pn_tasks_;
   DBuf<int4> tiles_, tiles_s_;
+  DBuf<int4> tiles64_;  // the fused path's rest updates, 64x64 tiles
   DBuf<int> mid_nodes_;  // lvl_nodes with each level's fronts largest first (mid-front launches)
   cudaStream_t st2_ = nullptr;        // huge-level lookahead stream
   std::vector<cudaEvent_t> evs_;      // per huge panel: panel done, rest done

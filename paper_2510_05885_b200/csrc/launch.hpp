@@ -58,6 +58,9 @@ void launch_wide_panel(const SnDev& sd, const FactorDev& fd, const int4* tasks, 
 void launch_wide_update(const SnDev& sd, const FactorDev& fd, const int4* tiles, int count,
                         const int* fronts, int nd, int panel, cudaStream_t st, bool pdl,
                         const double* scr = nullptr, int gtr = -1);
+// the fused path's rest updates as 64x64 tiles (symbolic tiles64)
+void launch_wide_update64(const SnDev& sd, const FactorDev& fd, const int4* tiles, int count,
+                          const int* fronts, int nd, int panel, cudaStream_t st, bool pdl, const double* scr);
 // a huge level's panels and trailing updates as one persistent launch
 // (wide_kernels.cu k_huge_level): global panels [g0, g1) of the schedule
 struct HugeDev {

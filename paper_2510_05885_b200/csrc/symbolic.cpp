@@ -990,6 +990,7 @@ Supernodal build_supernodal(const LowerCsc& A, const Symbolic& S, int schur_n0) 
   T.lp_ptr.assign(static_cast<size_t>(nlev) + 1, 0);
   T.pn_ptr.assign(1, 0);
   T.tl_ptr.assign(1, 0);
+  T.tl64_ptr.assign(1, 0);
   T.ts_ptr.assign(1, 0);
   T.dg_ptr.assign(1, 0);
   for (int l = 0; l < nlev; ++l) {
@@ -1023,10 +1024,16 @@ Supernodal build_supernodal(const LowerCsc& A, const Symbolic& S, int schur_n0) 
         for (int ti = 0; ti < nt; ++ti)
           for (int tj = 0; tj <= ti; ++tj)
             (more && tj == 0 ? T.tiles_s : T.tiles).push_back({s, p1 + ti * kUpdTile, p1 + tj * kUpdTile, p});
+        {  // the rest region (columns from p1, or p1 + 32 when the next panel takes that strip) in 64x64 tiles
+          const int c0 = p1 + (more ? kUpdTile : 0);
+          for (int q0 = c0; q0 < f; q0 += 2 * kUpdTile)
+            for (int r0 = q0; r0 < f; r0 += 2 * kUpdTile) T.tiles64.push_back({s, r0, q0, p});
+        }
         T.wide_update_flops += 2LL * (p1 - p * kWidePanel) * mt * (mt + 1) / 2;
       }
       T.pn_ptr.push_back(static_cast<int>(T.pn_tasks.size()));
       T.tl_ptr.push_back(static_cast<int>(T.tiles.size()));
+      T.tl64_ptr.push_back(static_cast<int>(T.tiles64.size()));
       T.ts_ptr.push_back(static_cast<int>(T.tiles_s.size()));
       T.dg_ptr.push_back(static_cast<int>(T.dg_nodes.size()));
       T.max_dg = std::max(T.max_dg, T.dg_ptr.back() - T.dg_ptr[T.dg_ptr.size() - 2]);

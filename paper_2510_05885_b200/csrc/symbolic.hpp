@@ -121,6 +121,10 @@ struct Supernodal {
   // tiles_s[ts_ptr[g]..], the rest tiles[tl_ptr[g]..]
   std::vector<std::array<int, 4>> tiles_s;
   std::vector<int> asm_task_ptr, lp_ptr, pn_ptr, tl_ptr, ts_ptr, dg_ptr;
+  // the same rest updates as 64x64 tiles {front, row0, col0, panel} for the
+  // fused path's k_wide_update64: tiles64[tl64_ptr[g]..]
+  std::vector<std::array<int, 4>> tiles64;
+  std::vector<int> tl64_ptr;
   int max_dg = 0;  // most fronts in one huge panel launch
   std::vector<std::array<int, 4>> tiles;
   long long wide_update_flops = 0;

@@ -1057,6 +1057,86 @@ k_wide_update(SnDev sd, FactorDev fd, const int4* __restrict__ tiles, int count,
 }
 
 // ---------------------------------------------------------------------------
+// The rest update as 64x64 tiles (fused path): one 8-warp CTA per tile, warp w
+// rows 8w..8w+8 x all 64 columns; A and B (the panel's L rows of the tile's
+// row and column blocks) are staged once for what four 32x32 tiles stage
+// twice each.  Per element the same DMMA sequence as tile_mma_store (k in
+// chunks of four, accumulated, then subtracted from C): bitwise the same.
+constexpr int kT64 = 2 * kUpdTile;
+constexpr int kSL64 = 72;  // column stride of a staged 64-row block (66 rows with the shift)
+struct Group64Smem {
+  double A[kWidePanel * kSL64], B[kWidePanel * kSL64], C[kT64 * kSL64];
+  double d[kWidePanel];
+};
+static_assert(offsetof(Group64Smem, B) % 16 == 0 && offsetof(Group64Smem, C) % 16 == 0, "Group64Smem alignment");
+__global__ void __launch_bounds__(256)
+k_wide_update64(SnDev sd, FactorDev fd, const int4* __restrict__ tiles, int count,
+                const int* __restrict__ fronts, int nd, int panel, const double* scr_base) {
+  extern __shared__ __align__(16) double g64_smem[];
+  Group64Smem& G = *reinterpret_cast<Group64Smem*>(g64_smem);
+  pdl_launch_dependents();
+  pdl_wait();  // the panel kernel
+  const int tid = threadIdx.x;
+  if (blockIdx.x == 0) {  // the panel's L11 blocks from the scratch slots (as k_wide_update)
+    for (int di = 0; di < nd; ++di) {
+      const int s = fronts[di];
+      const int c0 = sd.first[s], k = sd.first[s + 1] - c0, f = sd.f[s];
+      const size_t ld = wide_ld(f);
+      const int p0 = panel * kWidePanel, nb = min(p0 + kWidePanel, k) - p0;
+      const double* scr = scr_base + static_cast<size_t>(di) * (kWidePanel * kWidePanel);
+      double* F = fd.lval + sd.l_off[s];
+      for (int idx = tid; idx < kWidePanel * kWidePanel; idx += blockDim.x) {
+        const int i = idx / kWidePanel, p = idx % kWidePanel;
+        if (i > p && i < nb) F[(p0 + i) + (p0 + p) * ld] = scr[idx];
+      }
+    }
+  }
+  if (static_cast<int>(blockIdx.x) >= count) return;
+  const int4 t = tiles[blockIdx.x];
+  const int s = t.x, r0 = t.y, q0 = t.z;
+  const int c0 = sd.first[s], k = sd.first[s + 1] - c0, f = sd.f[s];
+  const size_t ld = wide_ld(f);
+  const int p0 = t.w * kWidePanel, nb = min(p0 + kWidePanel, k) - p0;
+  const int nr = min(kT64, f - r0), nc = min(kT64, f - q0);
+  const bool dg = r0 == q0;
+  double* F = fd.lval + sd.l_off[s];
+  constexpr int NR2 = (kT64 + 2) / 2;
+  const int shA = stage_block<NR2>(G.A, kSL64, F, ld, r0, p0, nb, tid, 256);
+  const int shB = dg ? shA : stage_block<NR2>(G.B, kSL64, F, ld, q0, p0, nb, tid, 256);
+  const int shC = stage_block<NR2>(G.C, kSL64, F, ld, r0, q0, nc, tid, 256);
+  if (tid < nb) G.d[tid] = __ldcg(fd.d + c0 + p0 + tid);
+  cp_wait_all();
+  __syncthreads();
+  const double* Bs = dg ? G.A : G.B;
+  const int lane = tid & 31, g = lane >> 2, tq = lane & 3;
+  const int rr = (tid >> 5) * 8 + g;
+  double acc[8][2];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) acc[j][0] = acc[j][1] = 0.0;
+#pragma unroll
+  for (int kk = 0; kk < kWidePanel / 4; ++kk) {
+    const int q = kk * 4 + tq;
+    const bool qv = q < nb;
+    const double a = (qv && rr < nr) ? G.A[q * kSL64 + rr + shA] : 0.0;
+    const double dq = qv ? G.d[q] : 0.0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int cc = j * 8 + g;
+      const double b = (qv && cc < nc) ? Bs[q * kSL64 + cc + shB] * dq : 0.0;
+      dmma_m8n8k4(acc[j][0], acc[j][1], a, b);
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < 8; ++j)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int c = j * 8 + tq * 2 + e;
+      if (rr < nr && c < nc && r0 + rr >= q0 + c)
+        F[(r0 + rr) + static_cast<size_t>(q0 + c) * ld] = G.C[c * kSL64 + rr + shC] - acc[j][e];
+    }
+}
+
+// ---------------------------------------------------------------------------
 // Mid fronts: levels whose fronts all have at most kMidF rows and a single
 // panel (k <= 32) -- on the 78k-bus mesh the 3,100 fronts of levels 0-4.
 // k_wide_front gives such a front a 512-thread cluster CTA (one per SM) that
@@ -1398,6 +1478,16 @@ void launch_wide_update(const SnDev& sd, const FactorDev& fd, const int4* tiles,
   if (blocks)
     launch_pdl(k_wide_update, blocks, 128, 0, st, pdl, sd, fd, tiles, count, fronts, nd, panel,
                scr ? scr : static_cast<const double*>(fd.dscr), gtr);
+}
+
+void launch_wide_update64(const SnDev& sd, const FactorDev& fd, const int4* tiles, int count,
+                          const int* fronts, int nd, int panel, cudaStream_t st, bool pdl, const double* scr) {
+  static PerDeviceOnce init;
+  constexpr int bytes = static_cast<int>(sizeof(Group64Smem));
+  init([] { cudaFuncSetAttribute(k_wide_update64, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes); });
+  const int blocks = count > 0 ? count : (nd > 0 ? 1 : 0);
+  if (blocks)
+    launch_pdl(k_wide_update64, blocks, 256, bytes, st, pdl, sd, fd, tiles, count, fronts, nd, panel, scr);
 }
 
 void launch_wide_panel_f(const SnDev& sd, const FactorDev& fd, const int4* tasks, int count, int panel,
