@@ -1057,8 +1057,8 @@ k_wide_update(SnDev sd, FactorDev fd, const int4* __restrict__ tiles, int count,
 }
 
 // ---------------------------------------------------------------------------
-// The rest update as 64x64 tiles (fused path): one 8-warp CTA per tile, warp w
-// rows 8w..8w+8 x all 64 columns; A and B (the panel's L rows of the tile's
+// The rest update as 64x64 tiles (fused path): one 16-warp CTA per tile, warp
+// w rows 8(w mod 8).. x one 32-column half; A and B (the panel's L rows of the tile's
 // row and column blocks) are staged once for what four 32x32 tiles stage
 // twice each.  Per element the same DMMA sequence as tile_mma_store (k in
 // chunks of four, accumulated, then subtracted from C): bitwise the same.
@@ -1069,7 +1069,7 @@ struct Group64Smem {
   double d[kWidePanel];
 };
 static_assert(offsetof(Group64Smem, B) % 16 == 0 && offsetof(Group64Smem, C) % 16 == 0, "Group64Smem alignment");
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(512)
 k_wide_update64(SnDev sd, FactorDev fd, const int4* __restrict__ tiles, int count,
                 const int* __restrict__ fronts, int nd, int panel, const double* scr_base) {
   extern __shared__ __align__(16) double g64_smem[];
@@ -1101,18 +1101,18 @@ k_wide_update64(SnDev sd, FactorDev fd, const int4* __restrict__ tiles, int coun
   const bool dg = r0 == q0;
   double* F = fd.lval + sd.l_off[s];
   constexpr int NR2 = (kT64 + 2) / 2;
-  const int shA = stage_block<NR2>(G.A, kSL64, F, ld, r0, p0, nb, tid, 256);
-  const int shB = dg ? shA : stage_block<NR2>(G.B, kSL64, F, ld, q0, p0, nb, tid, 256);
-  const int shC = stage_block<NR2>(G.C, kSL64, F, ld, r0, q0, nc, tid, 256);
+  const int shA = stage_block<NR2>(G.A, kSL64, F, ld, r0, p0, nb, tid, 512);
+  const int shB = dg ? shA : stage_block<NR2>(G.B, kSL64, F, ld, q0, p0, nb, tid, 512);
+  const int shC = stage_block<NR2>(G.C, kSL64, F, ld, r0, q0, nc, tid, 512);
   if (tid < nb) G.d[tid] = __ldcg(fd.d + c0 + p0 + tid);
   cp_wait_all();
   __syncthreads();
   const double* Bs = dg ? G.A : G.B;
-  const int lane = tid & 31, g = lane >> 2, tq = lane & 3;
-  const int rr = (tid >> 5) * 8 + g;
-  double acc[8][2];
+  const int lane = tid & 31, g = lane >> 2, tq = lane & 3, w = tid >> 5;
+  const int rr = (w & 7) * 8 + g, ch = (w >> 3) * 32;  // warp: 8 rows x one 32-column half
+  double acc[4][2];
 #pragma unroll
-  for (int j = 0; j < 8; ++j) acc[j][0] = acc[j][1] = 0.0;
+  for (int j = 0; j < 4; ++j) acc[j][0] = acc[j][1] = 0.0;
 #pragma unroll
   for (int kk = 0; kk < kWidePanel / 4; ++kk) {
     const int q = kk * 4 + tq;
@@ -1120,17 +1120,17 @@ k_wide_update64(SnDev sd, FactorDev fd, const int4* __restrict__ tiles, int coun
     const double a = (qv && rr < nr) ? G.A[q * kSL64 + rr + shA] : 0.0;
     const double dq = qv ? G.d[q] : 0.0;
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const int cc = j * 8 + g;
+    for (int j = 0; j < 4; ++j) {
+      const int cc = ch + j * 8 + g;
       const double b = (qv && cc < nc) ? Bs[q * kSL64 + cc + shB] * dq : 0.0;
       dmma_m8n8k4(acc[j][0], acc[j][1], a, b);
     }
   }
 #pragma unroll
-  for (int j = 0; j < 8; ++j)
+  for (int j = 0; j < 4; ++j)
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
-      const int c = j * 8 + tq * 2 + e;
+      const int c = ch + j * 8 + tq * 2 + e;
       if (rr < nr && c < nc && r0 + rr >= q0 + c)
         F[(r0 + rr) + static_cast<size_t>(q0 + c) * ld] = G.C[c * kSL64 + rr + shC] - acc[j][e];
     }
@@ -1487,7 +1487,7 @@ void launch_wide_update64(const SnDev& sd, const FactorDev& fd, const int4* tile
   init([] { cudaFuncSetAttribute(k_wide_update64, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes); });
   const int blocks = count > 0 ? count : (nd > 0 ? 1 : 0);
   if (blocks)
-    launch_pdl(k_wide_update64, blocks, 256, bytes, st, pdl, sd, fd, tiles, count, fronts, nd, panel, scr);
+    launch_pdl(k_wide_update64, blocks, 512, bytes, st, pdl, sd, fd, tiles, count, fronts, nd, panel, scr);
 }
 
 void launch_wide_panel_f(const SnDev& sd, const FactorDev& fd, const int4* tasks, int count, int panel,
