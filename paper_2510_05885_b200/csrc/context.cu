@@ -240,10 +240,10 @@ class LdlSystem {
         for (int g = g0; g < g1; ++g) {
           const int nd = T.dg_ptr[g + 1] - T.dg_ptr[g];
           const int np = T.pn_ptr[g + 1] - T.pn_ptr[g];
-          // 64x64 tiles where the update is latency-bound (about one wave of
-          // 32x32 tile CTAs or less: the mesh, -12 us); the 32x32 kernel's
-          // parallelism where it is throughput-bound (elec's 3000-row front:
-          // 64x64 tiles were 0.8 ms slower per Newton step)
+          // 64x64 tiles where the update is latency-bound (up to ~two waves
+          // of 32x32 tile CTAs: the mesh, bearing); the 32x32 kernel's
+          // parallelism where it is throughput-bound (elec's 3000-row front's
+          // early panels)
           const bool t64 = use_t64_ && T.tl_ptr[g + 1] - T.tl_ptr[g] <= kT64MaxTiles;
           const int nt = t64 ? T.tl64_ptr[g + 1] - T.tl64_ptr[g] : T.tl_ptr[g + 1] - T.tl_ptr[g];
           auto rest = [&](cudaStream_t s2, bool pdl, double* sc) {
@@ -1241,7 +1241,10 @@ class LdlSystem {
   bool fused_panel_ = std::getenv("NCL_NO_FUSED_PANEL") == nullptr;
   // the fused path's rest updates as 64x64 tiles (NCL_UPD32=1: 32x32, k_wide_update)
   bool use_t64_ = std::getenv("NCL_UPD32") == nullptr;
-  static constexpr int kT64MaxTiles = 1036;  // 32x32 tiles: 7 CTAs per SM x 148
+  // 32x32 tiles per launch up to which 64x64 tiles are used: ~two waves of
+  // 32x32 tile CTAs (7 per SM x 148); measured: mesh indifferent above 1000,
+  // bearing best near 2000-3000, elec worse above 2000
+  static constexpr int kT64MaxTiles = 2000;
   // NCL_NO_STAGED_GATHER=1 (tests): the mid-front assembly and the tree forward
   // gather take their unstaged fallback paths (more children / entries than
   // the staging buffers hold)
